@@ -1,0 +1,145 @@
+/*
+ * pcbz_b200.h -- C ABI of libpcbz_b200.so, the B200 (sm_100a) implementation
+ * of PC-bzip2's entropy-judgement stage.
+ *
+ * Every entry point mirrors one callable of the reference package `pcbz`
+ * (/root/reference/pkg/src/pcbz, cited below as file:line) so that the
+ * reference's Python API can be backed by this library through ctypes
+ * (see INTEGRATION.md).  Conventions:
+ *   - plain pointers and sizes only, no framework types;
+ *   - return 0 on success, a negative PCBZ_E* code on failure; the message
+ *     of the last failure on the calling thread is pcbz_last_error();
+ *   - "host" entry points take host buffers and are synchronous; they are
+ *     reentrant and may be called from several threads at once (the
+ *     reference calls its kernels from a ThreadPool, criterion.py:165-169);
+ *   - "device" entry points take device pointers and a cudaStream_t (passed
+ *     as void*), are asynchronous and stream-ordered.
+ *   - images are C-contiguous row-major uint16 grids of h rows and w columns.
+ *   - predictor bytes: bit 7 = temporal delta first, bits 0..6 = intra id 0..12
+ *     (core.py:68-80).
+ */
+#ifndef PCBZ_B200_H
+#define PCBZ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCBZ_OK 0
+#define PCBZ_E_INVALID (-1)   /* bad argument: maps to Python ValueError   */
+#define PCBZ_E_CUDA (-2)      /* CUDA runtime failure: RuntimeError         */
+#define PCBZ_E_NODEVICE (-3)  /* no usable sm_100 device: RuntimeError      */
+#define PCBZ_E_INTERNAL (-4)  /* internal invariant broken: RuntimeError    */
+
+#define PCBZ_MAX_CANDIDATES 26
+
+#if defined(__GNUC__)
+#define PCBZ_API __attribute__((visibility("default")))
+#else
+#define PCBZ_API
+#endif
+
+PCBZ_API const char *pcbz_version(void);
+PCBZ_API const char *pcbz_last_error(void);
+/* Number of visible CUDA devices of compute capability 10.x (0 if none). */
+PCBZ_API int pcbz_device_count(void);
+
+/* ---------------------------------------------------------------------
+ * Kernel-level drop-ins (host buffers, synchronous).
+ * ------------------------------------------------------------------- */
+
+/* pcbz._kernels.residual_bwt_pair_hist(img, intra_id, px, py) -> int64[65536]
+ * (_kernels.py:157-204): approximate-BWT byte-pair histogram of the packed
+ * big-endian residual stream of one intra predictor. */
+PCBZ_API int pcbz_residual_bwt_pair_hist(const uint16_t *img, int64_t h, int64_t w, int intra_id,
+                                int64_t px, int64_t py, int64_t *hist_out);
+
+/* pcbz._kernels.residual_image(img, intra_id, px, py) (_kernels.py:46-66). */
+PCBZ_API int pcbz_residual_image(const uint16_t *img, int64_t h, int64_t w, int intra_id,
+                        int64_t px, int64_t py, uint16_t *out);
+
+/* pcbz.predictors.temporal_delta samples (predictors.py:116-120). */
+PCBZ_API int pcbz_temporal_delta(const uint16_t *cur, const uint16_t *prev, int64_t n, uint16_t *out);
+
+/* pcbz._kernels.counting_bwt (_kernels.py:93-113), pair_hist (:116-122),
+ * bwt_pair_hist (:136-154): the composed approximate-BWT route behind
+ * pcbz.criterion.approx_bwt / pair_histogram (criterion.py:43-83). */
+PCBZ_API int pcbz_counting_bwt(const uint8_t *s, int64_t n, uint8_t *out);
+PCBZ_API int pcbz_pair_hist(const uint8_t *s, int64_t n, int64_t *hist_out);
+PCBZ_API int pcbz_bwt_pair_hist(const uint8_t *s, int64_t n, int64_t *hist_out);
+
+/* pcbz.criterion.entropy2d (criterion.py:86-96) of a 65536-bin histogram. */
+PCBZ_API int pcbz_entropy2d(const int64_t *counts, int64_t total, double *out);
+
+/* ---------------------------------------------------------------------
+ * API-level: the entropy judge.
+ * ------------------------------------------------------------------- */
+
+/* pcbz.criterion.select_predictor(frame, prev, candidates) for one frame
+ * (criterion.py:136-173).  `specs` holds k distinct predictor bytes sorted
+ * ascending (the Python layer validates and sorts, criterion.py:145-156);
+ * `prev` may be NULL only if no spec has bit 7 set.  Outputs: ent_out[k]
+ * (entropy of each spec, same order), *selected (argmin over (entropy, byte)),
+ * and, if hist_out != NULL, the k pair histograms hist_out[k][65536]. */
+PCBZ_API int pcbz_select_predictor(const uint16_t *frame, const uint16_t *prev, int64_t h, int64_t w,
+                          int64_t px, int64_t py, const uint8_t *specs, int k,
+                          double *ent_out, uint8_t *selected, int64_t *hist_out);
+
+/* Batched judge + emission over a frame sequence, host buffers: the per-frame
+ * loop of pcbz.pipeline.compress_stack_detailed (pipeline.py:85-108) up to
+ * (but excluding) the bzip2 back end.
+ *   frames     [nframes][h][w]
+ *   halo_prev  previous original frame of frames[0], or NULL
+ *   temporal   0: never score temporal specs; 1: score them on every frame
+ *              that has a previous frame (pipeline.py:67-73,87)
+ *   specs[k]   sorted distinct predictor bytes (the candidate set)
+ * Outputs: ent_out[nframes][k] (NaN where a spec was not scored),
+ * sel_out[nframes], stream_out[nframes][2*h*w] (big-endian residual bytes
+ * of the selected predictor, core.py:228-237) or NULL. */
+PCBZ_API int pcbz_judge_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t nframes,
+                    int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *specs, int k,
+                    int temporal, double *ent_out, uint8_t *sel_out, uint8_t *stream_out);
+
+/* Device-resident form of pcbz_judge_host: all buffers are device pointers,
+ * work is enqueued on `stream` (a cudaStream_t) and nothing synchronises.
+ * `workspace` must hold pcbz_judge_workspace_size(...) bytes. */
+PCBZ_API size_t pcbz_judge_workspace_size(int64_t nframes, int64_t h, int64_t w, int k, int want_hist);
+PCBZ_API int pcbz_judge_device(const uint16_t *d_frames, const uint16_t *d_halo_prev, int64_t nframes,
+                      int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *specs, int k,
+                      int temporal, double *d_ent_out, uint8_t *d_sel_out, uint8_t *d_stream_out,
+                      uint32_t *d_hist_out, void *d_workspace, size_t workspace_bytes,
+                      void *stream);
+
+/* Emission only (pipeline.py:99-101 with a forced predictor): stream_out[f] =
+ * pack_symbols(apply_predictor(frames[f], sel[f], prev)) for every frame,
+ * prev = frames[f-1] (halo_prev for f = 0; must be non-NULL if sel[0] has
+ * bit 7 set). */
+PCBZ_API int pcbz_emit_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t nframes, int64_t h,
+                   int64_t w, int64_t px, int64_t py, const uint8_t *sel, uint8_t *stream_out);
+
+/* Decompression side (reference pipeline.py:121-139, _kernels.py:69-90,
+ * predictors.py:101-147): residuals[f] (native-order uint16 symbol images)
+ * -> original frames, applying the inverse intra prediction of sel[f] and,
+ * when bit 7 is set, the modular undelta against the reconstructed frame f-1
+ * (halo_prev for f = 0). */
+PCBZ_API int pcbz_reconstruct_host(const uint16_t *residuals, const uint16_t *halo_prev, int64_t nframes,
+                          int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *sel,
+                          uint16_t *frames_out);
+
+/* Testing hook: force the number of segments each (frame, candidate) stream
+ * is split into (0 = automatic).  Outputs must not depend on it. */
+PCBZ_API int pcbz_set_segment_override(int segments);
+
+/* Timing of the most recent pcbz_judge_device call on this thread when it was
+ * made with pcbz_set_profiling(1): milliseconds of the histogram kernel and of
+ * the whole judge (CUDA events on the launch stream; synchronises). */
+PCBZ_API int pcbz_set_profiling(int on);
+PCBZ_API int pcbz_last_timing(float *hist_ms, float *total_ms, int *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCBZ_B200_H */

@@ -1,0 +1,103 @@
+"""ctypes binding of libpcbz_b200.so (the C ABI in include/pcbz_b200.h).
+
+There is no CPU fallback: if the shared library or an sm_100 device is
+missing, every compute call raises.  Error codes map to the exceptions the
+reference raises for the same conditions (ValueError for bad arguments,
+RuntimeError for device failures).
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "_native" / "libpcbz_b200.so"
+
+PCBZ_OK = 0
+PCBZ_E_INVALID = -1
+PCBZ_E_CUDA = -2
+PCBZ_E_NODEVICE = -3
+PCBZ_E_INTERNAL = -4
+MAX_CANDIDATES = 26
+
+_c_i64 = ctypes.c_int64
+_c_int = ctypes.c_int
+_c_size = ctypes.c_size_t
+_vp = ctypes.c_void_p
+
+# name -> (restype, argtypes); every symbol include/pcbz_b200.h declares
+SIGNATURES = {
+    "pcbz_version": (ctypes.c_char_p, []),
+    "pcbz_last_error": (ctypes.c_char_p, []),
+    "pcbz_device_count": (_c_int, []),
+    "pcbz_residual_bwt_pair_hist": (_c_int, [_vp, _c_i64, _c_i64, _c_int, _c_i64, _c_i64, _vp]),
+    "pcbz_residual_image": (_c_int, [_vp, _c_i64, _c_i64, _c_int, _c_i64, _c_i64, _vp]),
+    "pcbz_temporal_delta": (_c_int, [_vp, _vp, _c_i64, _vp]),
+    "pcbz_counting_bwt": (_c_int, [_vp, _c_i64, _vp]),
+    "pcbz_pair_hist": (_c_int, [_vp, _c_i64, _vp]),
+    "pcbz_bwt_pair_hist": (_c_int, [_vp, _c_i64, _vp]),
+    "pcbz_entropy2d": (_c_int, [_vp, _c_i64, _vp]),
+    "pcbz_select_predictor": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _c_int,
+                                       _vp, _vp, _vp]),
+    "pcbz_judge_host": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _c_int,
+                                 _c_int, _vp, _vp, _vp]),
+    "pcbz_judge_workspace_size": (_c_size, [_c_i64, _c_i64, _c_i64, _c_int, _c_int]),
+    "pcbz_judge_device": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _c_int,
+                                   _c_int, _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),
+    "pcbz_emit_host": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp]),
+    "pcbz_reconstruct_host": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp,
+                                       _vp]),
+    "pcbz_set_segment_override": (_c_int, [_c_int]),
+    "pcbz_set_profiling": (_c_int, [_c_int]),
+    "pcbz_last_timing": (_c_int, [_vp, _vp, _vp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load(path: Path | str | None = None) -> ctypes.CDLL:
+    """Load (once) and return the native library; raises if it is absent."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            p = Path(path) if path else LIB_PATH
+            if not p.exists():
+                raise ImportError(
+                    f"{p} is missing: build it with `python -m paper_2310_09467_b200.build_native` "
+                    "(there is no CPU fallback for the entropy judge)")
+            lib = ctypes.CDLL(str(p))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def check(rc: int) -> None:
+    """Raise the Python exception matching a PCBZ_E* return code."""
+    if rc == PCBZ_OK:
+        return
+    msg = load().pcbz_last_error().decode(errors="replace")
+    if rc == PCBZ_E_INVALID:
+        raise ValueError(msg)
+    raise RuntimeError(f"libpcbz_b200 error {rc}: {msg}")
+
+
+def ptr(a: np.ndarray | None):
+    """Data pointer of a C-contiguous numpy array (None -> NULL)."""
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"], "native calls need C-contiguous buffers"
+    return a.ctypes.data
+
+
+def version() -> str:
+    return load().pcbz_version().decode()
+
+
+def device_count() -> int:
+    return int(load().pcbz_device_count())

@@ -1,0 +1,550 @@
+// capi.cu -- extern "C" boundary of libpcbz_b200.so (declared in
+// include/pcbz_b200.h).  Host-buffer entry points stage data through a
+// thread-local context (own stream + grow-only device buffers) so they are
+// reentrant, like the reference's nogil kernels called from a ThreadPool
+// (reference criterion.py:165-169, _kernels.py:157).
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/pcbz_b200.h"
+#include "judge.cuh"
+
+using namespace pcbz;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local bool g_profile = false;
+thread_local float g_hist_ms = 0.f, g_total_ms = 0.f;
+thread_local int g_launches = 0;
+thread_local int g_seg_override = 0;
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                    \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(PCBZ_E_CUDA, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_),    \
+                  __FILE__, __LINE__);                                                 \
+  } while (0)
+
+int num_sms_cached() {
+  static int nsm = -1;
+  if (nsm < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) nsm = 148;
+  }
+  return nsm;
+}
+
+int check_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return fail(PCBZ_E_NODEVICE, "no CUDA device visible");
+  int dev = 0, major = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10) return fail(PCBZ_E_NODEVICE, "device %d is sm_%d x, this build is sm_100a", dev, major);
+  static bool configured = false;
+  if (!configured) {
+    CUDA_TRY(judge_configure());
+    configured = true;
+  }
+  return PCBZ_OK;
+}
+
+// grow-only device allocation
+struct DevBuf {
+  void *p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t n) {
+    if (n <= cap) return PCBZ_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(n, 1 << 16);
+    CUDA_TRY(cudaMalloc(&p, want));
+    cap = want;
+    return PCBZ_OK;
+  }
+  template <typename T> T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+struct HostCtx {
+  cudaStream_t stream = nullptr;
+  DevBuf frames, prev, out, ent, sel, stream_out, hist, ws, scratch, bytes;
+  int init() {
+    if (stream) return PCBZ_OK;
+    int rc = check_device();
+    if (rc) return rc;
+    CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    return PCBZ_OK;
+  }
+};
+
+thread_local HostCtx g_ctx;
+
+int validate_geometry(int64_t h, int64_t w, int64_t px, int64_t py) {
+  if (h < 1 || w < 1) return fail(PCBZ_E_INVALID, "frame must contain at least one sample (h=%lld w=%lld)", (long long)h, (long long)w);
+  if (px < 1 || py < 1) return fail(PCBZ_E_INVALID, "pitch must be positive (px=%lld py=%lld)", (long long)px, (long long)py);
+  if (w > 0x7FFFFFFF || h > 0x7FFFFFFF || px > 0x7FFFFFFF || py > 0x7FFFFFFF)
+    return fail(PCBZ_E_INVALID, "dimension exceeds int32");
+  return PCBZ_OK;
+}
+
+int validate_specs(const uint8_t *specs, int k) {
+  if (k < 1 || k > PCBZ_MAX_CANDIDATES) return fail(PCBZ_E_INVALID, "candidate count %d outside [1, %d]", k, PCBZ_MAX_CANDIDATES);
+  for (int i = 0; i < k; ++i) {
+    if ((specs[i] & 0x7F) > 12) return fail(PCBZ_E_INVALID, "invalid intra predictor id %d in byte 0x%02X", specs[i] & 0x7F, specs[i]);
+    if (i && specs[i] <= specs[i - 1]) return fail(PCBZ_E_INVALID, "candidate bytes must be distinct and sorted ascending");
+  }
+  return PCBZ_OK;
+}
+
+// Work decomposition: segments per pair so that the persistent grid sees
+// about two waves of items, while no segment exceeds kMaxSegPixels.
+int choose_segments(int64_t npairs, int64_t npix, bool want_hist) {
+  const int64_t nsm = num_sms_cached();
+  int64_t s = (2 * nsm + npairs - 1) / npairs;
+  const int64_t max_by_len = std::max<int64_t>(1, npix / (64 * kJudgeThreads));
+  s = std::min(s, max_by_len);
+  s = std::max<int64_t>(s, (npix + kMaxSegPixels - 1) / kMaxSegPixels);
+  if (s > 4096) s = 4096;
+  (void)want_hist;
+  return (int)std::max<int64_t>(1, s);
+}
+
+struct Plan {
+  JudgeParams jp{};
+  int grid = 0;
+  size_t ws_bytes = 0;
+  size_t off_counter = 0, off_err = 0, off_fscratch = 0, off_segsum = 0, off_ghist = 0;
+};
+
+int build_lists(const uint8_t *specs, int k, bool halo, int temporal, CandLists &cl) {
+  memset(&cl, 0, sizeof cl);
+  cl.k = k;
+  for (int i = 0; i < k; ++i) {
+    const bool t = specs[i] & 0x80;
+    if (!t || (temporal && halo)) { cl.byteA[cl.kA] = specs[i]; cl.idxA[cl.kA++] = (uint8_t)i; }
+    if (!t || temporal) { cl.byteB[cl.kB] = specs[i]; cl.idxB[cl.kB++] = (uint8_t)i; }
+  }
+  if (cl.kA == 0) return fail(PCBZ_E_INVALID, "no usable candidate for a frame without a previous frame");
+  return PCBZ_OK;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int make_plan(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *specs,
+              int k, bool halo, int temporal, bool want_hist, Plan &pl) {
+  int rc = validate_geometry(h, w, px, py);
+  if (rc) return rc;
+  rc = validate_specs(specs, k);
+  if (rc) return rc;
+  if (nframes < 1) return fail(PCBZ_E_INVALID, "at least one frame is required");
+  JudgeParams &jp = pl.jp;
+  rc = build_lists(specs, k, halo, temporal, jp.cl);
+  if (rc) return rc;
+  jp.nframes = nframes;
+  jp.npix = h * w;
+  jp.H = (int)h; jp.W = (int)w; jp.px = (int)px; jp.py = (int)py;
+  jp.npairs = jp.cl.kA + (nframes - 1) * jp.cl.kB;
+  jp.S = g_seg_override > 0 ? (int)std::min<int64_t>(g_seg_override, jp.npix)
+                            : choose_segments(jp.npairs, jp.npix, want_hist);
+  if ((jp.npix + jp.S - 1) / jp.S > kMaxSegPixels)
+    return fail(PCBZ_E_INVALID, "segment override %d leaves segments above %lld pixels", jp.S,
+                (long long)kMaxSegPixels);
+  jp.direct = (jp.S == 1 && !want_hist) ? 1 : 0;
+  const int64_t items = jp.npairs * jp.S;
+  pl.grid = (int)std::min<int64_t>(items, num_sms_cached());
+  size_t off = 0;
+  pl.off_counter = off; off = align_up(off + 4);
+  pl.off_err = off; off = align_up(off + 4);
+  pl.off_fscratch = off; off = align_up(off + (size_t)pl.grid * kJudgeThreads * 256);
+  if (!jp.direct) {
+    pl.off_segsum = off; off = align_up(off + (size_t)nframes * k * jp.S * 512 * sizeof(int16_t));
+    pl.off_ghist = off; off = align_up(off + (want_hist ? 0 : (size_t)nframes * k * 65536 * 4));
+  }
+  pl.ws_bytes = off;
+  return PCBZ_OK;
+}
+
+// Enqueue the whole judge (+ optional emission) on `st`.
+int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double *d_ent,
+             uint8_t *d_sel, uint8_t *d_stream, uint32_t *d_hist, void *d_ws, cudaStream_t st) {
+  JudgeParams &jp = pl.jp;
+  char *ws = static_cast<char *>(d_ws);
+  jp.frames = d_frames;
+  jp.halo = d_halo;
+  jp.ent = d_ent;
+  jp.counter = reinterpret_cast<int *>(ws + pl.off_counter);
+  jp.err = reinterpret_cast<int *>(ws + pl.off_err);
+  jp.fscratch = reinterpret_cast<uint8_t *>(ws + pl.off_fscratch);
+  if (!jp.direct) {
+    jp.segsum = reinterpret_cast<int16_t *>(ws + pl.off_segsum);
+    jp.ghist = d_hist ? d_hist : reinterpret_cast<uint32_t *>(ws + pl.off_ghist);
+  }
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+  if (g_profile) {
+    cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
+    cudaEventRecord(e0, st);
+  }
+  int launches = 0;
+  CUDA_TRY(cudaMemsetAsync(ws, 0, pl.off_fscratch, st));   // counter + err
+  CUDA_TRY(cudaMemsetAsync(d_ent, 0xFF, (size_t)jp.nframes * jp.cl.k * sizeof(double), st));  // NaN
+  if (!jp.direct)
+    CUDA_TRY(cudaMemsetAsync(jp.ghist, 0, (size_t)jp.nframes * jp.cl.k * 65536 * 4, st));
+  CUDA_TRY(launch_judge(jp, pl.grid, st));
+  ++launches;
+  if (g_profile) cudaEventRecord(e1, st);
+  if (!jp.direct) { CUDA_TRY(launch_finalize(jp, st)); ++launches; }
+  CUDA_TRY(launch_select(jp, d_sel, st));
+  ++launches;
+  if (d_stream) {
+    EmitParams ep{d_frames, d_halo, jp.nframes, jp.npix, jp.H, jp.W, jp.px, jp.py, d_sel, d_stream};
+    CUDA_TRY(launch_emit(ep, st));
+    ++launches;
+  }
+  g_launches = launches;
+  if (g_profile) {
+    cudaEventRecord(e2, st);
+    cudaEventSynchronize(e2);
+    cudaEventElapsedTime(&g_hist_ms, e0, e1);
+    cudaEventElapsedTime(&g_total_ms, e0, e2);
+    cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
+  }
+  return PCBZ_OK;
+}
+
+int check_err_flag(const Plan &pl, void *d_ws, cudaStream_t st) {
+  int flag = 0;
+  CUDA_TRY(cudaMemcpyAsync(&flag, static_cast<char *>(d_ws) + pl.off_err, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (flag) return fail(PCBZ_E_INTERNAL, "judge kernel reported internal error %d", flag);
+  return PCBZ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *pcbz_version(void) { return "pcbz_b200 0.1.0 sm_100a"; }
+
+const char *pcbz_last_error(void) { return g_err.c_str(); }
+
+int pcbz_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  int good = 0;
+  for (int d = 0; d < n; ++d) {
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d);
+    good += major == 10;
+  }
+  return good;
+}
+
+int pcbz_set_profiling(int on) {
+  g_profile = on != 0;
+  return PCBZ_OK;
+}
+
+int pcbz_last_timing(float *hist_ms, float *total_ms, int *launches) {
+  if (hist_ms) *hist_ms = g_hist_ms;
+  if (total_ms) *total_ms = g_total_ms;
+  if (launches) *launches = g_launches;
+  return PCBZ_OK;
+}
+
+size_t pcbz_judge_workspace_size(int64_t nframes, int64_t h, int64_t w, int k, int want_hist) {
+  std::vector<uint8_t> specs(std::max(k, 1));
+  for (int i = 0; i < k; ++i) specs[i] = (uint8_t)i;  // shape-only plan
+  Plan pl;
+  if (make_plan(nframes, h, w, 1, 1, specs.data(), k, true, 1, want_hist != 0, pl)) return 0;
+  return pl.ws_bytes;
+}
+
+int pcbz_judge_device(const uint16_t *d_frames, const uint16_t *d_halo_prev, int64_t nframes,
+                      int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *specs, int k,
+                      int temporal, double *d_ent_out, uint8_t *d_sel_out, uint8_t *d_stream_out,
+                      uint32_t *d_hist_out, void *d_workspace, size_t workspace_bytes,
+                      void *stream) {
+  int rc = check_device();
+  if (rc) return rc;
+  Plan pl;
+  rc = make_plan(nframes, h, w, px, py, specs, k, d_halo_prev != nullptr, temporal,
+                 d_hist_out != nullptr, pl);
+  if (rc) return rc;
+  if (workspace_bytes < pl.ws_bytes)
+    return fail(PCBZ_E_INVALID, "workspace too small: %zu < %zu bytes", workspace_bytes, pl.ws_bytes);
+  return run_plan(pl, d_frames, d_halo_prev, d_ent_out, d_sel_out, d_stream_out, d_hist_out,
+                  d_workspace, static_cast<cudaStream_t>(stream));
+}
+
+int pcbz_judge_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t nframes, int64_t h,
+                    int64_t w, int64_t px, int64_t py, const uint8_t *specs, int k, int temporal,
+                    double *ent_out, uint8_t *sel_out, uint8_t *stream_out) {
+  HostCtx &c = g_ctx;
+  int rc = c.init();
+  if (rc) return rc;
+  Plan pl;
+  rc = make_plan(nframes, h, w, px, py, specs, k, halo_prev != nullptr, temporal, false, pl);
+  if (rc) return rc;
+  const size_t fbytes = (size_t)nframes * h * w * 2;
+  if ((rc = c.frames.ensure(fbytes)) || (rc = c.ent.ensure((size_t)nframes * k * 8)) ||
+      (rc = c.sel.ensure((size_t)nframes)) || (rc = c.ws.ensure(pl.ws_bytes)))
+    return rc;
+  if (halo_prev && (rc = c.prev.ensure((size_t)h * w * 2))) return rc;
+  if (stream_out && (rc = c.stream_out.ensure(fbytes))) return rc;
+  cudaStream_t st = c.stream;
+  CUDA_TRY(cudaMemcpyAsync(c.frames.p, frames, fbytes, cudaMemcpyHostToDevice, st));
+  if (halo_prev) CUDA_TRY(cudaMemcpyAsync(c.prev.p, halo_prev, (size_t)h * w * 2, cudaMemcpyHostToDevice, st));
+  rc = run_plan(pl, c.frames.as<uint16_t>(), halo_prev ? c.prev.as<uint16_t>() : nullptr,
+                c.ent.as<double>(), c.sel.as<uint8_t>(), stream_out ? c.stream_out.as<uint8_t>() : nullptr,
+                nullptr, c.ws.p, st);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(ent_out, c.ent.p, (size_t)nframes * k * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(sel_out, c.sel.p, (size_t)nframes, cudaMemcpyDeviceToHost, st));
+  if (stream_out) CUDA_TRY(cudaMemcpyAsync(stream_out, c.stream_out.p, fbytes, cudaMemcpyDeviceToHost, st));
+  return check_err_flag(pl, c.ws.p, st);
+}
+
+int pcbz_select_predictor(const uint16_t *frame, const uint16_t *prev, int64_t h, int64_t w,
+                          int64_t px, int64_t py, const uint8_t *specs, int k, double *ent_out,
+                          uint8_t *selected, int64_t *hist_out) {
+  bool any_temporal = false;
+  for (int i = 0; i < k; ++i) any_temporal |= (specs[i] & 0x80) != 0;
+  if (any_temporal && !prev) return fail(PCBZ_E_INVALID, "temporal candidate given but no previous frame");
+  HostCtx &c = g_ctx;
+  int rc = c.init();
+  if (rc) return rc;
+  // the previous frame rides as the "halo" of a one-frame sequence, so every
+  // candidate (temporal ones included) is scored on frame 0 only
+  const int64_t nfr = 1;
+  Plan pl;
+  rc = make_plan(nfr, h, w, px, py, specs, k, prev != nullptr, 1, hist_out != nullptr, pl);
+  if (rc) return rc;
+  const size_t fb = (size_t)h * w * 2;
+  if ((rc = c.frames.ensure(fb)) || (rc = c.ent.ensure((size_t)k * 8)) ||
+      (rc = c.sel.ensure(1)) || (rc = c.ws.ensure(pl.ws_bytes)))
+    return rc;
+  if (prev && (rc = c.prev.ensure(fb))) return rc;
+  if (hist_out && (rc = c.hist.ensure((size_t)k * 65536 * 4))) return rc;
+  cudaStream_t st = c.stream;
+  if (prev) CUDA_TRY(cudaMemcpyAsync(c.prev.p, prev, fb, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c.frames.p, frame, fb, cudaMemcpyHostToDevice, st));
+  rc = run_plan(pl, c.frames.as<uint16_t>(), prev ? c.prev.as<uint16_t>() : nullptr,
+                c.ent.as<double>(), c.sel.as<uint8_t>(), nullptr,
+                hist_out ? c.hist.as<uint32_t>() : nullptr, c.ws.p, st);
+  if (rc) return rc;
+  std::vector<double> ent((size_t)nfr * k);
+  std::vector<uint8_t> sel(nfr);
+  CUDA_TRY(cudaMemcpyAsync(ent.data(), c.ent.p, ent.size() * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(sel.data(), c.sel.p, nfr, cudaMemcpyDeviceToHost, st));
+  std::vector<uint32_t> h32;
+  if (hist_out) {
+    h32.resize((size_t)k * 65536);
+    CUDA_TRY(cudaMemcpyAsync(h32.data(), c.hist.as<uint32_t>() + (size_t)(nfr - 1) * k * 65536,
+                             h32.size() * 4, cudaMemcpyDeviceToHost, st));
+  }
+  rc = check_err_flag(pl, c.ws.p, st);
+  if (rc) return rc;
+  memcpy(ent_out, ent.data() + (size_t)(nfr - 1) * k, (size_t)k * 8);
+  *selected = sel[nfr - 1];
+  if (hist_out)
+    for (size_t i = 0; i < h32.size(); ++i) hist_out[i] = h32[i];
+  return PCBZ_OK;
+}
+
+int pcbz_residual_bwt_pair_hist(const uint16_t *img, int64_t h, int64_t w, int intra_id,
+                                int64_t px, int64_t py, int64_t *hist_out) {
+  if (intra_id < 0 || intra_id > 12) return fail(PCBZ_E_INVALID, "intra predictor id must be in [0, 12], got %d", intra_id);
+  const uint8_t spec = (uint8_t)intra_id;
+  double ent = 0;
+  uint8_t sel = 0;
+  return pcbz_select_predictor(img, nullptr, h, w, px, py, &spec, 1, &ent, &sel, hist_out);
+}
+
+int pcbz_residual_image(const uint16_t *img, int64_t h, int64_t w, int intra_id, int64_t px,
+                        int64_t py, uint16_t *out) {
+  int rc = validate_geometry(h, w, px, py);
+  if (rc) return rc;
+  if (intra_id < 0 || intra_id > 12) return fail(PCBZ_E_INVALID, "intra predictor id must be in [0, 12], got %d", intra_id);
+  HostCtx &c = g_ctx;
+  if ((rc = c.init())) return rc;
+  const size_t nb = (size_t)h * w * 2;
+  if ((rc = c.frames.ensure(nb)) || (rc = c.out.ensure(nb))) return rc;
+  cudaStream_t st = c.stream;
+  CUDA_TRY(cudaMemcpyAsync(c.frames.p, img, nb, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_residual_image(c.frames.as<uint16_t>(), nullptr, h, w, intra_id, (int)px, (int)py,
+                                 c.out.as<uint16_t>(), 0, st));
+  CUDA_TRY(cudaMemcpyAsync(out, c.out.p, nb, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return PCBZ_OK;
+}
+
+int pcbz_temporal_delta(const uint16_t *cur, const uint16_t *prev, int64_t n, uint16_t *out) {
+  if (n < 0) return fail(PCBZ_E_INVALID, "negative length");
+  if (n == 0) return PCBZ_OK;
+  HostCtx &c = g_ctx;
+  int rc = c.init();
+  if (rc) return rc;
+  const size_t nb = (size_t)n * 2;
+  if ((rc = c.frames.ensure(nb)) || (rc = c.prev.ensure(nb)) || (rc = c.out.ensure(nb))) return rc;
+  cudaStream_t st = c.stream;
+  CUDA_TRY(cudaMemcpyAsync(c.frames.p, cur, nb, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c.prev.p, prev, nb, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_temporal_delta(c.frames.as<uint16_t>(), c.prev.as<uint16_t>(), n, c.out.as<uint16_t>(), st));
+  CUDA_TRY(cudaMemcpyAsync(out, c.out.p, nb, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return PCBZ_OK;
+}
+
+int pcbz_counting_bwt(const uint8_t *s, int64_t n, uint8_t *out) {
+  if (n < 0) return fail(PCBZ_E_INVALID, "negative length");
+  if (n == 0) return PCBZ_OK;
+  HostCtx &c = g_ctx;
+  int rc = c.init();
+  if (rc) return rc;
+  const size_t sw = counting_bwt_scratch_words(n);
+  if ((rc = c.bytes.ensure((size_t)n)) || (rc = c.out.ensure((size_t)n)) || (rc = c.scratch.ensure(sw * 4))) return rc;
+  cudaStream_t st = c.stream;
+  CUDA_TRY(cudaMemcpyAsync(c.bytes.p, s, (size_t)n, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_counting_bwt(c.bytes.as<uint8_t>(), n, c.out.as<uint8_t>(), c.scratch.as<uint32_t>(), sw, st));
+  CUDA_TRY(cudaMemcpyAsync(out, c.out.p, (size_t)n, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return PCBZ_OK;
+}
+
+static int pair_hist_dev(HostCtx &c, const uint8_t *d_s, int64_t n, int64_t *hist_out) {
+  int rc = c.hist.ensure(65536 * 4);
+  if (rc) return rc;
+  cudaStream_t st = c.stream;
+  CUDA_TRY(cudaMemsetAsync(c.hist.p, 0, 65536 * 4, st));
+  if (n >= 2) CUDA_TRY(launch_pair_hist(d_s, n, c.hist.as<uint32_t>(), st));
+  std::vector<uint32_t> h32(65536);
+  CUDA_TRY(cudaMemcpyAsync(h32.data(), c.hist.p, 65536 * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (int i = 0; i < 65536; ++i) hist_out[i] = h32[i];
+  return PCBZ_OK;
+}
+
+int pcbz_pair_hist(const uint8_t *s, int64_t n, int64_t *hist_out) {
+  if (n < 0) return fail(PCBZ_E_INVALID, "negative length");
+  HostCtx &c = g_ctx;
+  int rc = c.init();
+  if (rc) return rc;
+  if ((rc = c.bytes.ensure((size_t)std::max<int64_t>(n, 1)))) return rc;
+  if (n) CUDA_TRY(cudaMemcpyAsync(c.bytes.p, s, (size_t)n, cudaMemcpyHostToDevice, c.stream));
+  return pair_hist_dev(c, c.bytes.as<uint8_t>(), n, hist_out);
+}
+
+int pcbz_bwt_pair_hist(const uint8_t *s, int64_t n, int64_t *hist_out) {
+  if (n < 0) return fail(PCBZ_E_INVALID, "negative length");
+  HostCtx &c = g_ctx;
+  int rc = c.init();
+  if (rc) return rc;
+  if (n < 2) {
+    for (int i = 0; i < 65536; ++i) hist_out[i] = 0;
+    return PCBZ_OK;
+  }
+  const size_t sw = counting_bwt_scratch_words(n);
+  if ((rc = c.bytes.ensure((size_t)n)) || (rc = c.out.ensure((size_t)n)) || (rc = c.scratch.ensure(sw * 4))) return rc;
+  cudaStream_t st = c.stream;
+  CUDA_TRY(cudaMemcpyAsync(c.bytes.p, s, (size_t)n, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_counting_bwt(c.bytes.as<uint8_t>(), n, c.out.as<uint8_t>(), c.scratch.as<uint32_t>(), sw, st));
+  return pair_hist_dev(c, c.out.as<uint8_t>(), n, hist_out);
+}
+
+int pcbz_entropy2d(const int64_t *counts, int64_t total, double *out) {
+  HostCtx &c = g_ctx;
+  int rc = c.init();
+  if (rc) return rc;
+  if ((rc = c.hist.ensure(65536 * 8)) || (rc = c.ent.ensure(8))) return rc;
+  cudaStream_t st = c.stream;
+  CUDA_TRY(cudaMemcpyAsync(c.hist.p, counts, 65536 * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_entropy_u64(c.hist.as<uint64_t>(), total > 0 ? (double)total : 0.0, c.ent.as<double>(), st));
+  CUDA_TRY(cudaMemcpyAsync(out, c.ent.p, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return PCBZ_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int pcbz_set_segment_override(int segments) {
+  g_seg_override = segments > 0 ? segments : 0;
+  return PCBZ_OK;
+}
+
+static int check_sel(const uint8_t *sel, int64_t nframes, bool halo) {
+  for (int64_t f = 0; f < nframes; ++f) {
+    if ((sel[f] & 0x7F) > 12) return fail(PCBZ_E_INVALID, "invalid intra predictor id %d in byte 0x%02X", sel[f] & 0x7F, sel[f]);
+    if (f == 0 && !halo && (sel[f] & 0x80)) return fail(PCBZ_E_INVALID, "temporal predictor requires a previous frame");
+  }
+  return PCBZ_OK;
+}
+
+int pcbz_emit_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t nframes, int64_t h,
+                   int64_t w, int64_t px, int64_t py, const uint8_t *sel, uint8_t *stream_out) {
+  int rc = validate_geometry(h, w, px, py);
+  if (rc) return rc;
+  if (nframes < 1) return fail(PCBZ_E_INVALID, "at least one frame is required");
+  if ((rc = check_sel(sel, nframes, halo_prev != nullptr))) return rc;
+  HostCtx &c = g_ctx;
+  if ((rc = c.init())) return rc;
+  const size_t fb = (size_t)nframes * h * w * 2;
+  if ((rc = c.frames.ensure(fb)) || (rc = c.stream_out.ensure(fb)) || (rc = c.sel.ensure(nframes))) return rc;
+  if (halo_prev && (rc = c.prev.ensure((size_t)h * w * 2))) return rc;
+  cudaStream_t st = c.stream;
+  CUDA_TRY(cudaMemcpyAsync(c.frames.p, frames, fb, cudaMemcpyHostToDevice, st));
+  if (halo_prev) CUDA_TRY(cudaMemcpyAsync(c.prev.p, halo_prev, (size_t)h * w * 2, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c.sel.p, sel, (size_t)nframes, cudaMemcpyHostToDevice, st));
+  EmitParams ep{c.frames.as<uint16_t>(), halo_prev ? c.prev.as<uint16_t>() : nullptr, nframes,
+                h * w, (int)h, (int)w, (int)px, (int)py, c.sel.as<uint8_t>(), c.stream_out.as<uint8_t>()};
+  CUDA_TRY(launch_emit(ep, st));
+  CUDA_TRY(cudaMemcpyAsync(stream_out, c.stream_out.p, fb, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return PCBZ_OK;
+}
+
+int pcbz_reconstruct_host(const uint16_t *residuals, const uint16_t *halo_prev, int64_t nframes,
+                          int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *sel,
+                          uint16_t *frames_out) {
+  int rc = validate_geometry(h, w, px, py);
+  if (rc) return rc;
+  if (nframes < 1) return fail(PCBZ_E_INVALID, "at least one frame is required");
+  if ((rc = check_sel(sel, nframes, halo_prev != nullptr))) return rc;
+  HostCtx &c = g_ctx;
+  if ((rc = c.init())) return rc;
+  const size_t fb = (size_t)nframes * h * w * 2;
+  if ((rc = c.frames.ensure(fb)) || (rc = c.out.ensure(fb)) || (rc = c.sel.ensure(nframes))) return rc;
+  if (halo_prev && (rc = c.prev.ensure((size_t)h * w * 2))) return rc;
+  cudaStream_t st = c.stream;
+  CUDA_TRY(cudaMemcpyAsync(c.frames.p, residuals, fb, cudaMemcpyHostToDevice, st));
+  if (halo_prev) CUDA_TRY(cudaMemcpyAsync(c.prev.p, halo_prev, (size_t)h * w * 2, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c.sel.p, sel, (size_t)nframes, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_reconstruct(c.frames.as<uint16_t>(), halo_prev ? c.prev.as<uint16_t>() : nullptr,
+                              nframes, h, w, (int)px, (int)py, c.sel.as<uint8_t>(), c.out.as<uint16_t>(), st));
+  CUDA_TRY(cudaMemcpyAsync(frames_out, c.out.p, fb, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return PCBZ_OK;
+}
+
+}  // extern "C"

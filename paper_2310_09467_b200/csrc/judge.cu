@@ -1,0 +1,584 @@
+// judge.cu -- sm_100a kernels of the entropy-judgement stage.
+//
+// Semantics follow the reference's fused kernel residual_bwt_pair_hist
+// (pkg/src/pcbz/_kernels.py:157-204) and criterion.select_predictor
+// (criterion.py:136-173); the parallel decomposition is new:
+//
+//   * the packed residual stream of one (frame, candidate) pair is cut into
+//     segments; one CTA owns a segment, each of its 192 threads owns a
+//     contiguous run of pixels and runs the reference's per-key chain
+//     automaton (_kernels.py:192-201) on it with a lane-private last-pred
+//     table in shared memory (no cross-lane communication in the hot loop);
+//   * pair increments go to a CTA-private 65,536-bin histogram of packed u16
+//     counters in shared memory (128 KiB); a bin that reaches 0x8000 spills
+//     0x8000 into a small list, so no count is ever lost;
+//   * runs are stitched in stream order through their (first, last) pred per
+//     key -- the associative segment summary of SURVEY.md Appendix A -- first
+//     inside the CTA, then across segments in judge_finalize_kernel;
+//   * the bucket seams of _stitch_buckets (_kernels.py:125-133) close the
+//     histogram, and the fp64 entropy (criterion.py:86-96) is reduced in a
+//     fixed order by every path, so identical histograms give identical bits.
+#include "judge.cuh"
+
+#include <cub/device/device_scan.cuh>
+
+namespace pcbz {
+
+// ---------------------------------------------------------------------------
+// residuals
+// ---------------------------------------------------------------------------
+
+// Source sample: the frame itself or, for temporal candidates, the modular
+// delta against the previous original frame (predictors.py:116-120).
+__device__ __forceinline__ int sample_at(const uint16_t *__restrict__ s,
+                                         const uint16_t *__restrict__ p, int64_t idx) {
+  int v = __ldg(s + idx);
+  if (p) v = (v - (int)__ldg(p + idx)) & 0xFFFF;
+  return v;
+}
+
+// f1..f4 on a neighbour triple; '>> 1' on int32 is floor division for any
+// sign, as in the reference (_kernels.py:5-7,31-43).
+__device__ __forceinline__ int predict_f(int a, int b, int c, int f) {
+  switch (f) {
+    case 1: return a + b - c;
+    case 2: return a + ((b - c) >> 1);
+    case 3: return b + ((a - c) >> 1);
+    default: return (a + b) >> 1;
+  }
+}
+
+__device__ __forceinline__ int predict_at(const uint16_t *s, const uint16_t *p, int W, int y, int x,
+                                          int sx, int sy, int f) {
+  const int64_t row = (int64_t)y * W;
+  const bool left = x >= sx, top = y >= sy;
+  const int a = left ? sample_at(s, p, row + x - sx) : 0;
+  const int b = top ? sample_at(s, p, row - (int64_t)sy * W + x) : 0;
+  const int c = (left && top) ? sample_at(s, p, row - (int64_t)sy * W + x - sx) : 0;
+  return predict_f(a, b, c, f);
+}
+
+// One residual symbol (_kernels.py:60-65, 179-186).
+__device__ __forceinline__ uint32_t residual_at(const uint16_t *s, const uint16_t *p, int W, int y,
+                                                int x, const PredCfg &c) {
+  const int X = sample_at(s, p, (int64_t)y * W + x);
+  if (c.grp < 0) return (uint32_t)X;
+  int pr = predict_at(s, p, W, y, x, c.sx, c.sy, c.f);
+  if (c.grp == 2) pr = (pr + predict_at(s, p, W, y, x, 1, 1, c.f)) >> 1;
+  return (uint32_t)(X - pr) & 0xFFFFu;
+}
+
+// ---------------------------------------------------------------------------
+// shared histogram of packed u16 counters with spill list
+// ---------------------------------------------------------------------------
+
+struct SmemHist {
+  uint32_t *bins;    // kHistWords
+  uint32_t *spill;   // kSpillCap
+  int *nspill;
+  int *err;
+
+  // Add 1 to `bin`.  Exactly one increment observes the 0x7FFF -> 0x8000
+  // crossing of a counter (adds are +1 and the only subtraction is made by
+  // that observer), so each crossing spills once and a half never exceeds
+  // 0x8000 + (increments in flight), far below 0xFFFF.
+  __device__ __forceinline__ void inc(uint32_t bin) const {
+    const uint32_t sh = (bin & 1u) << 4;
+    const uint32_t old = atomicAdd(&bins[bin >> 1], 1u << sh);
+    if (((old >> sh) & 0xFFFFu) == kSpill - 1) spill_one(bin, sh);
+  }
+  __device__ __noinline__ void spill_one(uint32_t bin, uint32_t sh) const {
+    atomicSub(&bins[bin >> 1], kSpill << sh);
+    const int i = atomicAdd(nspill, 1);
+    if (i < kSpillCap) spill[i] = bin;
+    else atomicExch(err, 2);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// deterministic fp64 entropy: -sum p*log2(p), p = c / total (criterion.py:86-96)
+// ---------------------------------------------------------------------------
+
+// All entropy reductions run with kEntropyThreads threads, bin b handled by
+// thread b % kEntropyThreads in ascending order, then a fixed xor-tree per
+// warp and an in-order sum over warps: the same histogram always yields the
+// same double, whichever kernel produced it.
+template <typename Get>
+__device__ double block_entropy(Get get, double total, double *red) {
+  double acc = 0.0;
+  if (total > 0.0) {
+    for (int b = threadIdx.x; b < 65536; b += kEntropyThreads) {
+      const double c = get(b);
+      if (c > 0.0) {
+        const double p = c / total;
+        acc += p * log2(p);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < kEntropyThreads / 32; ++w) s += red[w];
+  __syncthreads();
+  return -s;
+}
+
+// ---------------------------------------------------------------------------
+// pair -> (frame, candidate) mapping
+// ---------------------------------------------------------------------------
+
+struct PairRef {
+  int64_t frame;
+  int spec;   // predictor byte
+  int64_t slot;   // frame * k + index in the full list
+};
+
+__device__ __forceinline__ PairRef pair_ref(const JudgeParams &P, int64_t pair) {
+  PairRef r;
+  if (pair < P.cl.kA) {
+    r.frame = 0;
+    r.spec = P.cl.byteA[pair];
+    r.slot = P.cl.idxA[pair];
+  } else {
+    const int64_t q = pair - P.cl.kA;
+    r.frame = 1 + q / P.cl.kB;
+    const int j = (int)(q % P.cl.kB);
+    r.spec = P.cl.byteB[j];
+    r.slot = r.frame * P.cl.k + P.cl.idxB[j];
+  }
+  return r;
+}
+
+__device__ __forceinline__ const uint16_t *prev_of(const uint16_t *frames, const uint16_t *halo,
+                                                   int64_t npix, int64_t frame) {
+  return frame > 0 ? frames + (frame - 1) * npix : halo;
+}
+
+// ---------------------------------------------------------------------------
+// the judge kernel: one CTA per (pair, segment) item, dynamically scheduled
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const JudgeParams P) {
+  extern __shared__ uint4 smem_raw[];
+  uint32_t *hist_w = reinterpret_cast<uint32_t *>(smem_raw);
+  uint32_t *last_w = hist_w + kHistWords;                 // [kLastWords][kJudgeThreads]
+  uint32_t *spill_w = last_w + kLastWords * kJudgeThreads;
+  __shared__ int s_item, s_nspill;
+  __shared__ double s_red[kJudgeThreads / 32];
+  // after the stitch the last-pred tables are dead: words [0, 2048) become the
+  // spilled-bin bitmap, [2048, 2560) the CTA's first/last pred per key
+  int *s_first = reinterpret_cast<int *>(last_w) + 2048;
+  int *s_last = s_first + 256;
+
+  const int tid = threadIdx.x;
+  const int64_t nitems = P.npairs * P.S;
+  const SmemHist H{hist_w, spill_w, &s_nspill, P.err};
+  uint8_t *Fcta = P.fscratch + (size_t)blockIdx.x * kJudgeThreads * 256;
+  uint8_t *Flane = Fcta + (size_t)tid * 256;
+  uint32_t *Llane = last_w + tid;
+
+  for (;;) {
+    if (tid == 0) {
+      s_item = atomicAdd(P.counter, 1);
+      s_nspill = 0;
+    }
+    uint4 *h4 = reinterpret_cast<uint4 *>(hist_w);
+    for (int i = tid; i < kHistWords / 4; i += kJudgeThreads) h4[i] = make_uint4(0, 0, 0, 0);
+    for (int w = 0; w < kLastWords; ++w) Llane[w * kJudgeThreads] = kUnseen | (kUnseen << 16);
+    __syncthreads();
+    const int64_t item = s_item;
+    if (item >= nitems) break;
+
+    const int64_t pair = item / P.S;
+    const int seg = (int)(item % P.S);
+    const PairRef pr = pair_ref(P, pair);
+    const uint16_t *src = P.frames + pr.frame * P.npix;
+    const uint16_t *prv = (pr.spec & 0x80) ? prev_of(P.frames, P.halo, P.npix, pr.frame) : nullptr;
+    const PredCfg cfg = make_cfg(pr.spec & 0x7F, P.px, P.py);
+    const int W = P.W;
+
+    // ---- this lane's run of pixels [a, b) -----------------------------------
+    const int64_t sb = P.npix * seg / P.S, se = P.npix * (seg + 1) / P.S;
+    const int64_t len = se - sb;
+    const int64_t a = sb + len * tid / kJudgeThreads;
+    const int64_t b = sb + len * (tid + 1) / kJudgeThreads;
+    if (a < b) {
+      // predecessor of the run's first byte: low byte of pixel a-1, or of the
+      // last pixel for the stream's wrap-around (_kernels.py:172-190)
+      const int64_t q = a > 0 ? a - 1 : P.npix - 1;
+      uint32_t prev_lo = residual_at(src, prv, W, (int)(q / W), (int)(q % W), cfg) & 0xFFu;
+      int y = (int)(a / W), x = (int)(a % W);
+      for (int64_t k = a; k < b; ++k) {
+        const uint32_t r = residual_at(src, prv, W, y, x, cfg);
+        const uint32_t hi = r >> 8, lo = r & 0xFFu;
+        // two stream bytes -> two chain events (key, pred) (_kernels.py:192-201)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint32_t key = e == 0 ? hi : lo;
+          const uint32_t pred = e == 0 ? prev_lo : hi;
+          uint32_t *wp = Llane + (key >> 1) * kJudgeThreads;
+          const uint32_t sh = (key & 1u) << 4;
+          const uint32_t wv = *wp;
+          const uint32_t last = (wv >> sh) & 0xFFFFu;
+          *wp = (wv & ~(0xFFFFu << sh)) | (pred << sh);
+          if (last == kUnseen) Flane[key] = (uint8_t)pred;
+          else H.inc((last << 8) | pred);
+        }
+        prev_lo = lo;
+        if (++x == W) { x = 0; ++y; }
+      }
+    }
+    __syncthreads();
+
+    // ---- stitch the 192 runs in stream order (segment-summary combine) -------
+    int my_first[2] = {-1, -1}, my_last[2] = {-1, -1};
+    for (int v = tid; v < 256; v += kJudgeThreads) {
+      int carried = -1, first = -1;
+      const uint32_t *col = last_w + (v >> 1) * kJudgeThreads;
+      const uint32_t sh = (v & 1) << 4;
+      for (int j = 0; j < kJudgeThreads; ++j) {
+        const uint32_t e = (col[j] >> sh) & 0xFFFFu;
+        const uint32_t f = Fcta[(size_t)j * 256 + v];
+        if (e != kUnseen) {
+          if (carried >= 0) H.inc(((uint32_t)carried << 8) | f);
+          else first = (int)f;
+          carried = (int)e;
+        }
+      }
+      my_first[v >= kJudgeThreads] = first;
+      my_last[v >= kJudgeThreads] = carried;
+    }
+    __syncthreads();
+    for (int v = tid, i = 0; v < 256; v += kJudgeThreads, ++i) {
+      s_first[v] = my_first[i];
+      s_last[v] = my_last[i];
+    }
+    __syncthreads();
+
+    if (P.direct) {
+      // whole stream in this CTA: bucket seams (_kernels.py:125-133) ...
+      if (tid == 0) {
+        int carried = -1;
+        for (int v = 0; v < 256; ++v) {
+          if (s_first[v] < 0) continue;
+          if (carried >= 0) H.inc(((uint32_t)carried << 8) | (uint32_t)s_first[v]);
+          carried = s_last[v];
+        }
+      }
+      __syncthreads();
+      // ... spilled bins marked in a bitmap (reuses the dead last-pred tables)
+      uint32_t *spilled = last_w;  // 2048 words
+      for (int i = tid; i < 2048; i += kJudgeThreads) spilled[i] = 0;
+      __syncthreads();
+      const int ns = min(s_nspill, kSpillCap);
+      for (int i = tid; i < ns; i += kJudgeThreads)
+        atomicOr(&spilled[spill_w[i] >> 5], 1u << (spill_w[i] & 31));
+      __syncthreads();
+      auto get = [&](int bin) -> double {
+        uint32_t c = (hist_w[bin >> 1] >> ((bin & 1) << 4)) & 0xFFFFu;
+        if (spilled[bin >> 5] & (1u << (bin & 31))) {
+          for (int i = 0; i < ns; ++i) c += spill_w[i] == (uint32_t)bin ? kSpill : 0u;
+        }
+        return (double)c;
+      };
+      const double e = block_entropy(get, (double)(2 * P.npix - 1), s_red);
+      if (tid == 0) P.ent[pr.slot] = e;
+    } else {
+      // flush into the pair's global histogram and publish the summary
+      uint32_t *G = P.ghist + (size_t)pr.slot * 65536;
+      for (int w = tid; w < kHistWords; w += kJudgeThreads) {
+        const uint32_t v = hist_w[w];
+        if (v & 0xFFFFu) atomicAdd(&G[2 * w], v & 0xFFFFu);
+        if (v >> 16) atomicAdd(&G[2 * w + 1], v >> 16);
+      }
+      const int ns = min(s_nspill, kSpillCap);
+      for (int i = tid; i < ns; i += kJudgeThreads) atomicAdd(&G[spill_w[i]], kSpill);
+      int16_t *sum = P.segsum + ((size_t)pr.slot * P.S + seg) * 512;
+      for (int v = tid; v < 256; v += kJudgeThreads) {
+        sum[v] = (int16_t)s_first[v];
+        sum[256 + v] = (int16_t)s_last[v];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Cross-segment stitch, bucket seams and entropy of each pair whose stream
+// was split over several CTAs (or whose histogram the caller wants).
+__global__ void __launch_bounds__(kEntropyThreads) judge_finalize_kernel(const JudgeParams P) {
+  __shared__ int s_first[256], s_last[256];
+  __shared__ double s_red[kEntropyThreads / 32];
+  const PairRef pr = pair_ref(P, blockIdx.x);
+  uint32_t *G = P.ghist + (size_t)pr.slot * 65536;
+  const int16_t *sum = P.segsum + (size_t)pr.slot * P.S * 512;
+  for (int v = threadIdx.x; v < 256; v += kEntropyThreads) {
+    int carried = -1, first = -1;
+    for (int s = 0; s < P.S; ++s) {
+      const int f = sum[(size_t)s * 512 + v];
+      if (f < 0) continue;
+      if (carried >= 0) atomicAdd(&G[(carried << 8) | f], 1u);
+      else first = f;
+      carried = sum[(size_t)s * 512 + 256 + v];
+    }
+    s_first[v] = first;
+    s_last[v] = carried;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int carried = -1;
+    for (int v = 0; v < 256; ++v) {
+      if (s_first[v] < 0) continue;
+      if (carried >= 0) atomicAdd(&G[(carried << 8) | s_first[v]], 1u);
+      carried = s_last[v];
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  auto get = [&](int bin) -> double { return (double)__ldcg(G + bin); };
+  const double e = block_entropy(get, (double)(2 * P.npix - 1), s_red);
+  if (threadIdx.x == 0) P.ent[pr.slot] = e;
+}
+
+// argmin over (entropy, byte) per frame (criterion.py:171-173): the lists
+// are sorted by byte, so the first strict minimum wins ties.
+__global__ void judge_select_kernel(const JudgeParams P, uint8_t *sel) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= P.nframes) return;
+  const int kk = f == 0 ? P.cl.kA : P.cl.kB;
+  double best = 0.0;
+  int bi = -1;
+  for (int j = 0; j < kk; ++j) {
+    const int idx = f == 0 ? P.cl.idxA[j] : P.cl.idxB[j];
+    const double e = P.ent[f * P.cl.k + idx];
+    if (bi < 0 || e < best) { best = e; bi = j; }
+  }
+  sel[f] = f == 0 ? P.cl.byteA[bi] : P.cl.byteB[bi];
+}
+
+// Selected residual stream, row-major, high byte first (core.py:228-237).
+__global__ void emit_kernel(const EmitParams P) {
+  const int64_t total = P.nframes * P.npix;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = t / P.npix, k = t - f * P.npix;
+    const int spec = P.sel[f];
+    const uint16_t *src = P.frames + f * P.npix;
+    const uint16_t *prv = (spec & 0x80) ? prev_of(P.frames, P.halo, P.npix, f) : nullptr;
+    const PredCfg cfg = make_cfg(spec & 0x7F, P.px, P.py);
+    const uint32_t r = residual_at(src, prv, P.W, (int)(k / P.W), (int)(k % P.W), cfg);
+    P.stream[2 * t] = (uint8_t)(r >> 8);
+    P.stream[2 * t + 1] = (uint8_t)r;
+  }
+}
+
+__global__ void residual_image_kernel(const uint16_t *img, const uint16_t *prev, int64_t h,
+                                      int64_t w, int spec, int px, int py, uint16_t *out,
+                                      int big_endian) {
+  const int64_t total = h * w;
+  const PredCfg cfg = make_cfg(spec & 0x7F, px, py);
+  const uint16_t *prv = (spec & 0x80) ? prev : nullptr;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = residual_at(img, prv, (int)w, (int)(t / w), (int)(t % w), cfg);
+    out[t] = big_endian ? (uint16_t)((r >> 8) | ((r & 0xFFu) << 8)) : (uint16_t)r;
+  }
+}
+
+__global__ void temporal_delta_kernel(const uint16_t *cur, const uint16_t *prev, int64_t n,
+                                      uint16_t *out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = (uint16_t)(cur[t] - prev[t]);
+}
+
+// overlapping byte pairs, first byte high (_kernels.py:116-122)
+__global__ void pair_hist_kernel(const uint8_t *s, int64_t n, uint32_t *hist) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t + 1 < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&hist[((uint32_t)s[t] << 8) | s[t + 1]], 1u);
+}
+
+// ---- counting_bwt (_kernels.py:93-113) as a stable multi-block counting sort.
+// Chunk c of kBwtChunk bytes: counts[v][c] -> exclusive scan in (v, c) order
+// gives each chunk's first output slot per byte value; a chunk then scatters
+// its predecessors in input order, which keeps the sort stable.
+constexpr int kBwtChunk = 2048;
+
+__global__ void bwt_count_kernel(const uint8_t *s, int64_t n, int64_t nchunks, uint32_t *counts) {
+  __shared__ uint32_t c[256];
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) c[v] = 0;
+  __syncthreads();
+  const int64_t ch = blockIdx.x;
+  const int64_t beg = ch * kBwtChunk, end = min(n, beg + kBwtChunk);
+  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) atomicAdd(&c[s[i]], 1u);
+  __syncthreads();
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) counts[(int64_t)v * nchunks + ch] = c[v];
+}
+
+__global__ void bwt_scatter_kernel(const uint8_t *s, int64_t n, int64_t nchunks,
+                                   const uint32_t *offsets, uint8_t *out) {
+  // one thread per chunk keeps the in-chunk order (not on the timed path)
+  const int64_t ch = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ch >= nchunks) return;
+  uint32_t pos[256];
+  for (int v = 0; v < 256; ++v) pos[v] = offsets[(int64_t)v * nchunks + ch];
+  const int64_t beg = ch * kBwtChunk, end = min(n, beg + kBwtChunk);
+  for (int64_t i = beg; i < end; ++i) out[pos[s[i]]++] = s[i == 0 ? n - 1 : i - 1];
+}
+
+__global__ void entropy_u64_kernel(const uint64_t *counts, double total, double *out) {
+  __shared__ double s_red[kEntropyThreads / 32];
+  auto get = [&](int bin) -> double { return (double)counts[bin]; };
+  const double e = block_entropy(get, total, s_red);
+  if (threadIdx.x == 0) *out = e;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+
+static int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)g;
+}
+
+cudaError_t judge_configure() {
+  return cudaFuncSetAttribute(judge_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)kJudgeSmemBytes);
+}
+
+cudaError_t launch_judge(const JudgeParams &p, int grid, cudaStream_t st) {
+  judge_hist_kernel<<<grid, kJudgeThreads, kJudgeSmemBytes, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const JudgeParams &p, cudaStream_t st) {
+  judge_finalize_kernel<<<(unsigned)p.npairs, kEntropyThreads, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select(const JudgeParams &p, uint8_t *sel, cudaStream_t st) {
+  judge_select_kernel<<<(unsigned)((p.nframes + 127) / 128), 128, 0, st>>>(p, sel);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_emit(const EmitParams &p, cudaStream_t st) {
+  emit_kernel<<<grid_for(p.nframes * p.npix, 256), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_residual_image(const uint16_t *img, const uint16_t *prev, int64_t h, int64_t w,
+                                  int spec, int px, int py, uint16_t *out, int big_endian,
+                                  cudaStream_t st) {
+  residual_image_kernel<<<grid_for(h * w, 256), 256, 0, st>>>(img, prev, h, w, spec, px, py, out,
+                                                              big_endian);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_temporal_delta(const uint16_t *cur, const uint16_t *prev, int64_t n,
+                                  uint16_t *out, cudaStream_t st) {
+  temporal_delta_kernel<<<grid_for(n, 256), 256, 0, st>>>(cur, prev, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pair_hist(const uint8_t *s, int64_t n, uint32_t *hist, cudaStream_t st) {
+  pair_hist_kernel<<<grid_for(n, 256), 256, 0, st>>>(s, n, hist);
+  return cudaGetLastError();
+}
+
+size_t counting_bwt_scratch_words(int64_t n) {
+  const int64_t nchunks = (n + kBwtChunk - 1) / kBwtChunk;
+  size_t temp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, temp, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                (int)(256 * nchunks));
+  return (size_t)(2 * 256 * nchunks) + (temp + 3) / 4 + 4;
+}
+
+cudaError_t launch_counting_bwt(const uint8_t *s, int64_t n, uint8_t *out, uint32_t *scratch,
+                                size_t scratch_words, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t nchunks = (n + kBwtChunk - 1) / kBwtChunk;
+  uint32_t *counts = scratch, *offs = scratch + 256 * nchunks;
+  void *temp = offs + 256 * nchunks;
+  size_t temp_bytes = (scratch_words - 2 * 256 * nchunks) * 4;
+  bwt_count_kernel<<<(unsigned)nchunks, 256, 0, st>>>(s, n, nchunks, counts);
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, counts, offs,
+                                                (int)(256 * nchunks), st);
+  if (e != cudaSuccess) return e;
+  bwt_scatter_kernel<<<(unsigned)((nchunks + 63) / 64), 64, 0, st>>>(s, n, nchunks, offs, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_entropy_u64(const uint64_t *counts, double total, double *out,
+                               cudaStream_t st) {
+  entropy_u64_kernel<<<1, kEntropyThreads, 0, st>>>(counts, total, out);
+  return cudaGetLastError();
+}
+
+
+
+// ---------------------------------------------------------------------------
+// decompression side (reference _kernels.py:69-90, predictors.py:101-147)
+// ---------------------------------------------------------------------------
+
+// Inverse intra prediction of one frame per CTA.  Every neighbour of (y, x)
+// lies on an earlier anti-diagonal (x' + y' < x + y), so the CTA sweeps the
+// anti-diagonals in order with a barrier between them.
+__global__ void __launch_bounds__(1024) reconstruct_kernel(const uint16_t *res, int64_t h,
+                                                           int64_t w, int px, int py,
+                                                           const uint8_t *sel, uint16_t *out) {
+  const int64_t f = blockIdx.x;
+  const int64_t npix = h * w;
+  const uint16_t *r = res + f * npix;
+  uint16_t *o = out + f * npix;
+  const PredCfg c = make_cfg(sel[f] & 0x7F, px, py);
+  if (c.grp < 0) {
+    for (int64_t i = threadIdx.x; i < npix; i += blockDim.x) o[i] = r[i];
+    return;
+  }
+  const int W = (int)w;
+  for (int64_t t = 0; t < h + w - 1; ++t) {
+    const int64_t y_lo = t - (w - 1) > 0 ? t - (w - 1) : 0;
+    const int64_t y_hi = t < h - 1 ? t : h - 1;
+    for (int64_t y = y_lo + threadIdx.x; y <= y_hi; y += blockDim.x) {
+      const int x = (int)(t - y);
+      int pr = predict_at(o, nullptr, W, (int)y, x, c.sx, c.sy, c.f);
+      if (c.grp == 2) pr = (pr + predict_at(o, nullptr, W, (int)y, x, 1, 1, c.f)) >> 1;
+      o[y * w + x] = (uint16_t)(r[y * w + x] + pr);
+    }
+    __syncthreads();
+  }
+}
+
+// Temporal undelta chain: frame f = inverse_f (+ frame f-1 if temporal).
+// Pixels are independent, frames are walked in order by every thread.
+__global__ void undelta_chain_kernel(uint16_t *frames, const uint16_t *halo, int64_t nframes,
+                                     int64_t npix, const uint8_t *sel) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npix;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t run = halo ? halo[i] : 0u;
+    for (int64_t f = 0; f < nframes; ++f) {
+      uint32_t v = frames[f * npix + i];
+      if (sel[f] & 0x80) v = (v + run) & 0xFFFFu;
+      frames[f * npix + i] = (uint16_t)v;
+      run = v;
+    }
+  }
+}
+
+cudaError_t launch_reconstruct(const uint16_t *res, const uint16_t *halo, int64_t nframes,
+                               int64_t h, int64_t w, int px, int py, const uint8_t *sel,
+                               uint16_t *out, cudaStream_t st) {
+  reconstruct_kernel<<<(unsigned)nframes, 1024, 0, st>>>(res, h, w, px, py, sel, out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  undelta_chain_kernel<<<grid_for(h * w, 256), 256, 0, st>>>(out, halo, nframes, h * w, sel);
+  return cudaGetLastError();
+}
+
+}  // namespace pcbz

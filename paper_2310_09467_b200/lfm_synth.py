@@ -1,0 +1,126 @@
+"""Synthetic light-field-microscopy frames for tests and benchmarks.
+
+Reproduces, value for value, the synthetic corpus of the reference
+(pkg/src/pcbz/synth.py: SynthParams / generate) so that the CPU oracle and
+the GPU judge see identical inputs on machines where the reference package is
+not installed (the GPU box).  Bit-identity with the reference generator is
+pinned by tests/test_synth_parity.py against hashes the reference produced.
+
+Two scene models: "smooth_lenslet" (a band-limited random 4D field over
+lenslet row/col and intra-lenslet v/u, times a per-lenslet vignetting
+envelope) and "beads" (Gaussian spots of radius pitch/2 on a flat
+background); per-frame Poisson photon noise (Gaussian approximation above a
+mean of 1000 counts) and Gaussian read noise, clipped to 16 bits.  Frame t of
+a series is the scene rolled right by round(drift * t) pixels.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+MODES = ("smooth_lenslet", "beads")
+_SCENE_TAG = 0x5CE9E                 # scene RNG key suffix (reference synth.py:34)
+_POISSON_EXACT_MAX = 1000.0          # reference synth.py:35
+
+
+@dataclass(frozen=True)
+class SynthParams:
+    """Same fields, defaults and validation as reference synth.py:38-68."""
+
+    width: int
+    height: int
+    pitch_x: int = 1
+    pitch_y: int = 1
+    mode: str = "smooth_lenslet"
+    signal_amplitude: float = 20000.0
+    noise_sigma: float = 0.0
+    photon_scale: float = 0.0
+    frames: int = 1
+    drift: float = 0.0
+    seed: int = 0
+
+    def __post_init__(self):
+        if min(self.width, self.height) < 1:
+            raise ValueError(f"bad frame size {self.width}x{self.height}")
+        if min(self.pitch_x, self.pitch_y) < 1:
+            raise ValueError(f"bad pitch {self.pitch_x}x{self.pitch_y}")
+        if self.frames < 1:
+            raise ValueError(f"frames must be >= 1, got {self.frames}")
+        if self.mode not in MODES:
+            raise ValueError(f"mode must be one of {MODES}, got {self.mode!r}")
+        if min(self.signal_amplitude, self.noise_sigma, self.photon_scale) < 0:
+            raise ValueError("signal_amplitude, noise_sigma and photon_scale must be >= 0")
+        if self.signal_amplitude + 4 * self.noise_sigma > 65535:
+            raise ValueError("signal amplitude plus noise headroom exceeds 16 bits")
+
+
+def _unit_range(a: np.ndarray) -> np.ndarray:
+    lo, hi = a.min(), a.max()
+    if hi > lo:
+        return (a - lo) / (hi - lo)
+    return np.zeros_like(a)
+
+
+def scene(p: SynthParams) -> np.ndarray:
+    """The noiseless float64 scene (before drift and noise)."""
+    from scipy.ndimage import gaussian_filter
+
+    rng = np.random.default_rng([p.seed, _SCENE_TAG])
+    if p.mode == "beads":
+        img = np.full((p.height, p.width), 100.0)
+        count = max(1, (p.height * p.width) // 500)
+        cy = rng.uniform(0, p.height, count)
+        cx = rng.uniform(0, p.width, count)
+        r = max(1.0, min(p.pitch_x, p.pitch_y) / 2.0)
+        reach = int(np.ceil(3 * r))
+        two_r2 = 2 * r ** 2
+        for y, x in zip(cy, cx):
+            ya, yb = max(0, int(y) - reach), min(p.height, int(y) + reach + 1)
+            xa, xb = max(0, int(x) - reach), min(p.width, int(x) + reach + 1)
+            gy, gx = np.mgrid[ya:yb, xa:xb]
+            img[ya:yb, xa:xb] += p.signal_amplitude * np.exp(-((gy - y) ** 2 + (gx - x) ** 2) / two_r2)
+        return img
+    nlx = -(-p.width // p.pitch_x)
+    nly = -(-p.height // p.pitch_y)
+    field4 = rng.standard_normal((nly, nlx, p.pitch_y, p.pitch_x))
+    widths = (2.0, 2.0, max(p.pitch_y / 3.0, 0.8), max(p.pitch_x / 3.0, 0.8))
+    field4 = _unit_range(gaussian_filter(field4, sigma=widths, mode="wrap"))
+    env = gaussian_filter(rng.standard_normal((p.pitch_y, p.pitch_x)),
+                          sigma=max(min(p.pitch_x, p.pitch_y) / 4.0, 0.8), mode="wrap")
+    env = 0.3 + 0.7 * _unit_range(env)
+    yy, xx = np.mgrid[0:p.height, 0:p.width]
+    vy, vx = yy % p.pitch_y, xx % p.pitch_x
+    return field4[yy // p.pitch_y, xx // p.pitch_x, vy, vx] * (0.3 + 0.7 * env[vy, vx]) * p.signal_amplitude
+
+
+def noisy_frame(base: np.ndarray, p: SynthParams, t: int) -> np.ndarray:
+    """Frame t of the series: drifted scene plus that frame's noise draw."""
+    shift = int(round(p.drift * t))
+    img = np.roll(base, shift, axis=1) if shift else base
+    rng = np.random.default_rng([p.seed, t])
+    val = img
+    if p.photon_scale > 0:
+        lam = img * p.photon_scale
+        low = lam <= _POISSON_EXACT_MAX
+        exact = rng.poisson(np.where(low, lam, 0.0))     # draw order fixed, content-independent
+        normal = rng.standard_normal(lam.shape)
+        val = np.where(low, exact, lam + normal * np.sqrt(lam)) / p.photon_scale
+    if p.noise_sigma > 0:
+        val = val + rng.normal(0.0, p.noise_sigma, img.shape)
+    return np.clip(np.rint(val), 0, 65535).astype(np.uint16)
+
+
+def generate_array(p: SynthParams, frames: range | None = None) -> np.ndarray:
+    """[F, H, W] uint16 volume equal to reference generate(p).to_array()
+    (or the given sub-range of frame indices)."""
+    base = scene(p)
+    idx = range(p.frames) if frames is None else frames
+    return np.stack([noisy_frame(base, p, t) for t in idx])
+
+
+def generate(p: SynthParams):
+    """FrameStack like reference synth.generate (synth.py:128-142)."""
+    from .core import FrameStack, LensletGeometry
+
+    return FrameStack.from_array(generate_array(p), LensletGeometry(p.pitch_x, p.pitch_y))

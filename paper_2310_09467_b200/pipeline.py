@@ -1,0 +1,193 @@
+"""Stack compression / decompression around the B200 judge
+(reference pkg/src/pcbz/pipeline.py).
+
+compress_stack_detailed keeps the reference's per-frame semantics
+(pipeline.py:76-113) but runs them batched: all frames of a chunk are judged
+and their selected residual streams emitted by one device call
+(pcbz_judge_host), then every (frame, block) pair is bzip2-coded on a host
+thread pool while the next chunk is on the GPU.  Output bytes are a pure
+function of (stack, options) and identical to the reference's.
+"""
+from __future__ import annotations
+
+import time
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .codec import (DEFAULT_BLOCK_SIZE, BlockPlan, CompressedBlocks, CorruptContainerError,
+                    bz2_block, decompress_blocks, read_container, split_blocks, write_container)
+from .core import Frame, FrameStack, LensletGeometry, PredictorSpec, unpack_symbols
+from .criterion import EntropyReport, default_candidates
+
+#: frames per device call in compress_stack (bounded host/device memory)
+GPU_CHUNK_FRAMES = 32
+
+
+@dataclass(frozen=True)
+class CompressOptions:
+    """Same knobs as reference pipeline.py:26-49."""
+
+    candidates: tuple | None = None
+    forced: PredictorSpec | None = None
+    block_size: int = DEFAULT_BLOCK_SIZE
+    workers: int = 1
+    temporal: bool = True
+
+    def __post_init__(self):
+        if self.workers < 1:
+            raise ValueError(f"workers must be >= 1, got {self.workers}")
+        if self.block_size < 1:
+            raise ValueError(f"block_size must be >= 1, got {self.block_size}")
+        if self.candidates is not None and not self.candidates:
+            raise ValueError("candidate set must not be empty")
+
+
+@dataclass
+class CompressResult:
+    data: bytes
+    specs: list
+    reports: list
+    select_seconds: float = 0.0
+    encode_seconds: float = 0.0
+
+
+def candidate_codes(opts: CompressOptions) -> list:
+    """Full candidate byte list of a stack (sorted, validated); the device
+    drops temporal ones on frames without a previous frame, which is
+    reference _frame_candidates (pipeline.py:67-73)."""
+    cands = default_candidates(True, opts.temporal) if opts.candidates is None else opts.candidates
+    codes = [s.to_byte() for s in cands]
+    if len(set(codes)) != len(codes):
+        raise ValueError("candidate set contains duplicates")
+    if not any(not c & 0x80 for c in codes):
+        raise ValueError("no usable candidate for a frame without a previous frame")
+    return sorted(codes)
+
+
+def judge_volume(vol: np.ndarray, geo: LensletGeometry, codes: list, temporal: bool,
+                 halo: np.ndarray | None = None, want_stream: bool = True):
+    """One device call: entropies [F, k] (NaN = not scored), selected bytes [F],
+    emitted streams [F, 2HW] for a C-contiguous [F, H, W] uint16 volume."""
+    F, H, W = vol.shape
+    spec = np.array(codes, np.uint8)
+    ent = np.empty((F, spec.size), np.float64)
+    sel = np.empty(F, np.uint8)
+    stream = np.empty((F, 2 * H * W), np.uint8) if want_stream else None
+    _lib.check(_lib.load().pcbz_judge_host(
+        _lib.ptr(vol), _lib.ptr(halo), F, H, W, geo.pitch_x, geo.pitch_y, _lib.ptr(spec), spec.size,
+        1 if temporal else 0, _lib.ptr(ent), _lib.ptr(sel), _lib.ptr(stream)))
+    return ent, sel, stream
+
+
+def emit_volume(vol: np.ndarray, geo: LensletGeometry, sel: np.ndarray,
+                halo: np.ndarray | None = None) -> np.ndarray:
+    F, H, W = vol.shape
+    s = np.ascontiguousarray(sel, dtype=np.uint8)
+    stream = np.empty((F, 2 * H * W), np.uint8)
+    _lib.check(_lib.load().pcbz_emit_host(_lib.ptr(vol), _lib.ptr(halo), F, H, W, geo.pitch_x,
+                                          geo.pitch_y, _lib.ptr(s), _lib.ptr(stream)))
+    return stream
+
+
+def _reports(ent: np.ndarray, codes: list) -> list:
+    out = []
+    for row in ent:
+        entries = tuple((PredictorSpec.from_byte(c), float(e)) for c, e in zip(codes, row)
+                        if not np.isnan(e))
+        best = min(entries, key=lambda se: (se[1], se[0].to_byte()))
+        out.append(EntropyReport(entries=entries, selected=best[0]))
+    return out
+
+
+def compress_stack_detailed(stack: FrameStack, opts: CompressOptions | None = None) -> CompressResult:
+    """Reference pipeline.py:76-113 semantics, batched on the device."""
+    opts = opts or CompressOptions()
+    vol = np.ascontiguousarray(stack.to_array())
+    geo = stack.geometry
+    F = vol.shape[0]
+    forced = opts.forced
+    codes = None if forced is not None else candidate_codes(opts)
+    specs, reports = [], []
+    payloads = [None] * F
+    select_s = encode_s = 0.0
+    pool = ThreadPoolExecutor(max(1, opts.workers))
+    futures = []
+    try:
+        for a in range(0, F, GPU_CHUNK_FRAMES):
+            b = min(F, a + GPU_CHUNK_FRAMES)
+            chunk = vol[a:b]
+            halo = vol[a - 1] if (a > 0 and opts.temporal) else None
+            t0 = time.perf_counter()
+            if forced is None:
+                ent, sel, streams = judge_volume(chunk, geo, codes, opts.temporal, halo)
+                reports += _reports(ent, codes)
+                select_s += time.perf_counter() - t0
+            else:
+                sel = np.array([forced.to_byte() if (a + i > 0 and opts.temporal) else forced.intra_id
+                                for i in range(b - a)], np.uint8)
+                streams = emit_volume(chunk, geo, sel, halo)
+                reports += [None] * (b - a)
+                encode_s += time.perf_counter() - t0
+            specs += [PredictorSpec.from_byte(int(c)) for c in sel]
+            for i in range(b - a):
+                for j, blk in enumerate(split_blocks(streams[i], opts.block_size)):
+                    futures.append((a + i, j, pool.submit(bz2_block, blk)))
+        t0 = time.perf_counter()
+        by_frame = {}
+        for fi, j, fut in futures:
+            by_frame.setdefault(fi, []).append(fut.result())
+        encode_s += time.perf_counter() - t0
+    finally:
+        pool.shutdown(wait=True)
+    for fi in range(F):
+        blocks = by_frame.get(fi, [])
+        payloads[fi] = CompressedBlocks(BlockPlan(opts.block_size, len(blocks)), tuple(blocks))
+    data = write_container(stack.width, stack.height, geo.pitch_x, geo.pitch_y, opts.block_size,
+                           list(zip(specs, payloads)))
+    return CompressResult(data, specs, reports, select_s, encode_s)
+
+
+def compress_stack(stack: FrameStack, opts: CompressOptions | None = None) -> bytes:
+    return compress_stack_detailed(stack, opts).data
+
+
+def decompress_stack(data, workers: int = 1) -> FrameStack:
+    """Reference pipeline.py:121-139: bzip2 on host threads, inverse
+    prediction and temporal undelta on the device."""
+    header, records, payloads = read_container(data)
+    H, W = header.height, header.width
+    res = np.empty((header.frame_count, H, W), np.uint16)
+    for i, rec in enumerate(records):
+        blocks = CompressedBlocks(BlockPlan(header.block_size, len(rec.block_sizes)),
+                                  tuple(bytes(p) for p in payloads[i]))
+        try:
+            res[i] = unpack_symbols(decompress_blocks(blocks, workers), W, H)
+        except ValueError as exc:
+            raise CorruptContainerError(f"frame {i}: {exc}") from exc
+    sel = np.array([r.spec.to_byte() for r in records], np.uint8)
+    out = np.empty_like(res)
+    _lib.check(_lib.load().pcbz_reconstruct_host(_lib.ptr(res), None, res.shape[0], H, W,
+                                                 header.pitch_x, header.pitch_y, _lib.ptr(sel),
+                                                 _lib.ptr(out)))
+    geo = LensletGeometry(header.pitch_x, header.pitch_y)
+    return FrameStack(tuple(Frame(f, geo) for f in out))
+
+
+@dataclass
+class Metrics:
+    uncompressed_bytes: int
+    container_bytes: int
+    compression_ratio: float
+    bits_per_dim: float
+    compress_seconds: float | None = None
+    decompress_seconds: float | None = None
+
+
+def measure(container: bytes, stack: FrameStack, compress_seconds=None, decompress_seconds=None):
+    """Reference pipeline.py:154-168."""
+    n = stack.width * stack.height * stack.frame_count
+    return Metrics(stack.nbytes, len(container), stack.nbytes / len(container),
+                   8.0 * len(container) / n, compress_seconds, decompress_seconds)
