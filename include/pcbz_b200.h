@@ -133,9 +133,12 @@ PCBZ_API int pcbz_reconstruct_host(const uint16_t *residuals, const uint16_t *ha
  * is split into (0 = automatic).  Outputs must not depend on it. */
 PCBZ_API int pcbz_set_segment_override(int segments);
 
-/* Timing of the most recent pcbz_judge_device call on this thread when it was
- * made with pcbz_set_profiling(1): milliseconds of the histogram kernel and of
- * the whole judge (CUDA events on the launch stream; synchronises). */
+/* Profiling: while pcbz_set_profiling(1) is on, every judge call on this
+ * thread records CUDA events on its launch stream (no host synchronisation).
+ * pcbz_last_timing waits for them and returns the SUMS since the previous
+ * query: milliseconds spent in the histogram kernel, in the whole judge
+ * sequence, and the number of kernels launched (the last call's count when
+ * profiling was off). */
 PCBZ_API int pcbz_set_profiling(int on);
 PCBZ_API int pcbz_last_timing(float *hist_ms, float *total_ms, int *launches);
 

@@ -20,8 +20,10 @@ namespace {
 
 thread_local std::string g_err;
 thread_local bool g_profile = false;
-thread_local float g_hist_ms = 0.f, g_total_ms = 0.f;
 thread_local int g_launches = 0;
+// CUDA events of profiled judge calls, summed lazily by pcbz_last_timing
+struct TimedCall { cudaEvent_t e0, e1, e2; int launches; };
+thread_local std::vector<TimedCall> g_timed;
 thread_local int g_seg_override = 0;
 
 int fail(int code, const char *fmt, ...) {
@@ -199,10 +201,10 @@ int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double 
     jp.segsum = reinterpret_cast<int16_t *>(ws + pl.off_segsum);
     jp.ghist = d_hist ? d_hist : reinterpret_cast<uint32_t *>(ws + pl.off_ghist);
   }
-  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+  TimedCall tc{nullptr, nullptr, nullptr, 0};
   if (g_profile) {
-    cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
-    cudaEventRecord(e0, st);
+    cudaEventCreate(&tc.e0); cudaEventCreate(&tc.e1); cudaEventCreate(&tc.e2);
+    cudaEventRecord(tc.e0, st);
   }
   int launches = 0;
   CUDA_TRY(cudaMemsetAsync(ws, 0, pl.off_fscratch, st));   // counter + err
@@ -211,7 +213,7 @@ int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double 
     CUDA_TRY(cudaMemsetAsync(jp.ghist, 0, (size_t)jp.nframes * jp.cl.k * 65536 * 4, st));
   CUDA_TRY(launch_judge(jp, pl.grid, st));
   ++launches;
-  if (g_profile) cudaEventRecord(e1, st);
+  if (g_profile) cudaEventRecord(tc.e1, st);
   if (!jp.direct) { CUDA_TRY(launch_finalize(jp, st)); ++launches; }
   CUDA_TRY(launch_select(jp, d_sel, st));
   ++launches;
@@ -222,11 +224,9 @@ int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double 
   }
   g_launches = launches;
   if (g_profile) {
-    cudaEventRecord(e2, st);
-    cudaEventSynchronize(e2);
-    cudaEventElapsedTime(&g_hist_ms, e0, e1);
-    cudaEventElapsedTime(&g_total_ms, e0, e2);
-    cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
+    cudaEventRecord(tc.e2, st);
+    tc.launches = launches;
+    g_timed.push_back(tc);
   }
   return PCBZ_OK;
 }
@@ -265,9 +265,21 @@ int pcbz_set_profiling(int on) {
 }
 
 int pcbz_last_timing(float *hist_ms, float *total_ms, int *launches) {
-  if (hist_ms) *hist_ms = g_hist_ms;
-  if (total_ms) *total_ms = g_total_ms;
-  if (launches) *launches = g_launches;
+  float hs = 0.f, ts = 0.f;
+  int nl = 0;
+  for (TimedCall &tc : g_timed) {
+    float a = 0.f, b = 0.f;
+    CUDA_TRY(cudaEventSynchronize(tc.e2));
+    CUDA_TRY(cudaEventElapsedTime(&a, tc.e0, tc.e1));
+    CUDA_TRY(cudaEventElapsedTime(&b, tc.e0, tc.e2));
+    hs += a; ts += b; nl += tc.launches;
+    cudaEventDestroy(tc.e0); cudaEventDestroy(tc.e1); cudaEventDestroy(tc.e2);
+  }
+  const bool any = !g_timed.empty();
+  g_timed.clear();
+  if (hist_ms) *hist_ms = hs;
+  if (total_ms) *total_ms = ts;
+  if (launches) *launches = any ? nl : g_launches;
   return PCBZ_OK;
 }
 

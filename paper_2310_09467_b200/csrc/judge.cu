@@ -99,31 +99,106 @@ struct SmemHist {
 // deterministic fp64 entropy: -sum p*log2(p), p = c / total (criterion.py:86-96)
 // ---------------------------------------------------------------------------
 
-// All entropy reductions run with kEntropyThreads threads, bin b handled by
-// thread b % kEntropyThreads in ascending order, then a fixed xor-tree per
-// warp and an in-order sum over warps: the same histogram always yields the
-// same double, whichever kernel produced it.
+// Exact, order-independent sum of the fp64 terms -p*log2(p).  Every term is
+// first rounded exactly like the reference's numpy expression
+// (p = c / total; p * log2(p)), then accumulated EXACTLY in 192-bit fixed
+// point (scale 2^-160: terms >= 2^-108 convert without loss; the sum is
+// < 2^16), and the total is rounded to double once.  Consequences: the
+// result does not depend on bin order, thread count or reduction tree, so
+// histograms that are permutations of each other give bit-identical
+// entropies (ties then resolve to the smaller byte, criterion.py:172), and
+// the value is within 1 ulp of the exact sum of the reference's terms.
+struct Fix192 {
+  unsigned long long w0, w1, w2;  // little-endian limbs, value = w * 2^-160
+};
+
+__device__ __forceinline__ void fix_add(Fix192 &a, const Fix192 &b) {
+  asm("add.cc.u64 %0, %0, %3;\n\taddc.cc.u64 %1, %1, %4;\n\taddc.u64 %2, %2, %5;"
+      : "+l"(a.w0), "+l"(a.w1), "+l"(a.w2)
+      : "l"(b.w0), "l"(b.w1), "l"(b.w2));
+}
+
+// exact conversion of a non-negative double (0 or >= 2^-108, < 2^31)
+__device__ __forceinline__ Fix192 fix_from_double(double d) {
+  Fix192 r{0ull, 0ull, 0ull};
+  if (!(d > 0.0)) return r;
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(d);
+  const int e = (int)((bits >> 52) & 0x7FF);
+  const unsigned long long m = (bits & 0xFFFFFFFFFFFFFull) | (1ull << 52);
+  int sh = e - 1075 + 160;  // value = m * 2^(e-1075) = (m << sh) * 2^-160
+  if (sh < 0) {             // below the 2^-160 grid: unreachable for entropy terms
+    r.w0 = m >> (-sh < 64 ? -sh : 63);
+    return r;
+  }
+  const int limb = sh >> 6, off = sh & 63;
+  const unsigned long long lo = m << off;
+  const unsigned long long hi = off ? (m >> (64 - off)) : 0ull;
+  if (limb == 0) { r.w0 = lo; r.w1 = hi; }
+  else if (limb == 1) { r.w1 = lo; r.w2 = hi; }
+  else if (limb == 2) { r.w2 = lo; }
+  return r;
+}
+
+// correctly rounded (nearest-even) double of a Fix192 value
+__device__ __forceinline__ double fix_to_double(const Fix192 &a) {
+  unsigned long long v;
+  bool sticky;
+  int shift;  // value = v * 2^(shift - 160) (+ sticky residue)
+  if (a.w2) {
+    const int lz = __clzll(a.w2);
+    const int s = 64 - lz;  // bits of w2; take the top 64 of (w2:w1:w0)
+    v = s == 64 ? a.w2 : ((a.w2 << (64 - s)) | (a.w1 >> s));
+    sticky = (s == 64 ? a.w1 : (a.w1 << (64 - s))) != 0 || a.w0 != 0;
+    shift = 64 + s;
+  } else if (a.w1) {
+    const int lz = __clzll(a.w1);
+    const int s = 64 - lz;
+    v = s == 64 ? a.w1 : ((a.w1 << (64 - s)) | (a.w0 >> s));
+    sticky = (s == 64 ? a.w0 : (a.w0 << (64 - s))) != 0;
+    shift = s;
+  } else {
+    v = a.w0;
+    sticky = false;
+    shift = 0;
+  }
+  // v carries 64 significant bits (or fewer when exact); the sticky bit below
+  // them sits under double's rounding position, so OR-ing it into bit 0
+  // keeps round-to-nearest-even exact
+  if (sticky) v |= 1ull;
+  return ldexp(__ull2double_rn(v), shift - 160);
+}
+
+__device__ __forceinline__ Fix192 fix_shfl_xor(const Fix192 &a, int o) {
+  Fix192 r;
+  r.w0 = __shfl_xor_sync(0xffffffffu, a.w0, o);
+  r.w1 = __shfl_xor_sync(0xffffffffu, a.w1, o);
+  r.w2 = __shfl_xor_sync(0xffffffffu, a.w2, o);
+  return r;
+}
+
+// Block-wide entropy -sum p*log2(p), p = c / total (criterion.py:86-96);
+// `red` must hold kEntropyThreads / 32 Fix192 values.
 template <typename Get>
-__device__ double block_entropy(Get get, double total, double *red) {
-  double acc = 0.0;
+__device__ double block_entropy(Get get, double total, Fix192 *red) {
+  Fix192 acc{0ull, 0ull, 0ull};
   if (total > 0.0) {
     for (int b = threadIdx.x; b < 65536; b += kEntropyThreads) {
       const double c = get(b);
       if (c > 0.0) {
         const double p = c / total;
-        acc += p * log2(p);
+        fix_add(acc, fix_from_double(-(p * log2(p))));
       }
     }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  for (int o = 16; o > 0; o >>= 1) fix_add(acc, fix_shfl_xor(acc, o));
   __syncthreads();
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
-  double s = 0.0;
-  for (int w = 0; w < kEntropyThreads / 32; ++w) s += red[w];
+  Fix192 s{0ull, 0ull, 0ull};
+  for (int w = 0; w < kEntropyThreads / 32; ++w) fix_add(s, red[w]);
   __syncthreads();
-  return -s;
+  return fix_to_double(s);
 }
 
 // ---------------------------------------------------------------------------
@@ -167,7 +242,7 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
   uint32_t *last_w = hist_w + kHistWords;                 // [kLastWords][kJudgeThreads]
   uint32_t *spill_w = last_w + kLastWords * kJudgeThreads;
   __shared__ int s_item, s_nspill;
-  __shared__ double s_red[kJudgeThreads / 32];
+  __shared__ Fix192 s_red[kJudgeThreads / 32];
   // after the stitch the last-pred tables are dead: words [0, 2048) become the
   // spilled-bin bitmap, [2048, 2560) the CTA's first/last pred per key
   int *s_first = reinterpret_cast<int *>(last_w) + 2048;
@@ -310,7 +385,7 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
 // was split over several CTAs (or whose histogram the caller wants).
 __global__ void __launch_bounds__(kEntropyThreads) judge_finalize_kernel(const JudgeParams P) {
   __shared__ int s_first[256], s_last[256];
-  __shared__ double s_red[kEntropyThreads / 32];
+  __shared__ Fix192 s_red[kEntropyThreads / 32];
   const PairRef pr = pair_ref(P, blockIdx.x);
   uint32_t *G = P.ghist + (size_t)pr.slot * 65536;
   const int16_t *sum = P.segsum + (size_t)pr.slot * P.S * 512;
@@ -430,7 +505,7 @@ __global__ void bwt_scatter_kernel(const uint8_t *s, int64_t n, int64_t nchunks,
 }
 
 __global__ void entropy_u64_kernel(const uint64_t *counts, double total, double *out) {
-  __shared__ double s_red[kEntropyThreads / 32];
+  __shared__ Fix192 s_red[kEntropyThreads / 32];
   auto get = [&](int bin) -> double { return (double)counts[bin]; };
   const double e = block_entropy(get, total, s_red);
   if (threadIdx.x == 0) *out = e;

@@ -68,14 +68,20 @@ def candidate_codes(opts: CompressOptions) -> list:
 
 
 def judge_volume(vol: np.ndarray, geo: LensletGeometry, codes: list, temporal: bool,
-                 halo: np.ndarray | None = None, want_stream: bool = True):
+                 halo: np.ndarray | None = None, want_stream: bool = True, out=None):
     """One device call: entropies [F, k] (NaN = not scored), selected bytes [F],
-    emitted streams [F, 2HW] for a C-contiguous [F, H, W] uint16 volume."""
+    emitted streams [F, 2HW] for a C-contiguous [F, H, W] uint16 volume.
+    `out` = (ent, sel, stream) host arrays to fill (e.g. pinned memory)."""
     F, H, W = vol.shape
     spec = np.array(codes, np.uint8)
-    ent = np.empty((F, spec.size), np.float64)
-    sel = np.empty(F, np.uint8)
-    stream = np.empty((F, 2 * H * W), np.uint8) if want_stream else None
+    if out is not None:
+        ent, sel, stream = out
+        assert ent.shape == (F, spec.size) and sel.shape == (F,)
+        assert stream is None or stream.shape == (F, 2 * H * W)
+    else:
+        ent = np.empty((F, spec.size), np.float64)
+        sel = np.empty(F, np.uint8)
+        stream = np.empty((F, 2 * H * W), np.uint8) if want_stream else None
     _lib.check(_lib.load().pcbz_judge_host(
         _lib.ptr(vol), _lib.ptr(halo), F, H, W, geo.pitch_x, geo.pitch_y, _lib.ptr(spec), spec.size,
         1 if temporal else 0, _lib.ptr(ent), _lib.ptr(sel), _lib.ptr(stream)))
