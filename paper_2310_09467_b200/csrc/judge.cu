@@ -99,106 +99,174 @@ struct SmemHist {
 // deterministic fp64 entropy: -sum p*log2(p), p = c / total (criterion.py:86-96)
 // ---------------------------------------------------------------------------
 
-// Exact, order-independent sum of the fp64 terms -p*log2(p).  Every term is
-// first rounded exactly like the reference's numpy expression
-// (p = c / total; p * log2(p)), then accumulated EXACTLY in 192-bit fixed
-// point (scale 2^-160: terms >= 2^-108 convert without loss; the sum is
-// < 2^16), and the total is rounded to double once.  Consequences: the
-// result does not depend on bin order, thread count or reduction tree, so
-// histograms that are permutations of each other give bit-identical
-// entropies (ties then resolve to the smaller byte, criterion.py:172), and
-// the value is within 1 ulp of the exact sum of the reference's terms.
-struct Fix192 {
-  unsigned long long w0, w1, w2;  // little-endian limbs, value = w * 2^-160
+// Entropy exactly as the reference evaluates it (criterion.py:86-96):
+//     p = counts[counts > 0] / float(total);  E = -(p * np.log2(p)).sum()
+// i.e. terms t_i = p_i * log2(p_i) over the occupied bins IN BIN ORDER,
+// summed with numpy's pairwise summation (blocks of <= 128 elements with
+// eight accumulators, split at n/2 rounded down to a multiple of 8; verified
+// bit-for-bit against np.sum for n = 1..65536).  The result
+// is therefore bit-identical to the reference whenever the device log2
+// rounds like numpy's (both are correctly rounded for nearly all inputs),
+// and ties between candidates resolve exactly as in the reference.
+//
+// Parallel form: every thread owns a contiguous bin range; a block scan of
+// per-range occupied counts gives each occupied bin its index in the
+// compacted term array; the recursion's leaves (index ranges) are evaluated
+// by different threads; one thread then folds the leaf sums in recursion
+// order.
+constexpr int kNpLeafMax = 1024;  // leaves hold >= 64 terms once n > 128
+constexpr int kNpBlock = 128;     // numpy PW_BLOCKSIZE
+
+struct NpScratch {
+  uint32_t off[kEntropyThreads + 1];  // compacted index of each range's first term
+  uint32_t leaf_beg[kNpLeafMax];
+  uint32_t leaf_len[kNpLeafMax];
+  double leaf_sum[kNpLeafMax];
+  int nleaf;
 };
+constexpr size_t kNpScratchBytes = sizeof(NpScratch);
 
-__device__ __forceinline__ void fix_add(Fix192 &a, const Fix192 &b) {
-  asm("add.cc.u64 %0, %0, %3;\n\taddc.cc.u64 %1, %1, %4;\n\taddc.u64 %2, %2, %5;"
-      : "+l"(a.w0), "+l"(a.w1), "+l"(a.w2)
-      : "l"(b.w0), "l"(b.w1), "l"(b.w2));
-}
+__device__ __forceinline__ int range_lo(int t) { return (int)((65536LL * t) / kEntropyThreads); }
 
-// exact conversion of a non-negative double (0 or >= 2^-108, < 2^31)
-__device__ __forceinline__ Fix192 fix_from_double(double d) {
-  Fix192 r{0ull, 0ull, 0ull};
-  if (!(d > 0.0)) return r;
-  const unsigned long long bits = (unsigned long long)__double_as_longlong(d);
-  const int e = (int)((bits >> 52) & 0x7FF);
-  const unsigned long long m = (bits & 0xFFFFFFFFFFFFFull) | (1ull << 52);
-  int sh = e - 1075 + 160;  // value = m * 2^(e-1075) = (m << sh) * 2^-160
-  if (sh < 0) {             // below the 2^-160 grid: unreachable for entropy terms
-    r.w0 = m >> (-sh < 64 ? -sh : 63);
-    return r;
-  }
-  const int limb = sh >> 6, off = sh & 63;
-  const unsigned long long lo = m << off;
-  const unsigned long long hi = off ? (m >> (64 - off)) : 0ull;
-  if (limb == 0) { r.w0 = lo; r.w1 = hi; }
-  else if (limb == 1) { r.w1 = lo; r.w2 = hi; }
-  else if (limb == 2) { r.w2 = lo; }
-  return r;
-}
-
-// correctly rounded (nearest-even) double of a Fix192 value
-__device__ __forceinline__ double fix_to_double(const Fix192 &a) {
-  unsigned long long v;
-  bool sticky;
-  int shift;  // value = v * 2^(shift - 160) (+ sticky residue)
-  if (a.w2) {
-    const int lz = __clzll(a.w2);
-    const int s = 64 - lz;  // bits of w2; take the top 64 of (w2:w1:w0)
-    v = s == 64 ? a.w2 : ((a.w2 << (64 - s)) | (a.w1 >> s));
-    sticky = (s == 64 ? a.w1 : (a.w1 << (64 - s))) != 0 || a.w0 != 0;
-    shift = 64 + s;
-  } else if (a.w1) {
-    const int lz = __clzll(a.w1);
-    const int s = 64 - lz;
-    v = s == 64 ? a.w1 : ((a.w1 << (64 - s)) | (a.w0 >> s));
-    sticky = (s == 64 ? a.w0 : (a.w0 << (64 - s))) != 0;
-    shift = s;
-  } else {
-    v = a.w0;
-    sticky = false;
-    shift = 0;
-  }
-  // v carries 64 significant bits (or fewer when exact); the sticky bit below
-  // them sits under double's rounding position, so OR-ing it into bit 0
-  // keeps round-to-nearest-even exact
-  if (sticky) v |= 1ull;
-  return ldexp(__ull2double_rn(v), shift - 160);
-}
-
-__device__ __forceinline__ Fix192 fix_shfl_xor(const Fix192 &a, int o) {
-  Fix192 r;
-  r.w0 = __shfl_xor_sync(0xffffffffu, a.w0, o);
-  r.w1 = __shfl_xor_sync(0xffffffffu, a.w1, o);
-  r.w2 = __shfl_xor_sync(0xffffffffu, a.w2, o);
-  return r;
-}
-
-// Block-wide entropy -sum p*log2(p), p = c / total (criterion.py:86-96);
-// `red` must hold kEntropyThreads / 32 Fix192 values.
-template <typename Get>
-__device__ double block_entropy(Get get, double total, Fix192 *red) {
-  Fix192 acc{0ull, 0ull, 0ull};
-  if (total > 0.0) {
-    for (int b = threadIdx.x; b < 65536; b += kEntropyThreads) {
-      const double c = get(b);
-      if (c > 0.0) {
-        const double p = c / total;
-        fix_add(acc, fix_from_double(-(p * log2(p))));
-      }
+// leaves of numpy's pairwise recursion over [beg, beg + n), in DFS order
+__device__ void np_enumerate_leaves(uint32_t beg, uint32_t n, NpScratch &S) {
+  uint32_t st_b[40], st_n[40];
+  int sp = 0, nl = 0;
+  st_b[sp] = beg; st_n[sp] = n; ++sp;
+  while (sp) {
+    --sp;
+    const uint32_t b = st_b[sp], m = st_n[sp];
+    if (m <= (uint32_t)kNpBlock) {
+      S.leaf_beg[nl] = b; S.leaf_len[nl] = m; ++nl;
+    } else {
+      uint32_t h = m / 2;
+      h -= h % 8;
+      st_b[sp] = b + h; st_n[sp] = m - h; ++sp;  // right half after the left one
+      st_b[sp] = b; st_n[sp] = h; ++sp;
     }
   }
+  S.nleaf = nl;
+}
+
+// fold leaf sums in the recursion's order: sum(a, n) = sum(left) + sum(right)
+__device__ double np_fold(uint32_t n, const NpScratch &S) {
+  // iterative post-order over the same split tree; leaves are consumed in DFS order
+  uint32_t st_n[40];
+  uint8_t st_state[40];
+  double st_left[40];
+  int sp = 0, leaf = 0;
+  double ret = 0.0;
+  st_n[0] = n; st_state[0] = 0; sp = 1;
+  bool have_ret = false;
+  while (sp) {
+    const int top = sp - 1;
+    const uint32_t m = st_n[top];
+    if (m <= (uint32_t)kNpBlock) {
+      ret = S.leaf_sum[leaf++];
+      have_ret = true;
+      --sp;
+      continue;
+    }
+    uint32_t h = m / 2;
+    h -= h % 8;
+    if (st_state[top] == 0) {          // descend left
+      st_state[top] = 1;
+      st_n[sp] = h; st_state[sp] = 0; ++sp;
+      have_ret = false;
+    } else if (st_state[top] == 1) {   // left done -> descend right
+      st_left[top] = ret;
+      st_state[top] = 2;
+      st_n[sp] = m - h; st_state[sp] = 0; ++sp;
+      have_ret = false;
+    } else {                           // both done
+      ret = st_left[top] + ret;
+      have_ret = true;
+      --sp;
+    }
+  }
+  (void)have_ret;
+  return ret;
+}
+
+template <typename Get>
+__device__ double block_entropy(Get get, double total, NpScratch &S) {
+  const int t = threadIdx.x;
+  const int lo = range_lo(t), hi = range_lo(t + 1);
+  uint32_t cnt = 0;
+  if (total > 0.0)
+    for (int b = lo; b < hi; ++b) cnt += get(b) > 0.0;
+  // block exclusive scan of cnt (kEntropyThreads = 6 warps)
+  uint32_t incl = cnt;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) fix_add(acc, fix_shfl_xor(acc, o));
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((t & 31) >= o) incl += v;
+  }
   __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  if ((t & 31) == 31) S.off[t >> 5] = incl;   // warp totals (temporarily)
   __syncthreads();
-  Fix192 s{0ull, 0ull, 0ull};
-  for (int w = 0; w < kEntropyThreads / 32; ++w) fix_add(s, red[w]);
+  uint32_t warp_base = 0;
+  for (int w = 0; w < (t >> 5); ++w) warp_base += S.off[w];
+  uint32_t n_all = 0;
+  for (int w = 0; w < kEntropyThreads / 32; ++w) n_all += S.off[w];
   __syncthreads();
-  return fix_to_double(s);
+  S.off[t] = warp_base + incl - cnt;
+  if (t == 0) {
+    S.off[kEntropyThreads] = n_all;
+    if (n_all > 0) np_enumerate_leaves(0, n_all, S);
+    else S.nleaf = 0;
+  }
+  __syncthreads();
+  const int nleaf = S.nleaf;
+  for (int L = t; L < nleaf; L += kEntropyThreads) {
+    const uint32_t beg = S.leaf_beg[L], len = S.leaf_len[L];
+    // owner range of compacted index `beg`: last r with off[r] <= beg
+    int r0 = 0, r1 = kEntropyThreads - 1;
+    while (r0 < r1) {
+      const int mid = (r0 + r1 + 1) >> 1;
+      if (S.off[mid] <= beg) r0 = mid; else r1 = mid - 1;
+    }
+    int b = range_lo(r0);
+    uint32_t idx = S.off[r0];
+    // advance to the beg-th occupied bin
+    double c = get(b);
+    while (!(c > 0.0) || idx < beg) {
+      if (c > 0.0) ++idx;
+      ++b;
+      c = get(b);
+    }
+    auto next_term = [&]() -> double {  // term of the current occupied bin, then advance
+      const double p = c / total;
+      const double v = p * log2(p);
+      ++b;
+      while (b < 65536 && !((c = get(b)) > 0.0)) ++b;
+      return v;
+    };
+    double res;
+    if (len < 8) {
+      res = -0.0;
+      for (uint32_t i = 0; i < len; ++i) res += next_term();
+    } else {
+      double r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = next_term();
+      uint32_t i = 8;
+      for (; i < len - (len % 8); i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] += next_term();
+      }
+      res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+      for (; i < len; ++i) res += next_term();
+    }
+    S.leaf_sum[L] = res;
+  }
+  __syncthreads();
+  __shared__ double s_result;
+  if (t == 0) s_result = (total > 0.0 && n_all > 0) ? -np_fold(n_all, S) : 0.0;
+  __syncthreads();
+  const double e = s_result;
+  __syncthreads();
+  return e;
 }
 
 // ---------------------------------------------------------------------------
@@ -242,7 +310,6 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
   uint32_t *last_w = hist_w + kHistWords;                 // [kLastWords][kJudgeThreads]
   uint32_t *spill_w = last_w + kLastWords * kJudgeThreads;
   __shared__ int s_item, s_nspill;
-  __shared__ Fix192 s_red[kJudgeThreads / 32];
   // after the stitch the last-pred tables are dead: words [0, 2048) become the
   // spilled-bin bitmap, [2048, 2560) the CTA's first/last pred per key
   int *s_first = reinterpret_cast<int *>(last_w) + 2048;
@@ -359,7 +426,8 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
         }
         return (double)c;
       };
-      const double e = block_entropy(get, (double)(2 * P.npix - 1), s_red);
+      NpScratch &scr = *reinterpret_cast<NpScratch *>(last_w + 2560);
+      const double e = block_entropy(get, (double)(2 * P.npix - 1), scr);
       if (tid == 0) P.ent[pr.slot] = e;
     } else {
       // flush into the pair's global histogram and publish the summary
@@ -385,7 +453,7 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
 // was split over several CTAs (or whose histogram the caller wants).
 __global__ void __launch_bounds__(kEntropyThreads) judge_finalize_kernel(const JudgeParams P) {
   __shared__ int s_first[256], s_last[256];
-  __shared__ Fix192 s_red[kEntropyThreads / 32];
+  __shared__ NpScratch scr;
   const PairRef pr = pair_ref(P, blockIdx.x);
   uint32_t *G = P.ghist + (size_t)pr.slot * 65536;
   const int16_t *sum = P.segsum + (size_t)pr.slot * P.S * 512;
@@ -413,7 +481,7 @@ __global__ void __launch_bounds__(kEntropyThreads) judge_finalize_kernel(const J
   __threadfence();
   __syncthreads();
   auto get = [&](int bin) -> double { return (double)__ldcg(G + bin); };
-  const double e = block_entropy(get, (double)(2 * P.npix - 1), s_red);
+  const double e = block_entropy(get, (double)(2 * P.npix - 1), scr);
   if (threadIdx.x == 0) P.ent[pr.slot] = e;
 }
 
@@ -505,9 +573,9 @@ __global__ void bwt_scatter_kernel(const uint8_t *s, int64_t n, int64_t nchunks,
 }
 
 __global__ void entropy_u64_kernel(const uint64_t *counts, double total, double *out) {
-  __shared__ Fix192 s_red[kEntropyThreads / 32];
+  __shared__ NpScratch scr;
   auto get = [&](int bin) -> double { return (double)counts[bin]; };
-  const double e = block_entropy(get, total, s_red);
+  const double e = block_entropy(get, total, scr);
   if (threadIdx.x == 0) *out = e;
 }
 
