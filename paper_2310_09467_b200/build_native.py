@@ -17,8 +17,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_native"
 LIB = OUT_DIR / "libpcbz_b200.so"
-SOURCES = ["judge.cu", "capi.cu"]
-HEADERS = ["judge.cuh", ROOT / "include" / "pcbz_b200.h"]
+SOURCES = ["judge.cu", "aux_kernels.cu", "capi.cu"]
+HEADERS = ["judge.cuh", "common.cuh", "entropy.cuh", ROOT / "include" / "pcbz_b200.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

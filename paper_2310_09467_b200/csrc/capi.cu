@@ -25,6 +25,7 @@ thread_local int g_launches = 0;
 struct TimedCall { cudaEvent_t e0, e1, e2; int launches; };
 thread_local std::vector<TimedCall> g_timed;
 thread_local int g_seg_override = 0;
+thread_local bool g_fast_enabled = true;
 
 int fail(int code, const char *fmt, ...) {
   char buf[512];
@@ -172,6 +173,9 @@ int make_plan(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py, con
     return fail(PCBZ_E_INVALID, "segment override %d leaves segments above %lld pixels", jp.S,
                 (long long)kMaxSegPixels);
   jp.direct = (jp.S == 1 && !want_hist) ? 1 : 0;
+  // 8-pixel chunk path: rows of whole chunks and a pitch the fast kernel is
+  // instantiated for (pointer alignment is re-checked in run_plan)
+  jp.fast_px = (w % 8 == 0 && px <= kMaxFastPitch && g_fast_enabled) ? (int)px : 0;
   const int64_t items = jp.npairs * jp.S;
   pl.grid = (int)std::min<int64_t>(items, num_sms_cached());
   size_t off = 0;
@@ -193,6 +197,8 @@ int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double 
   char *ws = static_cast<char *>(d_ws);
   jp.frames = d_frames;
   jp.halo = d_halo;
+  if ((reinterpret_cast<uintptr_t>(d_frames) | reinterpret_cast<uintptr_t>(d_halo)) & 15)
+    jp.fast_px = 0;  // 128-bit loads need 16-byte aligned frames
   jp.ent = d_ent;
   jp.counter = reinterpret_cast<int *>(ws + pl.off_counter);
   jp.err = reinterpret_cast<int *>(ws + pl.off_err);

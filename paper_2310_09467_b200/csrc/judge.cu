@@ -1,282 +1,42 @@
-// judge.cu -- sm_100a kernels of the entropy-judgement stage.
+// judge.cu -- sm_100a kernels of the entropy judge.
 //
 // Semantics follow the reference's fused kernel residual_bwt_pair_hist
 // (pkg/src/pcbz/_kernels.py:157-204) and criterion.select_predictor
-// (criterion.py:136-173); the parallel decomposition is new (DESIGN.md):
+// (criterion.py:136-173); the parallel decomposition is new (DESIGN.md §3):
 //
 //   * the packed residual stream of one (frame, candidate) pair is cut into
 //     segments; one CTA owns a segment, each of its 192 threads owns a
 //     contiguous run of pixels and runs the reference's per-key chain
 //     automaton (_kernels.py:192-201) on it with a lane-private last-pred
-//     table in shared memory (no cross-lane communication in the hot loop);
+//     table in shared memory -- no cross-lane communication in the hot loop
+//     (warp-cooperative matching with __match_any_sync measured 12x slower
+//     than a shared atomic on B200, profiles/r01_microbench_atoms_match.log);
+//   * fast path (width % 8 == 0, pitch_x <= 16): each lane walks its run in
+//     8-pixel chunks with 128-bit read-only loads of the rows it needs and
+//     carries left-neighbour history in registers; the pitch is a template
+//     parameter, so lenslet-stride neighbours are static register picks;
 //   * pair increments go to a CTA-private 65,536-bin histogram of packed u16
-//     counters in shared memory (128 KiB); a bin that reaches 0x8000 spills
-//     0x8000 into a small list, so no count is ever lost;
+//     counters in shared memory (128 KiB); a counter reaching 0x8000 is
+//     spilled exactly once (atomicAnd claim) into a small list;
 //   * runs are stitched in stream order through their (first, last) pred per
-//     key -- the associative segment summary of SURVEY.md Appendix A -- first
-//     inside the CTA, then across segments in judge_finalize_kernel;
+//     key, inside the CTA and then across segments;
 //   * the bucket seams of _stitch_buckets (_kernels.py:125-133) close the
-//     histogram, and the fp64 entropy (criterion.py:86-96) is reduced in a
-//     fixed order by every path, so identical histograms give identical bits.
-#include "judge.cuh"
+//     histogram; entropy.cuh reduces it exactly like the reference's numpy.
+#include <utility>
 
-#include <cub/device/device_scan.cuh>
+#include "common.cuh"
+#include "entropy.cuh"
 
 namespace pcbz {
 
 // ---------------------------------------------------------------------------
-// residuals
-// ---------------------------------------------------------------------------
-
-// Source sample: the frame itself or, for temporal candidates, the modular
-// delta against the previous original frame (predictors.py:116-120).
-__device__ __forceinline__ int sample_at(const uint16_t *__restrict__ s,
-                                         const uint16_t *__restrict__ p, int64_t idx) {
-  int v = __ldg(s + idx);
-  if (p) v = (v - (int)__ldg(p + idx)) & 0xFFFF;
-  return v;
-}
-
-// f1..f4 on a neighbour triple; '>> 1' on int32 is floor division for any
-// sign, as in the reference (_kernels.py:5-7,31-43).
-__device__ __forceinline__ int predict_f(int a, int b, int c, int f) {
-  switch (f) {
-    case 1: return a + b - c;
-    case 2: return a + ((b - c) >> 1);
-    case 3: return b + ((a - c) >> 1);
-    default: return (a + b) >> 1;
-  }
-}
-
-__device__ __forceinline__ int predict_at(const uint16_t *s, const uint16_t *p, int W, int y, int x,
-                                          int sx, int sy, int f) {
-  const int64_t row = (int64_t)y * W;
-  const bool left = x >= sx, top = y >= sy;
-  const int a = left ? sample_at(s, p, row + x - sx) : 0;
-  const int b = top ? sample_at(s, p, row - (int64_t)sy * W + x) : 0;
-  const int c = (left && top) ? sample_at(s, p, row - (int64_t)sy * W + x - sx) : 0;
-  return predict_f(a, b, c, f);
-}
-
-// One residual symbol (_kernels.py:60-65, 179-186).
-__device__ __forceinline__ uint32_t residual_at(const uint16_t *s, const uint16_t *p, int W, int y,
-                                                int x, const PredCfg &c) {
-  const int X = sample_at(s, p, (int64_t)y * W + x);
-  if (c.grp < 0) return (uint32_t)X;
-  int pr = predict_at(s, p, W, y, x, c.sx, c.sy, c.f);
-  if (c.grp == 2) pr = (pr + predict_at(s, p, W, y, x, 1, 1, c.f)) >> 1;
-  return (uint32_t)(X - pr) & 0xFFFFu;
-}
-
-// ---------------------------------------------------------------------------
-// shared histogram of packed u16 counters with spill list
-// ---------------------------------------------------------------------------
-
-struct SmemHist {
-  uint32_t *bins;    // kHistWords
-  uint32_t *spill;   // kSpillCap
-  int *nspill;
-  int *err;
-
-  // Add 1 to `bin`.  Exactly one increment observes the 0x7FFF -> 0x8000
-  // crossing of a counter (adds are +1 and the only subtraction is made by
-  // that observer), so each crossing spills once and a half never exceeds
-  // 0x8000 + (increments in flight), far below 0xFFFF.
-  __device__ __forceinline__ void inc(uint32_t bin) const {
-    const uint32_t sh = (bin & 1u) << 4;
-    const uint32_t old = atomicAdd(&bins[bin >> 1], 1u << sh);
-    if (((old >> sh) & 0xFFFFu) == kSpill - 1) spill_one(bin, sh);
-  }
-  __device__ __noinline__ void spill_one(uint32_t bin, uint32_t sh) const {
-    atomicSub(&bins[bin >> 1], kSpill << sh);
-    const int i = atomicAdd(nspill, 1);
-    if (i < kSpillCap) spill[i] = bin;
-    else atomicExch(err, 2);
-  }
-};
-
-// ---------------------------------------------------------------------------
-// deterministic fp64 entropy: -sum p*log2(p), p = c / total (criterion.py:86-96)
-// ---------------------------------------------------------------------------
-
-// Entropy exactly as the reference evaluates it (criterion.py:86-96):
-//     p = counts[counts > 0] / float(total);  E = -(p * np.log2(p)).sum()
-// i.e. terms t_i = p_i * log2(p_i) over the occupied bins IN BIN ORDER,
-// summed with numpy's pairwise summation (blocks of <= 128 elements with
-// eight accumulators, split at n/2 rounded down to a multiple of 8; verified
-// bit-for-bit against np.sum for n = 1..65536).  The result
-// is therefore bit-identical to the reference whenever the device log2
-// rounds like numpy's (both are correctly rounded for nearly all inputs),
-// and ties between candidates resolve exactly as in the reference.
-//
-// Parallel form: every thread owns a contiguous bin range; a block scan of
-// per-range occupied counts gives each occupied bin its index in the
-// compacted term array; the recursion's leaves (index ranges) are evaluated
-// by different threads; one thread then folds the leaf sums in recursion
-// order.
-constexpr int kNpLeafMax = 1024;  // leaves hold >= 64 terms once n > 128
-constexpr int kNpBlock = 128;     // numpy PW_BLOCKSIZE
-
-struct NpScratch {
-  uint32_t off[kEntropyThreads + 1];  // compacted index of each range's first term
-  uint32_t leaf_beg[kNpLeafMax];
-  uint32_t leaf_len[kNpLeafMax];
-  double leaf_sum[kNpLeafMax];
-  int nleaf;
-};
-constexpr size_t kNpScratchBytes = sizeof(NpScratch);
-
-__device__ __forceinline__ int range_lo(int t) { return (int)((65536LL * t) / kEntropyThreads); }
-
-// leaves of numpy's pairwise recursion over [beg, beg + n), in DFS order
-__device__ void np_enumerate_leaves(uint32_t beg, uint32_t n, NpScratch &S) {
-  uint32_t st_b[40], st_n[40];
-  int sp = 0, nl = 0;
-  st_b[sp] = beg; st_n[sp] = n; ++sp;
-  while (sp) {
-    --sp;
-    const uint32_t b = st_b[sp], m = st_n[sp];
-    if (m <= (uint32_t)kNpBlock) {
-      S.leaf_beg[nl] = b; S.leaf_len[nl] = m; ++nl;
-    } else {
-      uint32_t h = m / 2;
-      h -= h % 8;
-      st_b[sp] = b + h; st_n[sp] = m - h; ++sp;  // right half after the left one
-      st_b[sp] = b; st_n[sp] = h; ++sp;
-    }
-  }
-  S.nleaf = nl;
-}
-
-// fold leaf sums in the recursion's order: sum(a, n) = sum(left) + sum(right)
-__device__ double np_fold(uint32_t n, const NpScratch &S) {
-  // iterative post-order over the same split tree; leaves are consumed in DFS order
-  uint32_t st_n[40];
-  uint8_t st_state[40];
-  double st_left[40];
-  int sp = 0, leaf = 0;
-  double ret = 0.0;
-  st_n[0] = n; st_state[0] = 0; sp = 1;
-  bool have_ret = false;
-  while (sp) {
-    const int top = sp - 1;
-    const uint32_t m = st_n[top];
-    if (m <= (uint32_t)kNpBlock) {
-      ret = S.leaf_sum[leaf++];
-      have_ret = true;
-      --sp;
-      continue;
-    }
-    uint32_t h = m / 2;
-    h -= h % 8;
-    if (st_state[top] == 0) {          // descend left
-      st_state[top] = 1;
-      st_n[sp] = h; st_state[sp] = 0; ++sp;
-      have_ret = false;
-    } else if (st_state[top] == 1) {   // left done -> descend right
-      st_left[top] = ret;
-      st_state[top] = 2;
-      st_n[sp] = m - h; st_state[sp] = 0; ++sp;
-      have_ret = false;
-    } else {                           // both done
-      ret = st_left[top] + ret;
-      have_ret = true;
-      --sp;
-    }
-  }
-  (void)have_ret;
-  return ret;
-}
-
-template <typename Get>
-__device__ double block_entropy(Get get, double total, NpScratch &S) {
-  const int t = threadIdx.x;
-  const int lo = range_lo(t), hi = range_lo(t + 1);
-  uint32_t cnt = 0;
-  if (total > 0.0)
-    for (int b = lo; b < hi; ++b) cnt += get(b) > 0.0;
-  // block exclusive scan of cnt (kEntropyThreads = 6 warps)
-  uint32_t incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-    if ((t & 31) >= o) incl += v;
-  }
-  __syncthreads();
-  if ((t & 31) == 31) S.off[t >> 5] = incl;   // warp totals (temporarily)
-  __syncthreads();
-  uint32_t warp_base = 0;
-  for (int w = 0; w < (t >> 5); ++w) warp_base += S.off[w];
-  uint32_t n_all = 0;
-  for (int w = 0; w < kEntropyThreads / 32; ++w) n_all += S.off[w];
-  __syncthreads();
-  S.off[t] = warp_base + incl - cnt;
-  if (t == 0) {
-    S.off[kEntropyThreads] = n_all;
-    if (n_all > 0) np_enumerate_leaves(0, n_all, S);
-    else S.nleaf = 0;
-  }
-  __syncthreads();
-  const int nleaf = S.nleaf;
-  for (int L = t; L < nleaf; L += kEntropyThreads) {
-    const uint32_t beg = S.leaf_beg[L], len = S.leaf_len[L];
-    // owner range of compacted index `beg`: last r with off[r] <= beg
-    int r0 = 0, r1 = kEntropyThreads - 1;
-    while (r0 < r1) {
-      const int mid = (r0 + r1 + 1) >> 1;
-      if (S.off[mid] <= beg) r0 = mid; else r1 = mid - 1;
-    }
-    int b = range_lo(r0);
-    uint32_t idx = S.off[r0];
-    // advance to the beg-th occupied bin
-    double c = get(b);
-    while (!(c > 0.0) || idx < beg) {
-      if (c > 0.0) ++idx;
-      ++b;
-      c = get(b);
-    }
-    auto next_term = [&]() -> double {  // term of the current occupied bin, then advance
-      const double p = c / total;
-      const double v = p * log2(p);
-      ++b;
-      while (b < 65536 && !((c = get(b)) > 0.0)) ++b;
-      return v;
-    };
-    double res;
-    if (len < 8) {
-      res = -0.0;
-      for (uint32_t i = 0; i < len; ++i) res += next_term();
-    } else {
-      double r[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = next_term();
-      uint32_t i = 8;
-      for (; i < len - (len % 8); i += 8) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] += next_term();
-      }
-      res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-      for (; i < len; ++i) res += next_term();
-    }
-    S.leaf_sum[L] = res;
-  }
-  __syncthreads();
-  __shared__ double s_result;
-  if (t == 0) s_result = (total > 0.0 && n_all > 0) ? -np_fold(n_all, S) : 0.0;
-  __syncthreads();
-  const double e = s_result;
-  __syncthreads();
-  return e;
-}
-
-// ---------------------------------------------------------------------------
-// pair -> (frame, candidate) mapping
+// pair -> (frame, candidate)
 // ---------------------------------------------------------------------------
 
 struct PairRef {
   int64_t frame;
-  int spec;   // predictor byte
-  int64_t slot;   // frame * k + index in the full list
+  int spec;      // predictor byte
+  int64_t slot;  // frame * k + index in the full candidate list
 };
 
 __device__ __forceinline__ PairRef pair_ref(const JudgeParams &P, int64_t pair) {
@@ -295,31 +55,249 @@ __device__ __forceinline__ PairRef pair_ref(const JudgeParams &P, int64_t pair) 
   return r;
 }
 
-__device__ __forceinline__ const uint16_t *prev_of(const uint16_t *frames, const uint16_t *halo,
-                                                   int64_t npix, int64_t frame) {
-  return frame > 0 ? frames + (frame - 1) * npix : halo;
+// ---------------------------------------------------------------------------
+// chain state of one lane
+// ---------------------------------------------------------------------------
+
+struct ChainState {
+  uint32_t *hist;   // shared, kHistWords packed u16 counters
+  uint32_t lbase;   // shared address of this lane's last-pred column
+  uint8_t *F;       // this lane's first-pred row (global scratch)
+  uint32_t *spill;  // shared spill list
+  int *nspill;
+  int *err;
+};
+
+// One stream byte as an event (key, pred) of the reference automaton
+// (_kernels.py:192-201): pair with the pred of the previous event of the same
+// key, or remember pred as the key's first.  The last-pred entry is a u16
+// (0x100 = unseen) read and overwritten with independent 16-bit accesses, so
+// consecutive events do not wait on each other's shared-memory latency.
+// Returns the incremented bin (or ~0u) and ORs the counter's toggled bits
+// into `flag`: bit 15 of a half toggles exactly when that counter crosses
+// 0x7FFF -> 0x8000.
+__device__ __forceinline__ uint32_t chain_event(const ChainState &cs, uint32_t key, uint32_t pred,
+                                                uint32_t &flag) {
+  const uint32_t a = cs.lbase + (key >> 1) * (4u * kJudgeThreads) + ((key & 1u) << 1);
+  uint32_t last;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(last) : "r"(a));
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(pred));
+  if (last == kUnseen) {
+    cs.F[key] = (uint8_t)pred;
+    return ~0u;
+  }
+  const uint32_t bin = (last << 8) | pred;
+  const uint32_t inc = 1u << ((pred & 1u) << 4);
+  const uint32_t old = atomicAdd(&cs.hist[bin >> 1], inc);
+  flag |= old ^ (old + inc);
+  return bin;
+}
+
+// Move 0x8000 out of `bin`'s counter if its bit 15 is set.  atomicAnd makes
+// exactly one claimant per crossing; counts are never lost or doubled.
+__device__ __forceinline__ void claim_spill(const ChainState &cs, uint32_t bin) {
+  if (bin == ~0u) return;
+  const uint32_t m = 0x8000u << ((bin & 1u) << 4);
+  const uint32_t old = atomicAnd(&cs.hist[bin >> 1], ~m);
+  if (old & m) {
+    const int i = atomicAdd(cs.nspill, 1);
+    if (i < kSpillCap) cs.spill[i] = bin;
+    else atomicExch(cs.err, 2);
+  }
+}
+
+// increment outside the hot loop (stitching): claim immediately
+__device__ __forceinline__ void hist_inc_now(const ChainState &cs, uint32_t bin) {
+  const uint32_t inc = 1u << ((bin & 1u) << 4);
+  const uint32_t old = atomicAdd(&cs.hist[bin >> 1], inc);
+  if ((old ^ (old + inc)) & 0x80008000u) claim_spill(cs, bin);
 }
 
 // ---------------------------------------------------------------------------
-// the judge kernel: one CTA per (pair, segment) item, dynamically scheduled
+// generic lane: any width / pitch, one pixel at a time
 // ---------------------------------------------------------------------------
 
+__device__ void lane_generic(const uint16_t *src, const uint16_t *prv, const PredCfg &cfg, int W,
+                             int64_t npix, int64_t a, int64_t b, const ChainState &cs) {
+  if (a >= b) return;
+  const int64_t q = a > 0 ? a - 1 : npix - 1;  // wrap predecessor (_kernels.py:172-190)
+  uint32_t prev_lo = residual_at(src, prv, W, (int)(q / W), (int)(q % W), cfg) & 0xFFu;
+  int y = (int)(a / W), x = (int)(a % W);
+  uint32_t flag = 0;
+  for (int64_t k = a; k < b; ++k) {
+    const uint32_t r = residual_at(src, prv, W, y, x, cfg);
+    const uint32_t hi = r >> 8, lo = r & 0xFFu;
+    const uint32_t b0 = chain_event(cs, hi, prev_lo, flag);
+    const uint32_t b1 = chain_event(cs, lo, hi, flag);
+    if (flag & 0x80008000u) {
+      claim_spill(cs, b0);
+      claim_spill(cs, b1);
+    }
+    flag = 0;
+    prev_lo = lo;
+    if (++x == W) { x = 0; ++y; }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fast lane: 8-pixel chunks, 128-bit loads, register neighbour history
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint4 ld_chunk(const uint16_t *__restrict__ s,
+                                          const uint16_t *__restrict__ p, int64_t off) {
+  uint4 a = __ldg(reinterpret_cast<const uint4 *>(s + off));
+  if (p) {
+    const uint4 b = __ldg(reinterpret_cast<const uint4 *>(p + off));
+    a.x = sub16x2(a.x, b.x); a.y = sub16x2(a.y, b.y);
+    a.z = sub16x2(a.z, b.z); a.w = sub16x2(a.w, b.w);
+  }
+  return a;
+}
+
+__device__ __forceinline__ void unpack8(const uint4 &w, int (&v)[8]) {
+  v[0] = w.x & 0xFFFF; v[1] = w.x >> 16; v[2] = w.y & 0xFFFF; v[3] = w.y >> 16;
+  v[4] = w.z & 0xFFFF; v[5] = w.z >> 16; v[6] = w.w & 0xFFFF; v[7] = w.w >> 16;
+}
+
+// f1..f4 as base + ((u - v) >> k) with uniform selectors:
+// f1 (A,B,C,0)  f2 (A,B,C,1)  f3 (B,A,C,1)  f4 (A,B,A,1) -- f4 = A + floor((B-A)/2)
+struct FSel {
+  bool f3, f4;
+  int k;
+};
+
+__device__ __forceinline__ int pred_sel(int A, int B, int C, const FSel &fs) {
+  const int base = fs.f3 ? B : A;
+  const int u = fs.f3 ? A : B;
+  const int v = fs.f4 ? A : C;
+  return base + ((u - v) >> fs.k);
+}
+
+template <int PX, int GRP>
+__device__ void lane_fast(const uint16_t *__restrict__ src, const uint16_t *__restrict__ prv,
+                          const FSel fs, int W, int py, int64_t npix, int64_t a, int64_t nch,
+                          const PredCfg &cfg, const ChainState &cs) {
+  constexpr bool kT1 = GRP == 0 || GRP == 2;  // row y-1   (pixel-adjacent B, C)
+  constexpr bool kTS = GRP == 1 || GRP == 2;  // row y-py  (lenslet B, C)
+  constexpr bool kXH = GRP >= 0;              // left history of row y
+  constexpr bool kXH2 = (GRP == 1 || GRP == 2) && PX > 8;
+  if (nch <= 0) return;
+  const int64_t q = a > 0 ? a - 1 : npix - 1;  // wrap predecessor (_kernels.py:172-190)
+  uint32_t prev_lo = residual_at(src, prv, W, (int)(q / W), (int)(q % W), cfg) & 0xFFu;
+  int y = (int)(a / W), x0 = (int)(a % W);
+  const uint4 Z = make_uint4(0, 0, 0, 0);
+  auto row = [&](int yy) -> int64_t { return (int64_t)yy * W; };
+  uint4 Xh1 = Z, Xh2 = Z, T1h = Z, TSh1 = Z, TSh2 = Z;
+  if (x0 > 0) {  // history of a run that starts mid-row
+    if (kXH) Xh1 = ld_chunk(src, prv, row(y) + x0 - 8);
+    if (kXH2 && x0 >= 16) Xh2 = ld_chunk(src, prv, row(y) + x0 - 16);
+    if (kT1 && y >= 1) T1h = ld_chunk(src, prv, row(y - 1) + x0 - 8);
+    if (kTS && y >= py) {
+      TSh1 = ld_chunk(src, prv, row(y - py) + x0 - 8);
+      if (kXH2 && x0 >= 16) TSh2 = ld_chunk(src, prv, row(y - py) + x0 - 16);
+    }
+  }
+  uint4 cX = ld_chunk(src, prv, row(y) + x0);
+  uint4 cT1 = (kT1 && y >= 1) ? ld_chunk(src, prv, row(y - 1) + x0) : Z;
+  uint4 cTS = (kTS && y >= py) ? ld_chunk(src, prv, row(y - py) + x0) : Z;
+  uint32_t flag = 0;
+  for (int64_t c = 0; c < nch; ++c) {
+    int ny = y, nx = x0 + 8;
+    if (nx == W) { nx = 0; ++ny; }
+    uint4 nX = Z, nT1 = Z, nTS = Z;
+    if (c + 1 < nch) {  // prefetch the next chunk
+      nX = ld_chunk(src, prv, row(ny) + nx);
+      if (kT1 && ny >= 1) nT1 = ld_chunk(src, prv, row(ny - 1) + nx);
+      if (kTS && ny >= py) nTS = ld_chunk(src, prv, row(ny - py) + nx);
+    }
+    int X[8], T1[8], TS[8], H1[8], H2[8], S1[8], S2[8], t1h[8];
+    unpack8(cX, X);
+    if (kT1) { unpack8(cT1, T1); unpack8(T1h, t1h); }
+    if (kTS) { unpack8(cTS, TS); unpack8(TSh1, S1); }
+    if (kXH) unpack8(Xh1, H1);
+    if (kXH2) { unpack8(Xh2, H2); unpack8(TSh2, S2); }
+    uint32_t r[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if constexpr (GRP < 0) {
+        r[i] = (uint32_t)X[i];
+      } else {
+        int p = 0, p1 = 0;
+        if constexpr (kT1) {  // pixel-adjacent neighbours (1, 1)
+          const int A = i ? X[i - 1] : H1[7];
+          const int C = i ? T1[i - 1] : t1h[7];
+          p1 = pred_sel(A, T1[i], C, fs);
+        }
+        if constexpr (kTS) {  // lenslet-stride neighbours (PX, py)
+          const int qq = i - PX;
+          int A, C;
+          if (qq >= 0) { A = X[qq]; C = TS[qq]; }
+          else if (qq >= -8) { A = H1[qq + 8]; C = S1[qq + 8]; }
+          else { A = H2[qq + 16]; C = S2[qq + 16]; }
+          const int p2 = pred_sel(A, TS[i], C, fs);
+          p = GRP == 2 ? ((p1 + p2) >> 1) : p2;  // phase group averages (_kernels.py:63-64)
+        } else {
+          p = p1;
+        }
+        r[i] = (uint32_t)(X[i] - p) & 0xFFFFu;
+      }
+    }
+    uint32_t bins[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t hi = r[i] >> 8, lo = r[i] & 0xFFu;
+      bins[2 * i] = chain_event(cs, hi, prev_lo, flag);
+      bins[2 * i + 1] = chain_event(cs, lo, hi, flag);
+      prev_lo = lo;
+    }
+    if (flag & 0x80008000u) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) claim_spill(cs, bins[e]);
+    }
+    flag = 0;
+    if (nx == 0) {
+      Xh1 = Xh2 = T1h = TSh1 = TSh2 = Z;  // new row: left neighbours are 0
+    } else {
+      Xh2 = Xh1; Xh1 = cX; T1h = cT1; TSh2 = TSh1; TSh1 = cTS;
+    }
+    y = ny; x0 = nx;
+    cX = nX; cT1 = nT1; cTS = nTS;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the judge kernel: persistent CTAs pull (pair, segment) items
+// ---------------------------------------------------------------------------
+//
+// dynamic shared memory:
+//   hist   kHistWords            packed u16 counters
+//   last   kLastWords * 192      last-pred tables, word (key>>1)*192 + lane
+//   spill  kSpillCap             spilled bins
+// after the hot loop the last-pred region is reused for the spilled-bin
+// bitmap (words [0, 2048)), first/last per key ([2048, 2560)) and the
+// entropy scratch ([2560, ...)).
+
+template <int PX>
 __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const JudgeParams P) {
   extern __shared__ uint4 smem_raw[];
   uint32_t *hist_w = reinterpret_cast<uint32_t *>(smem_raw);
-  uint32_t *last_w = hist_w + kHistWords;                 // [kLastWords][kJudgeThreads]
+  uint32_t *last_w = hist_w + kHistWords;
   uint32_t *spill_w = last_w + kLastWords * kJudgeThreads;
   __shared__ int s_item, s_nspill;
-  // after the stitch the last-pred tables are dead: words [0, 2048) become the
-  // spilled-bin bitmap, [2048, 2560) the CTA's first/last pred per key
   int *s_first = reinterpret_cast<int *>(last_w) + 2048;
   int *s_last = s_first + 256;
+  NpScratch &scr = *reinterpret_cast<NpScratch *>(last_w + 2560);
 
   const int tid = threadIdx.x;
   const int64_t nitems = P.npairs * P.S;
-  const SmemHist H{hist_w, spill_w, &s_nspill, P.err};
-  uint8_t *Fcta = P.fscratch + (size_t)blockIdx.x * kJudgeThreads * 256;
-  uint8_t *Flane = Fcta + (size_t)tid * 256;
+  ChainState cs;
+  cs.hist = hist_w;
+  cs.lbase = (uint32_t)__cvta_generic_to_shared(last_w + tid);
+  cs.F = P.fscratch + ((size_t)blockIdx.x * kJudgeThreads + tid) * 256;
+  cs.spill = spill_w;
+  cs.nspill = &s_nspill;
+  cs.err = P.err;
+  const uint8_t *Fcta = P.fscratch + (size_t)blockIdx.x * kJudgeThreads * 256;
   uint32_t *Llane = last_w + tid;
 
   for (;;) {
@@ -340,44 +318,32 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
     const uint16_t *src = P.frames + pr.frame * P.npix;
     const uint16_t *prv = (pr.spec & 0x80) ? prev_of(P.frames, P.halo, P.npix, pr.frame) : nullptr;
     const PredCfg cfg = make_cfg(pr.spec & 0x7F, P.px, P.py);
-    const int W = P.W;
 
-    // ---- this lane's run of pixels [a, b) -----------------------------------
-    const int64_t sb = P.npix * seg / P.S, se = P.npix * (seg + 1) / P.S;
-    const int64_t len = se - sb;
-    const int64_t a = sb + len * tid / kJudgeThreads;
-    const int64_t b = sb + len * (tid + 1) / kJudgeThreads;
-    if (a < b) {
-      // predecessor of the run's first byte: low byte of pixel a-1, or of the
-      // last pixel for the stream's wrap-around (_kernels.py:172-190)
-      const int64_t q = a > 0 ? a - 1 : P.npix - 1;
-      uint32_t prev_lo = residual_at(src, prv, W, (int)(q / W), (int)(q % W), cfg) & 0xFFu;
-      int y = (int)(a / W), x = (int)(a % W);
-      for (int64_t k = a; k < b; ++k) {
-        const uint32_t r = residual_at(src, prv, W, y, x, cfg);
-        const uint32_t hi = r >> 8, lo = r & 0xFFu;
-        // two stream bytes -> two chain events (key, pred) (_kernels.py:192-201)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const uint32_t key = e == 0 ? hi : lo;
-          const uint32_t pred = e == 0 ? prev_lo : hi;
-          uint32_t *wp = Llane + (key >> 1) * kJudgeThreads;
-          const uint32_t sh = (key & 1u) << 4;
-          const uint32_t wv = *wp;
-          const uint32_t last = (wv >> sh) & 0xFFFFu;
-          *wp = (wv & ~(0xFFFFu << sh)) | (pred << sh);
-          if (last == kUnseen) Flane[key] = (uint8_t)pred;
-          else H.inc((last << 8) | pred);
-        }
-        prev_lo = lo;
-        if (++x == W) { x = 0; ++y; }
+    if constexpr (PX > 0) {
+      // chunk-granular segments and runs
+      const int64_t nchunk = P.npix / 8;
+      const int64_t cb = nchunk * seg / P.S, ce = nchunk * (seg + 1) / P.S;
+      const int64_t ca = cb + (ce - cb) * tid / kJudgeThreads;
+      const int64_t cz = cb + (ce - cb) * (tid + 1) / kJudgeThreads;
+      const int fn = cfg.f;
+      const FSel fs{fn == 3, fn == 4, fn == 1 ? 0 : 1};
+      switch (cfg.grp) {
+        case -1: lane_fast<PX, -1>(src, prv, fs, P.W, P.py, P.npix, ca * 8, cz - ca, cfg, cs); break;
+        case 0: lane_fast<PX, 0>(src, prv, fs, P.W, P.py, P.npix, ca * 8, cz - ca, cfg, cs); break;
+        case 1: lane_fast<PX, 1>(src, prv, fs, P.W, P.py, P.npix, ca * 8, cz - ca, cfg, cs); break;
+        default: lane_fast<PX, 2>(src, prv, fs, P.W, P.py, P.npix, ca * 8, cz - ca, cfg, cs); break;
       }
+    } else {
+      const int64_t sb = P.npix * seg / P.S, se = P.npix * (seg + 1) / P.S;
+      const int64_t len = se - sb;
+      lane_generic(src, prv, cfg, P.W, P.npix, sb + len * tid / kJudgeThreads,
+                   sb + len * (tid + 1) / kJudgeThreads, cs);
     }
     __syncthreads();
 
-    // ---- stitch the 192 runs in stream order (segment-summary combine) -------
-    int my_first[2] = {-1, -1}, my_last[2] = {-1, -1};
-    for (int v = tid; v < 256; v += kJudgeThreads) {
+    // ---- stitch the 192 runs in stream order (segment-summary combine) -----
+    int my_first0 = -1, my_last0 = -1, my_first1 = -1, my_last1 = -1;
+    for (int v = tid, i = 0; v < 256; v += kJudgeThreads, ++i) {
       int carried = -1, first = -1;
       const uint32_t *col = last_w + (v >> 1) * kJudgeThreads;
       const uint32_t sh = (v & 1) << 4;
@@ -385,18 +351,20 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
         const uint32_t e = (col[j] >> sh) & 0xFFFFu;
         const uint32_t f = Fcta[(size_t)j * 256 + v];
         if (e != kUnseen) {
-          if (carried >= 0) H.inc(((uint32_t)carried << 8) | f);
+          if (carried >= 0) hist_inc_now(cs, ((uint32_t)carried << 8) | f);
           else first = (int)f;
           carried = (int)e;
         }
       }
-      my_first[v >= kJudgeThreads] = first;
-      my_last[v >= kJudgeThreads] = carried;
+      if (i == 0) { my_first0 = first; my_last0 = carried; }
+      else { my_first1 = first; my_last1 = carried; }
     }
     __syncthreads();
-    for (int v = tid, i = 0; v < 256; v += kJudgeThreads, ++i) {
-      s_first[v] = my_first[i];
-      s_last[v] = my_last[i];
+    s_first[tid] = my_first0;
+    s_last[tid] = my_last0;
+    if (tid + kJudgeThreads < 256) {
+      s_first[tid + kJudgeThreads] = my_first1;
+      s_last[tid + kJudgeThreads] = my_last1;
     }
     __syncthreads();
 
@@ -406,13 +374,13 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
         int carried = -1;
         for (int v = 0; v < 256; ++v) {
           if (s_first[v] < 0) continue;
-          if (carried >= 0) H.inc(((uint32_t)carried << 8) | (uint32_t)s_first[v]);
+          if (carried >= 0) hist_inc_now(cs, ((uint32_t)carried << 8) | (uint32_t)s_first[v]);
           carried = s_last[v];
         }
       }
       __syncthreads();
-      // ... spilled bins marked in a bitmap (reuses the dead last-pred tables)
-      uint32_t *spilled = last_w;  // 2048 words
+      // ... spilled bins marked in a bitmap, then the entropy
+      uint32_t *spilled = last_w;
       for (int i = tid; i < 2048; i += kJudgeThreads) spilled[i] = 0;
       __syncthreads();
       const int ns = min(s_nspill, kSpillCap);
@@ -421,12 +389,10 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
       __syncthreads();
       auto get = [&](int bin) -> double {
         uint32_t c = (hist_w[bin >> 1] >> ((bin & 1) << 4)) & 0xFFFFu;
-        if (spilled[bin >> 5] & (1u << (bin & 31))) {
+        if (spilled[bin >> 5] & (1u << (bin & 31)))
           for (int i = 0; i < ns; ++i) c += spill_w[i] == (uint32_t)bin ? kSpill : 0u;
-        }
         return (double)c;
       };
-      NpScratch &scr = *reinterpret_cast<NpScratch *>(last_w + 2560);
       const double e = block_entropy(get, (double)(2 * P.npix - 1), scr);
       if (tid == 0) P.ent[pr.slot] = e;
     } else {
@@ -449,11 +415,18 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
   }
 }
 
-// Cross-segment stitch, bucket seams and entropy of each pair whose stream
-// was split over several CTAs (or whose histogram the caller wants).
-__global__ void __launch_bounds__(kEntropyThreads) judge_finalize_kernel(const JudgeParams P) {
-  __shared__ int s_first[256], s_last[256];
-  __shared__ NpScratch scr;
+// ---------------------------------------------------------------------------
+// cross-segment stitch + bucket seams + entropy (one CTA per pair)
+// ---------------------------------------------------------------------------
+
+constexpr size_t kFinalizeSmemBytes = 65536 * sizeof(uint16_t) + sizeof(NpScratch) + 2048;
+
+__global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(const JudgeParams P) {
+  extern __shared__ uint4 smem_raw[];
+  uint16_t *c16 = reinterpret_cast<uint16_t *>(smem_raw);
+  NpScratch &scr = *reinterpret_cast<NpScratch *>(c16 + 65536);
+  int *s_first = reinterpret_cast<int *>(reinterpret_cast<char *>(&scr) + sizeof(NpScratch));
+  int *s_last = s_first + 256;
   const PairRef pr = pair_ref(P, blockIdx.x);
   uint32_t *G = P.ghist + (size_t)pr.slot * 65536;
   const int16_t *sum = P.segsum + (size_t)pr.slot * P.S * 512;
@@ -480,7 +453,16 @@ __global__ void __launch_bounds__(kEntropyThreads) judge_finalize_kernel(const J
   }
   __threadfence();
   __syncthreads();
-  auto get = [&](int bin) -> double { return (double)__ldcg(G + bin); };
+  // stage saturated u16 copies of the counts in shared memory
+  for (int b = threadIdx.x; b < 65536; b += kEntropyThreads) {
+    const uint32_t c = __ldcg(G + b);
+    c16[b] = (uint16_t)(c < 0xFFFFu ? c : 0xFFFFu);
+  }
+  __syncthreads();
+  auto get = [&](int bin) -> double {
+    const uint32_t c = c16[bin];
+    return (double)(c < 0xFFFFu ? c : __ldcg(G + bin));
+  };
   const double e = block_entropy(get, (double)(2 * P.npix - 1), scr);
   if (threadIdx.x == 0) P.ent[pr.slot] = e;
 }
@@ -501,226 +483,47 @@ __global__ void judge_select_kernel(const JudgeParams P, uint8_t *sel) {
   sel[f] = f == 0 ? P.cl.byteA[bi] : P.cl.byteB[bi];
 }
 
-// Selected residual stream, row-major, high byte first (core.py:228-237).
-__global__ void emit_kernel(const EmitParams P) {
-  const int64_t total = P.nframes * P.npix;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t f = t / P.npix, k = t - f * P.npix;
-    const int spec = P.sel[f];
-    const uint16_t *src = P.frames + f * P.npix;
-    const uint16_t *prv = (spec & 0x80) ? prev_of(P.frames, P.halo, P.npix, f) : nullptr;
-    const PredCfg cfg = make_cfg(spec & 0x7F, P.px, P.py);
-    const uint32_t r = residual_at(src, prv, P.W, (int)(k / P.W), (int)(k % P.W), cfg);
-    P.stream[2 * t] = (uint8_t)(r >> 8);
-    P.stream[2 * t + 1] = (uint8_t)r;
-  }
-}
-
-__global__ void residual_image_kernel(const uint16_t *img, const uint16_t *prev, int64_t h,
-                                      int64_t w, int spec, int px, int py, uint16_t *out,
-                                      int big_endian) {
-  const int64_t total = h * w;
-  const PredCfg cfg = make_cfg(spec & 0x7F, px, py);
-  const uint16_t *prv = (spec & 0x80) ? prev : nullptr;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t r = residual_at(img, prv, (int)w, (int)(t / w), (int)(t % w), cfg);
-    out[t] = big_endian ? (uint16_t)((r >> 8) | ((r & 0xFFu) << 8)) : (uint16_t)r;
-  }
-}
-
-__global__ void temporal_delta_kernel(const uint16_t *cur, const uint16_t *prev, int64_t n,
-                                      uint16_t *out) {
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x)
-    out[t] = (uint16_t)(cur[t] - prev[t]);
-}
-
-// overlapping byte pairs, first byte high (_kernels.py:116-122)
-__global__ void pair_hist_kernel(const uint8_t *s, int64_t n, uint32_t *hist) {
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t + 1 < n;
-       t += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&hist[((uint32_t)s[t] << 8) | s[t + 1]], 1u);
-}
-
-// ---- counting_bwt (_kernels.py:93-113) as a stable multi-block counting sort.
-// Chunk c of kBwtChunk bytes: counts[v][c] -> exclusive scan in (v, c) order
-// gives each chunk's first output slot per byte value; a chunk then scatters
-// its predecessors in input order, which keeps the sort stable.
-constexpr int kBwtChunk = 2048;
-
-__global__ void bwt_count_kernel(const uint8_t *s, int64_t n, int64_t nchunks, uint32_t *counts) {
-  __shared__ uint32_t c[256];
-  for (int v = threadIdx.x; v < 256; v += blockDim.x) c[v] = 0;
-  __syncthreads();
-  const int64_t ch = blockIdx.x;
-  const int64_t beg = ch * kBwtChunk, end = min(n, beg + kBwtChunk);
-  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) atomicAdd(&c[s[i]], 1u);
-  __syncthreads();
-  for (int v = threadIdx.x; v < 256; v += blockDim.x) counts[(int64_t)v * nchunks + ch] = c[v];
-}
-
-__global__ void bwt_scatter_kernel(const uint8_t *s, int64_t n, int64_t nchunks,
-                                   const uint32_t *offsets, uint8_t *out) {
-  // one thread per chunk keeps the in-chunk order (not on the timed path)
-  const int64_t ch = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (ch >= nchunks) return;
-  uint32_t pos[256];
-  for (int v = 0; v < 256; ++v) pos[v] = offsets[(int64_t)v * nchunks + ch];
-  const int64_t beg = ch * kBwtChunk, end = min(n, beg + kBwtChunk);
-  for (int64_t i = beg; i < end; ++i) out[pos[s[i]]++] = s[i == 0 ? n - 1 : i - 1];
-}
-
-__global__ void entropy_u64_kernel(const uint64_t *counts, double total, double *out) {
-  __shared__ NpScratch scr;
-  auto get = [&](int bin) -> double { return (double)counts[bin]; };
-  const double e = block_entropy(get, total, scr);
-  if (threadIdx.x == 0) *out = e;
-}
-
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 
-static int grid_for(int64_t n, int threads) {
-  int64_t g = (n + threads - 1) / threads;
-  if (g < 1) g = 1;
-  if (g > 148 * 32) g = 148 * 32;
-  return (int)g;
+template <int... Ps>
+static cudaError_t configure_all(std::integer_sequence<int, Ps...>) {
+  cudaError_t errs[] = {cudaFuncSetAttribute(judge_hist_kernel<Ps>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kJudgeSmemBytes)...};
+  for (cudaError_t e : errs)
+    if (e != cudaSuccess) return e;
+  return cudaSuccess;
 }
 
 cudaError_t judge_configure() {
-  return cudaFuncSetAttribute(judge_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)kJudgeSmemBytes);
+  cudaError_t e = configure_all(std::make_integer_sequence<int, kMaxFastPitch + 1>{});
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(judge_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)kFinalizeSmemBytes);
+}
+
+template <int... Ps>
+static void launch_dispatch(int px, const JudgeParams &p, int grid, cudaStream_t st,
+                            std::integer_sequence<int, Ps...>) {
+  ((px == Ps ? (void)(judge_hist_kernel<Ps><<<grid, kJudgeThreads, kJudgeSmemBytes, st>>>(p))
+             : void()),
+   ...);
 }
 
 cudaError_t launch_judge(const JudgeParams &p, int grid, cudaStream_t st) {
-  judge_hist_kernel<<<grid, kJudgeThreads, kJudgeSmemBytes, st>>>(p);
+  launch_dispatch(p.fast_px, p, grid, st, std::make_integer_sequence<int, kMaxFastPitch + 1>{});
   return cudaGetLastError();
 }
 
 cudaError_t launch_finalize(const JudgeParams &p, cudaStream_t st) {
-  judge_finalize_kernel<<<(unsigned)p.npairs, kEntropyThreads, 0, st>>>(p);
+  judge_finalize_kernel<<<(unsigned)p.npairs, kEntropyThreads, kFinalizeSmemBytes, st>>>(p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_select(const JudgeParams &p, uint8_t *sel, cudaStream_t st) {
   judge_select_kernel<<<(unsigned)((p.nframes + 127) / 128), 128, 0, st>>>(p, sel);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_emit(const EmitParams &p, cudaStream_t st) {
-  emit_kernel<<<grid_for(p.nframes * p.npix, 256), 256, 0, st>>>(p);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_residual_image(const uint16_t *img, const uint16_t *prev, int64_t h, int64_t w,
-                                  int spec, int px, int py, uint16_t *out, int big_endian,
-                                  cudaStream_t st) {
-  residual_image_kernel<<<grid_for(h * w, 256), 256, 0, st>>>(img, prev, h, w, spec, px, py, out,
-                                                              big_endian);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_temporal_delta(const uint16_t *cur, const uint16_t *prev, int64_t n,
-                                  uint16_t *out, cudaStream_t st) {
-  temporal_delta_kernel<<<grid_for(n, 256), 256, 0, st>>>(cur, prev, n, out);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_pair_hist(const uint8_t *s, int64_t n, uint32_t *hist, cudaStream_t st) {
-  pair_hist_kernel<<<grid_for(n, 256), 256, 0, st>>>(s, n, hist);
-  return cudaGetLastError();
-}
-
-size_t counting_bwt_scratch_words(int64_t n) {
-  const int64_t nchunks = (n + kBwtChunk - 1) / kBwtChunk;
-  size_t temp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, temp, (uint32_t *)nullptr, (uint32_t *)nullptr,
-                                (int)(256 * nchunks));
-  return (size_t)(2 * 256 * nchunks) + (temp + 3) / 4 + 4;
-}
-
-cudaError_t launch_counting_bwt(const uint8_t *s, int64_t n, uint8_t *out, uint32_t *scratch,
-                                size_t scratch_words, cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  const int64_t nchunks = (n + kBwtChunk - 1) / kBwtChunk;
-  uint32_t *counts = scratch, *offs = scratch + 256 * nchunks;
-  void *temp = offs + 256 * nchunks;
-  size_t temp_bytes = (scratch_words - 2 * 256 * nchunks) * 4;
-  bwt_count_kernel<<<(unsigned)nchunks, 256, 0, st>>>(s, n, nchunks, counts);
-  cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, counts, offs,
-                                                (int)(256 * nchunks), st);
-  if (e != cudaSuccess) return e;
-  bwt_scatter_kernel<<<(unsigned)((nchunks + 63) / 64), 64, 0, st>>>(s, n, nchunks, offs, out);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_entropy_u64(const uint64_t *counts, double total, double *out,
-                               cudaStream_t st) {
-  entropy_u64_kernel<<<1, kEntropyThreads, 0, st>>>(counts, total, out);
-  return cudaGetLastError();
-}
-
-
-
-// ---------------------------------------------------------------------------
-// decompression side (reference _kernels.py:69-90, predictors.py:101-147)
-// ---------------------------------------------------------------------------
-
-// Inverse intra prediction of one frame per CTA.  Every neighbour of (y, x)
-// lies on an earlier anti-diagonal (x' + y' < x + y), so the CTA sweeps the
-// anti-diagonals in order with a barrier between them.
-__global__ void __launch_bounds__(1024) reconstruct_kernel(const uint16_t *res, int64_t h,
-                                                           int64_t w, int px, int py,
-                                                           const uint8_t *sel, uint16_t *out) {
-  const int64_t f = blockIdx.x;
-  const int64_t npix = h * w;
-  const uint16_t *r = res + f * npix;
-  uint16_t *o = out + f * npix;
-  const PredCfg c = make_cfg(sel[f] & 0x7F, px, py);
-  if (c.grp < 0) {
-    for (int64_t i = threadIdx.x; i < npix; i += blockDim.x) o[i] = r[i];
-    return;
-  }
-  const int W = (int)w;
-  for (int64_t t = 0; t < h + w - 1; ++t) {
-    const int64_t y_lo = t - (w - 1) > 0 ? t - (w - 1) : 0;
-    const int64_t y_hi = t < h - 1 ? t : h - 1;
-    for (int64_t y = y_lo + threadIdx.x; y <= y_hi; y += blockDim.x) {
-      const int x = (int)(t - y);
-      int pr = predict_at(o, nullptr, W, (int)y, x, c.sx, c.sy, c.f);
-      if (c.grp == 2) pr = (pr + predict_at(o, nullptr, W, (int)y, x, 1, 1, c.f)) >> 1;
-      o[y * w + x] = (uint16_t)(r[y * w + x] + pr);
-    }
-    __syncthreads();
-  }
-}
-
-// Temporal undelta chain: frame f = inverse_f (+ frame f-1 if temporal).
-// Pixels are independent, frames are walked in order by every thread.
-__global__ void undelta_chain_kernel(uint16_t *frames, const uint16_t *halo, int64_t nframes,
-                                     int64_t npix, const uint8_t *sel) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npix;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t run = halo ? halo[i] : 0u;
-    for (int64_t f = 0; f < nframes; ++f) {
-      uint32_t v = frames[f * npix + i];
-      if (sel[f] & 0x80) v = (v + run) & 0xFFFFu;
-      frames[f * npix + i] = (uint16_t)v;
-      run = v;
-    }
-  }
-}
-
-cudaError_t launch_reconstruct(const uint16_t *res, const uint16_t *halo, int64_t nframes,
-                               int64_t h, int64_t w, int px, int py, const uint8_t *sel,
-                               uint16_t *out, cudaStream_t st) {
-  reconstruct_kernel<<<(unsigned)nframes, 1024, 0, st>>>(res, h, w, px, py, sel, out);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  undelta_chain_kernel<<<grid_for(h * w, 256), 256, 0, st>>>(out, halo, nframes, h * w, sel);
   return cudaGetLastError();
 }
 

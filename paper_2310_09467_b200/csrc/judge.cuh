@@ -15,6 +15,7 @@ constexpr uint32_t kSpill = 0x8000;            // u16 bin spill threshold
 constexpr int kSpillCap = 512;                 // spill list entries per CTA
 constexpr int64_t kMaxSegPixels = 8000000;     // 2 events/pixel / kSpill < kSpillCap
 constexpr int kEntropyThreads = 192;           // all entropy reductions use this shape
+constexpr int kMaxFastPitch = 16;              // fast path: pitch_x <= 16 (template parameter)
 
 constexpr size_t kJudgeSmemBytes =
     (size_t)(kHistWords + kLastWords * kJudgeThreads + kSpillCap) * sizeof(uint32_t);
@@ -55,6 +56,7 @@ struct JudgeParams {
   int64_t npairs;           // scored (frame, candidate) pairs
   int S;                    // segments per pair
   int direct;               // 1: S == 1 and no histogram output -> entropy in-CTA
+  int fast_px;              // >0: 8-pixel chunk path instantiated for pitch_x; 0: generic
   double *ent;              // [nframes][k] (NaN = not scored)
   uint32_t *ghist;          // [nframes*k][65536] when !direct
   int16_t *segsum;          // [nframes*k][S][2][256] when !direct
