@@ -156,13 +156,15 @@ __device__ double block_entropy(Get get, double total, NpScratch &S) {
       while (!bits) bits = S.occ[++w];
       const int bin = 32 * w + __ffs(bits) - 1;
       bits &= bits - 1;
-      const double p = get(bin) / total;
-      return p * log2(p);
+      // explicit IEEE ops: no FMA contraction may fuse the product into the
+      // running sum (numpy rounds p*log2(p) before summing)
+      const double p = __ddiv_rn(get(bin), total);
+      return __dmul_rn(p, log2(p));
     };
     double res;
     if (len < 8) {
       res = -0.0;
-      for (uint32_t i = 0; i < len; ++i) res += next_term();
+      for (uint32_t i = 0; i < len; ++i) res = __dadd_rn(res, next_term());
     } else {
       double r[8];
 #pragma unroll
@@ -170,10 +172,10 @@ __device__ double block_entropy(Get get, double total, NpScratch &S) {
       uint32_t i = 8;
       for (; i < len - (len % 8); i += 8) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] += next_term();
+        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], next_term());
       }
       res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-      for (; i < len; ++i) res += next_term();
+      for (; i < len; ++i) res = __dadd_rn(res, next_term());
     }
     S.leaf_sum[L] = res;
   }
