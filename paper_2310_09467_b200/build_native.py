@@ -3,6 +3,8 @@
 Used by __graft_entry__.build() and by `python -m paper_2310_09467_b200.build_native`.
 The shared library lands in paper_2310_09467_b200/_native/ so it travels with
 the repository snapshot to the GPU box (it is git-ignored, not gpurun-ignored).
+The histogram kernel is instantiated once per fast-path pitch (judge_px.cu
+with -DPCBZ_PX=0..16); those translation units compile in parallel.
 """
 from __future__ import annotations
 
@@ -10,6 +12,7 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -17,11 +20,10 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_native"
 LIB = OUT_DIR / "libpcbz_b200.so"
-SOURCES = ["judge.cu", "aux_kernels.cu", "capi.cu"]
-HEADERS = ["judge.cuh", "common.cuh", "entropy.cuh", ROOT / "include" / "pcbz_b200.h"]
+MAX_FAST_PITCH = 16
 
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
     "-Xptxas", "-v",
@@ -35,6 +37,19 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found; the CUDA toolkit is required to build libpcbz_b200.so")
 
 
+def _units():
+    """(source, extra flags, object name) of every translation unit."""
+    units = [("judge.cu", [], "judge.o"), ("aux_kernels.cu", [], "aux_kernels.o"),
+             ("capi.cu", [], "capi.o")]
+    units += [("judge_px.cu", [f"-DPCBZ_PX={px}"], f"judge_px{px}.o")
+              for px in range(MAX_FAST_PITCH + 1)]
+    return units
+
+
+def _deps():
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "pcbz_b200.h"]
+
+
 def _stale(target: Path, deps) -> bool:
     if not target.exists():
         return True
@@ -42,32 +57,34 @@ def _stale(target: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
-def build_library(force: bool = False, verbose: bool = False) -> Path:
-    deps = [CSRC / s for s in SOURCES] + [CSRC / h if isinstance(h, str) else h for h in HEADERS]
-    if not force and not _stale(LIB, deps):
+def build_library(force: bool = False, verbose: bool = False, jobs: int | None = None) -> Path:
+    if not force and not _stale(LIB, _deps()):
         return LIB
     OUT_DIR.mkdir(exist_ok=True)
     nvcc = _nvcc()
-    objs = []
-    log = []
-    for src in SOURCES:
-        obj = OUT_DIR / (Path(src).stem + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o", str(obj)]
+
+    def compile_one(unit):
+        src, extra, obj = unit
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-c", str(CSRC / src),
+               "-o", str(OUT_DIR / obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
-        log.append(r.stdout + r.stderr)
         if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
-        objs.append(str(obj))
+            raise RuntimeError(f"nvcc failed for {src} {extra}:\n{r.stdout}\n{r.stderr}")
+        return f"== {src} {' '.join(extra)}\n{r.stdout}{r.stderr}"
+
+    units = _units()
+    with ThreadPoolExecutor(jobs or max(1, os.cpu_count() or 1)) as pool:
+        logs = list(pool.map(compile_one, units))
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp), *objs,
+    cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *[str(OUT_DIR / u[2]) for u in units],
            "-Xcompiler", "-fPIC"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
-    (OUT_DIR / "ptxas.log").write_text("\n".join(log))
+    (OUT_DIR / "ptxas.log").write_text("\n".join(logs))
     if verbose:
-        print("\n".join(log))
+        print("\n".join(logs))
     return LIB
 
 
@@ -83,5 +100,5 @@ def build_oracle() -> Path | None:
 
 
 if __name__ == "__main__":
-    print(build_library(force="--force" in sys.argv, verbose=True))
+    print(build_library(force="--force" in sys.argv, verbose="-v" in sys.argv))
     print(build_oracle())

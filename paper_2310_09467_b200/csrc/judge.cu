@@ -1,419 +1,8 @@
-// judge.cu -- sm_100a kernels of the entropy judge.
-//
-// Semantics follow the reference's fused kernel residual_bwt_pair_hist
-// (pkg/src/pcbz/_kernels.py:157-204) and criterion.select_predictor
-// (criterion.py:136-173); the parallel decomposition is new:
-//
-//   * the packed residual stream of one (frame, candidate) pair is cut into
-//     segments; one CTA owns a segment, each of its 192 threads owns a
-//     contiguous run of pixels and runs the reference's per-key chain
-//     automaton (_kernels.py:192-201) on it with a lane-private last-pred
-//     table in shared memory -- no cross-lane communication in the hot loop
-//     (warp-cooperative matching with __match_any_sync measured 12x slower
-//     than a shared atomic on B200, profiles/r01_microbench_atoms_match.log);
-//   * fast path (width % 8 == 0, pitch_x <= 16): each lane walks its run in
-//     8-pixel chunks with 128-bit read-only loads of the rows it needs and
-//     carries left-neighbour history in registers; the pitch is a template
-//     parameter, so lenslet-stride neighbours are static register picks;
-//   * pair increments go to a CTA-private 65,536-bin histogram of packed u16
-//     counters in shared memory (128 KiB); a counter reaching 0x8000 is
-//     spilled exactly once (atomicAnd claim) into a small list;
-//   * runs are stitched in stream order through their (first, last) pred per
-//     key, inside the CTA and then across segments;
-//   * the bucket seams of _stitch_buckets (_kernels.py:125-133) close the
-//     histogram; entropy.cuh reduces it exactly like the reference's numpy.
-#include <utility>
-
-#include "common.cuh"
-#include "entropy.cuh"
+// judge.cu -- cross-segment finalisation, argmin and the launch dispatch of
+// the entropy judge (the histogram kernel itself is in judge_kernel.cuh).
+#include "judge_kernel.cuh"
 
 namespace pcbz {
-
-// ---------------------------------------------------------------------------
-// pair -> (frame, candidate)
-// ---------------------------------------------------------------------------
-
-struct PairRef {
-  int64_t frame;
-  int spec;      // predictor byte
-  int64_t slot;  // frame * k + index in the full candidate list
-};
-
-__device__ __forceinline__ PairRef pair_ref(const JudgeParams &P, int64_t pair) {
-  PairRef r;
-  if (pair < P.cl.kA) {
-    r.frame = 0;
-    r.spec = P.cl.byteA[pair];
-    r.slot = P.cl.idxA[pair];
-  } else {
-    const int64_t q = pair - P.cl.kA;
-    r.frame = 1 + q / P.cl.kB;
-    const int j = (int)(q % P.cl.kB);
-    r.spec = P.cl.byteB[j];
-    r.slot = r.frame * P.cl.k + P.cl.idxB[j];
-  }
-  return r;
-}
-
-// ---------------------------------------------------------------------------
-// chain state of one lane
-// ---------------------------------------------------------------------------
-
-struct ChainState {
-  uint32_t *hist;   // shared, kHistWords packed u16 counters
-  uint32_t lbase;   // shared address of this lane's last-pred column
-  uint8_t *F;       // this lane's first-pred row (global scratch)
-  uint32_t *spill;  // shared spill list
-  int *nspill;
-  int *err;
-};
-
-// One stream byte as an event (key, pred) of the reference automaton
-// (_kernels.py:192-201): pair with the pred of the previous event of the same
-// key, or remember pred as the key's first.  The last-pred entry is a u16
-// (0x100 = unseen) read and overwritten with independent 16-bit accesses, so
-// consecutive events do not wait on each other's shared-memory latency.
-// Returns the incremented bin (or ~0u) and ORs the counter's toggled bits
-// into `flag`: bit 15 of a half toggles exactly when that counter crosses
-// 0x7FFF -> 0x8000.
-__device__ __forceinline__ uint32_t chain_event(const ChainState &cs, uint32_t key, uint32_t pred,
-                                                uint32_t &flag) {
-  const uint32_t a = cs.lbase + (key >> 1) * (4u * kJudgeThreads) + ((key & 1u) << 1);
-  uint32_t last;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(last) : "r"(a));
-  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(pred));
-  if (last == kUnseen) {
-    cs.F[key] = (uint8_t)pred;
-    return ~0u;
-  }
-  const uint32_t bin = (last << 8) | pred;
-  const uint32_t inc = 1u << ((pred & 1u) << 4);
-  const uint32_t old = atomicAdd(&cs.hist[bin >> 1], inc);
-  flag |= old ^ (old + inc);
-  return bin;
-}
-
-// Move 0x8000 out of `bin`'s counter if its bit 15 is set.  atomicAnd makes
-// exactly one claimant per crossing; counts are never lost or doubled.
-__device__ __forceinline__ void claim_spill(const ChainState &cs, uint32_t bin) {
-  if (bin == ~0u) return;
-  const uint32_t m = 0x8000u << ((bin & 1u) << 4);
-  const uint32_t old = atomicAnd(&cs.hist[bin >> 1], ~m);
-  if (old & m) {
-    const int i = atomicAdd(cs.nspill, 1);
-    if (i < kSpillCap) cs.spill[i] = bin;
-    else atomicExch(cs.err, 2);
-  }
-}
-
-// increment outside the hot loop (stitching): claim immediately
-__device__ __forceinline__ void hist_inc_now(const ChainState &cs, uint32_t bin) {
-  const uint32_t inc = 1u << ((bin & 1u) << 4);
-  const uint32_t old = atomicAdd(&cs.hist[bin >> 1], inc);
-  if ((old ^ (old + inc)) & 0x80008000u) claim_spill(cs, bin);
-}
-
-// ---------------------------------------------------------------------------
-// generic lane: any width / pitch, one pixel at a time
-// ---------------------------------------------------------------------------
-
-__device__ void lane_generic(const uint16_t *src, const uint16_t *prv, const PredCfg &cfg, int W,
-                             int64_t npix, int64_t a, int64_t b, const ChainState &cs) {
-  if (a >= b) return;
-  const int64_t q = a > 0 ? a - 1 : npix - 1;  // wrap predecessor (_kernels.py:172-190)
-  uint32_t prev_lo = residual_at(src, prv, W, (int)(q / W), (int)(q % W), cfg) & 0xFFu;
-  int y = (int)(a / W), x = (int)(a % W);
-  uint32_t flag = 0;
-  for (int64_t k = a; k < b; ++k) {
-    const uint32_t r = residual_at(src, prv, W, y, x, cfg);
-    const uint32_t hi = r >> 8, lo = r & 0xFFu;
-    const uint32_t b0 = chain_event(cs, hi, prev_lo, flag);
-    const uint32_t b1 = chain_event(cs, lo, hi, flag);
-    if (flag & 0x80008000u) {
-      claim_spill(cs, b0);
-      claim_spill(cs, b1);
-    }
-    flag = 0;
-    prev_lo = lo;
-    if (++x == W) { x = 0; ++y; }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// fast lane: 8-pixel chunks, 128-bit loads, register neighbour history
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ uint4 ld_chunk(const uint16_t *__restrict__ s,
-                                          const uint16_t *__restrict__ p, int64_t off) {
-  uint4 a = __ldg(reinterpret_cast<const uint4 *>(s + off));
-  if (p) {
-    const uint4 b = __ldg(reinterpret_cast<const uint4 *>(p + off));
-    a.x = sub16x2(a.x, b.x); a.y = sub16x2(a.y, b.y);
-    a.z = sub16x2(a.z, b.z); a.w = sub16x2(a.w, b.w);
-  }
-  return a;
-}
-
-__device__ __forceinline__ void unpack8(const uint4 &w, int (&v)[8]) {
-  v[0] = w.x & 0xFFFF; v[1] = w.x >> 16; v[2] = w.y & 0xFFFF; v[3] = w.y >> 16;
-  v[4] = w.z & 0xFFFF; v[5] = w.z >> 16; v[6] = w.w & 0xFFFF; v[7] = w.w >> 16;
-}
-
-// f1..f4 as base + ((u - v) >> k) with uniform selectors:
-// f1 (A,B,C,0)  f2 (A,B,C,1)  f3 (B,A,C,1)  f4 (A,B,A,1) -- f4 = A + floor((B-A)/2)
-struct FSel {
-  bool f3, f4;
-  int k;
-};
-
-__device__ __forceinline__ int pred_sel(int A, int B, int C, const FSel &fs) {
-  const int base = fs.f3 ? B : A;
-  const int u = fs.f3 ? A : B;
-  const int v = fs.f4 ? A : C;
-  return base + ((u - v) >> fs.k);
-}
-
-template <int PX, int GRP>
-__device__ void lane_fast(const uint16_t *__restrict__ src, const uint16_t *__restrict__ prv,
-                          const FSel fs, int W, int py, int64_t npix, int64_t a, int64_t nch,
-                          const PredCfg &cfg, const ChainState &cs) {
-  constexpr bool kT1 = GRP == 0 || GRP == 2;  // row y-1   (pixel-adjacent B, C)
-  constexpr bool kTS = GRP == 1 || GRP == 2;  // row y-py  (lenslet B, C)
-  constexpr bool kXH = GRP >= 0;              // left history of row y
-  constexpr bool kXH2 = (GRP == 1 || GRP == 2) && PX > 8;
-  if (nch <= 0) return;
-  const int64_t q = a > 0 ? a - 1 : npix - 1;  // wrap predecessor (_kernels.py:172-190)
-  uint32_t prev_lo = residual_at(src, prv, W, (int)(q / W), (int)(q % W), cfg) & 0xFFu;
-  int y = (int)(a / W), x0 = (int)(a % W);
-  const uint4 Z = make_uint4(0, 0, 0, 0);
-  auto row = [&](int yy) -> int64_t { return (int64_t)yy * W; };
-  uint4 Xh1 = Z, Xh2 = Z, T1h = Z, TSh1 = Z, TSh2 = Z;
-  if (x0 > 0) {  // history of a run that starts mid-row
-    if (kXH) Xh1 = ld_chunk(src, prv, row(y) + x0 - 8);
-    if (kXH2 && x0 >= 16) Xh2 = ld_chunk(src, prv, row(y) + x0 - 16);
-    if (kT1 && y >= 1) T1h = ld_chunk(src, prv, row(y - 1) + x0 - 8);
-    if (kTS && y >= py) {
-      TSh1 = ld_chunk(src, prv, row(y - py) + x0 - 8);
-      if (kXH2 && x0 >= 16) TSh2 = ld_chunk(src, prv, row(y - py) + x0 - 16);
-    }
-  }
-  uint4 cX = ld_chunk(src, prv, row(y) + x0);
-  uint4 cT1 = (kT1 && y >= 1) ? ld_chunk(src, prv, row(y - 1) + x0) : Z;
-  uint4 cTS = (kTS && y >= py) ? ld_chunk(src, prv, row(y - py) + x0) : Z;
-  uint32_t flag = 0;
-  for (int64_t c = 0; c < nch; ++c) {
-    int ny = y, nx = x0 + 8;
-    if (nx == W) { nx = 0; ++ny; }
-    uint4 nX = Z, nT1 = Z, nTS = Z;
-    if (c + 1 < nch) {  // prefetch the next chunk
-      nX = ld_chunk(src, prv, row(ny) + nx);
-      if (kT1 && ny >= 1) nT1 = ld_chunk(src, prv, row(ny - 1) + nx);
-      if (kTS && ny >= py) nTS = ld_chunk(src, prv, row(ny - py) + nx);
-    }
-    int X[8], T1[8], TS[8], H1[8], H2[8], S1[8], S2[8], t1h[8];
-    unpack8(cX, X);
-    if (kT1) { unpack8(cT1, T1); unpack8(T1h, t1h); }
-    if (kTS) { unpack8(cTS, TS); unpack8(TSh1, S1); }
-    if (kXH) unpack8(Xh1, H1);
-    if (kXH2) { unpack8(Xh2, H2); unpack8(TSh2, S2); }
-    uint32_t r[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if constexpr (GRP < 0) {
-        r[i] = (uint32_t)X[i];
-      } else {
-        int p = 0, p1 = 0;
-        if constexpr (kT1) {  // pixel-adjacent neighbours (1, 1)
-          const int A = i ? X[i - 1] : H1[7];
-          const int C = i ? T1[i - 1] : t1h[7];
-          p1 = pred_sel(A, T1[i], C, fs);
-        }
-        if constexpr (kTS) {  // lenslet-stride neighbours (PX, py)
-          const int qq = i - PX;
-          int A, C;
-          if (qq >= 0) { A = X[qq]; C = TS[qq]; }
-          else if (qq >= -8) { A = H1[qq + 8]; C = S1[qq + 8]; }
-          else { A = H2[qq + 16]; C = S2[qq + 16]; }
-          const int p2 = pred_sel(A, TS[i], C, fs);
-          p = GRP == 2 ? ((p1 + p2) >> 1) : p2;  // phase group averages (_kernels.py:63-64)
-        } else {
-          p = p1;
-        }
-        r[i] = (uint32_t)(X[i] - p) & 0xFFFFu;
-      }
-    }
-    uint32_t bins[16];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t hi = r[i] >> 8, lo = r[i] & 0xFFu;
-      bins[2 * i] = chain_event(cs, hi, prev_lo, flag);
-      bins[2 * i + 1] = chain_event(cs, lo, hi, flag);
-      prev_lo = lo;
-    }
-    if (flag & 0x80008000u) {
-#pragma unroll
-      for (int e = 0; e < 16; ++e) claim_spill(cs, bins[e]);
-    }
-    flag = 0;
-    if (nx == 0) {
-      Xh1 = Xh2 = T1h = TSh1 = TSh2 = Z;  // new row: left neighbours are 0
-    } else {
-      Xh2 = Xh1; Xh1 = cX; T1h = cT1; TSh2 = TSh1; TSh1 = cTS;
-    }
-    y = ny; x0 = nx;
-    cX = nX; cT1 = nT1; cTS = nTS;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// the judge kernel: persistent CTAs pull (pair, segment) items
-// ---------------------------------------------------------------------------
-//
-// dynamic shared memory:
-//   hist   kHistWords            packed u16 counters
-//   last   kLastWords * 192      last-pred tables, word (key>>1)*192 + lane
-//   spill  kSpillCap             spilled bins
-// after the hot loop the last-pred region is reused for the spilled-bin
-// bitmap (words [0, 2048)), first/last per key ([2048, 2560)) and the
-// entropy scratch ([2560, ...)).
-
-template <int PX>
-__global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const JudgeParams P) {
-  extern __shared__ uint4 smem_raw[];
-  uint32_t *hist_w = reinterpret_cast<uint32_t *>(smem_raw);
-  uint32_t *last_w = hist_w + kHistWords;
-  uint32_t *spill_w = last_w + kLastWords * kJudgeThreads;
-  __shared__ int s_item, s_nspill;
-  int *s_first = reinterpret_cast<int *>(last_w) + 2048;
-  int *s_last = s_first + 256;
-  NpScratch &scr = *reinterpret_cast<NpScratch *>(last_w + 2560);
-
-  const int tid = threadIdx.x;
-  const int64_t nitems = P.npairs * P.S;
-  ChainState cs;
-  cs.hist = hist_w;
-  cs.lbase = (uint32_t)__cvta_generic_to_shared(last_w + tid);
-  cs.F = P.fscratch + ((size_t)blockIdx.x * kJudgeThreads + tid) * 256;
-  cs.spill = spill_w;
-  cs.nspill = &s_nspill;
-  cs.err = P.err;
-  const uint8_t *Fcta = P.fscratch + (size_t)blockIdx.x * kJudgeThreads * 256;
-  uint32_t *Llane = last_w + tid;
-
-  for (;;) {
-    if (tid == 0) {
-      s_item = atomicAdd(P.counter, 1);
-      s_nspill = 0;
-    }
-    uint4 *h4 = reinterpret_cast<uint4 *>(hist_w);
-    for (int i = tid; i < kHistWords / 4; i += kJudgeThreads) h4[i] = make_uint4(0, 0, 0, 0);
-    for (int w = 0; w < kLastWords; ++w) Llane[w * kJudgeThreads] = kUnseen | (kUnseen << 16);
-    __syncthreads();
-    const int64_t item = s_item;
-    if (item >= nitems) break;
-
-    const int64_t pair = item / P.S;
-    const int seg = (int)(item % P.S);
-    const PairRef pr = pair_ref(P, pair);
-    const uint16_t *src = P.frames + pr.frame * P.npix;
-    const uint16_t *prv = (pr.spec & 0x80) ? prev_of(P.frames, P.halo, P.npix, pr.frame) : nullptr;
-    const PredCfg cfg = make_cfg(pr.spec & 0x7F, P.px, P.py);
-
-    if constexpr (PX > 0) {
-      // chunk-granular segments and runs
-      const int64_t nchunk = P.npix / 8;
-      const int64_t cb = nchunk * seg / P.S, ce = nchunk * (seg + 1) / P.S;
-      const int64_t ca = cb + (ce - cb) * tid / kJudgeThreads;
-      const int64_t cz = cb + (ce - cb) * (tid + 1) / kJudgeThreads;
-      const int fn = cfg.f;
-      const FSel fs{fn == 3, fn == 4, fn == 1 ? 0 : 1};
-      switch (cfg.grp) {
-        case -1: lane_fast<PX, -1>(src, prv, fs, P.W, P.py, P.npix, ca * 8, cz - ca, cfg, cs); break;
-        case 0: lane_fast<PX, 0>(src, prv, fs, P.W, P.py, P.npix, ca * 8, cz - ca, cfg, cs); break;
-        case 1: lane_fast<PX, 1>(src, prv, fs, P.W, P.py, P.npix, ca * 8, cz - ca, cfg, cs); break;
-        default: lane_fast<PX, 2>(src, prv, fs, P.W, P.py, P.npix, ca * 8, cz - ca, cfg, cs); break;
-      }
-    } else {
-      const int64_t sb = P.npix * seg / P.S, se = P.npix * (seg + 1) / P.S;
-      const int64_t len = se - sb;
-      lane_generic(src, prv, cfg, P.W, P.npix, sb + len * tid / kJudgeThreads,
-                   sb + len * (tid + 1) / kJudgeThreads, cs);
-    }
-    __syncthreads();
-
-    // ---- stitch the 192 runs in stream order (segment-summary combine) -----
-    int my_first0 = -1, my_last0 = -1, my_first1 = -1, my_last1 = -1;
-    for (int v = tid, i = 0; v < 256; v += kJudgeThreads, ++i) {
-      int carried = -1, first = -1;
-      const uint32_t *col = last_w + (v >> 1) * kJudgeThreads;
-      const uint32_t sh = (v & 1) << 4;
-      for (int j = 0; j < kJudgeThreads; ++j) {
-        const uint32_t e = (col[j] >> sh) & 0xFFFFu;
-        const uint32_t f = Fcta[(size_t)j * 256 + v];
-        if (e != kUnseen) {
-          if (carried >= 0) hist_inc_now(cs, ((uint32_t)carried << 8) | f);
-          else first = (int)f;
-          carried = (int)e;
-        }
-      }
-      if (i == 0) { my_first0 = first; my_last0 = carried; }
-      else { my_first1 = first; my_last1 = carried; }
-    }
-    __syncthreads();
-    s_first[tid] = my_first0;
-    s_last[tid] = my_last0;
-    if (tid + kJudgeThreads < 256) {
-      s_first[tid + kJudgeThreads] = my_first1;
-      s_last[tid + kJudgeThreads] = my_last1;
-    }
-    __syncthreads();
-
-    if (P.direct) {
-      // whole stream in this CTA: bucket seams (_kernels.py:125-133) ...
-      if (tid == 0) {
-        int carried = -1;
-        for (int v = 0; v < 256; ++v) {
-          if (s_first[v] < 0) continue;
-          if (carried >= 0) hist_inc_now(cs, ((uint32_t)carried << 8) | (uint32_t)s_first[v]);
-          carried = s_last[v];
-        }
-      }
-      __syncthreads();
-      // ... spilled bins marked in a bitmap, then the entropy
-      uint32_t *spilled = last_w;
-      for (int i = tid; i < 2048; i += kJudgeThreads) spilled[i] = 0;
-      __syncthreads();
-      const int ns = min(s_nspill, kSpillCap);
-      for (int i = tid; i < ns; i += kJudgeThreads)
-        atomicOr(&spilled[spill_w[i] >> 5], 1u << (spill_w[i] & 31));
-      __syncthreads();
-      auto get = [&](int bin) -> double {
-        uint32_t c = (hist_w[bin >> 1] >> ((bin & 1) << 4)) & 0xFFFFu;
-        if (spilled[bin >> 5] & (1u << (bin & 31)))
-          for (int i = 0; i < ns; ++i) c += spill_w[i] == (uint32_t)bin ? kSpill : 0u;
-        return (double)c;
-      };
-      const double e = block_entropy(get, (double)(2 * P.npix - 1), scr);
-      if (tid == 0) P.ent[pr.slot] = e;
-    } else {
-      // flush into the pair's global histogram and publish the summary
-      uint32_t *G = P.ghist + (size_t)pr.slot * 65536;
-      for (int w = tid; w < kHistWords; w += kJudgeThreads) {
-        const uint32_t v = hist_w[w];
-        if (v & 0xFFFFu) atomicAdd(&G[2 * w], v & 0xFFFFu);
-        if (v >> 16) atomicAdd(&G[2 * w + 1], v >> 16);
-      }
-      const int ns = min(s_nspill, kSpillCap);
-      for (int i = tid; i < ns; i += kJudgeThreads) atomicAdd(&G[spill_w[i]], kSpill);
-      int16_t *sum = P.segsum + ((size_t)pr.slot * P.S + seg) * 512;
-      for (int v = tid; v < 256; v += kJudgeThreads) {
-        sum[v] = (int16_t)s_first[v];
-        sum[256 + v] = (int16_t)s_last[v];
-      }
-    }
-    __syncthreads();
-  }
-}
 
 // ---------------------------------------------------------------------------
 // cross-segment stitch + bucket seams + entropy (one CTA per pair)
@@ -487,33 +76,36 @@ __global__ void judge_select_kernel(const JudgeParams P, uint8_t *sel) {
 // launchers
 // ---------------------------------------------------------------------------
 
-template <int... Ps>
-static cudaError_t configure_all(std::integer_sequence<int, Ps...>) {
-  cudaError_t errs[] = {cudaFuncSetAttribute(judge_hist_kernel<Ps>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)kJudgeSmemBytes)...};
-  for (cudaError_t e : errs)
-    if (e != cudaSuccess) return e;
-  return cudaSuccess;
-}
+#define PCBZ_PX_LIST(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) \
+  X(13) X(14) X(15) X(16)
+#define PCBZ_DECL(n)                             \
+  cudaError_t judge_configure_px##n();           \
+  void judge_launch_px##n(const JudgeParams &, int, cudaStream_t);
+PCBZ_PX_LIST(PCBZ_DECL)
+#undef PCBZ_DECL
+
+static_assert(kMaxFastPitch == 16, "PCBZ_PX_LIST must cover 0..kMaxFastPitch");
 
 cudaError_t judge_configure() {
-  cudaError_t e = configure_all(std::make_integer_sequence<int, kMaxFastPitch + 1>{});
-  if (e != cudaSuccess) return e;
+#define PCBZ_CONF(n)                              \
+  {                                               \
+    cudaError_t e = judge_configure_px##n();      \
+    if (e != cudaSuccess) return e;               \
+  }
+  PCBZ_PX_LIST(PCBZ_CONF)
+#undef PCBZ_CONF
   return cudaFuncSetAttribute(judge_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)kFinalizeSmemBytes);
 }
 
-template <int... Ps>
-static void launch_dispatch(int px, const JudgeParams &p, int grid, cudaStream_t st,
-                            std::integer_sequence<int, Ps...>) {
-  ((px == Ps ? (void)(judge_hist_kernel<Ps><<<grid, kJudgeThreads, kJudgeSmemBytes, st>>>(p))
-             : void()),
-   ...);
-}
-
 cudaError_t launch_judge(const JudgeParams &p, int grid, cudaStream_t st) {
-  launch_dispatch(p.fast_px, p, grid, st, std::make_integer_sequence<int, kMaxFastPitch + 1>{});
+  switch (p.fast_px) {
+#define PCBZ_CASE(n) \
+  case n: judge_launch_px##n(p, grid, st); break;
+    PCBZ_PX_LIST(PCBZ_CASE)
+#undef PCBZ_CASE
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
