@@ -9,6 +9,7 @@ namespace pcbz {
 // ---- tunables ------------------------------
 constexpr int kJudgeThreads = 192;             // lane-private chains per CTA (6 warps)
 constexpr int kHistWords = 32768;              // 65536 packed u16 bins
+constexpr int kDummyWords = 128;               // row 0x100xx: first occurrences land here
 constexpr int kLastWords = 128;                // 256 keys x u16 per lane, 2 per word
 constexpr uint32_t kUnseen = 0x100;            // per-lane "key not seen yet" marker
 constexpr uint32_t kSpill = 0x8000;            // u16 bin spill threshold
@@ -18,7 +19,7 @@ constexpr int kEntropyThreads = 192;           // all entropy reductions use thi
 constexpr int kMaxFastPitch = 16;              // fast path: pitch_x <= 16 (template parameter)
 
 constexpr size_t kJudgeSmemBytes =
-    (size_t)(kHistWords + kLastWords * kJudgeThreads + kSpillCap) * sizeof(uint32_t);
+    (size_t)(kHistWords + kDummyWords + kLastWords * kJudgeThreads + kSpillCap) * sizeof(uint32_t);
 
 // One predictor's neighbourhood configuration; reference _kernels.py:56-59,167-170.
 struct PredCfg {

@@ -63,6 +63,7 @@ __device__ __forceinline__ PairRef pair_ref(const JudgeParams &P, int64_t pair) 
 
 struct ChainState {
   uint32_t *hist;   // shared, kHistWords packed u16 counters
+  uint32_t hbase;   // shared-window address of hist
   uint32_t lbase;   // shared address of this lane's last-pred column
   uint8_t *F;       // this lane's first-pred row (global scratch)
   uint32_t *spill;  // shared spill list
@@ -180,14 +181,17 @@ __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v));
 }
 
-// predicated shared atomic add; returns the old word (0 when `on` is false)
-__device__ __forceinline__ uint32_t atoms_add_if(uint32_t on, uint32_t a, uint32_t inc) {
-  uint32_t old = 0;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p atom.shared.add.u32 %0, [%1], %3;\n\t}"
-      : "+r"(old)
-      : "r"(a), "r"(on), "r"(inc)
-      : "memory");
+// explicit shared-window atomics: the lane functions are not inlined into the
+// kernel, so generic pointers would compile to (slow) generic ATOM
+__device__ __forceinline__ uint32_t atoms_add(uint32_t a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v));
+  return old;
+}
+
+__device__ __forceinline__ uint32_t atoms_and(uint32_t a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.and.b32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v));
   return old;
 }
 
@@ -195,7 +199,7 @@ __device__ __forceinline__ uint32_t atoms_add_if(uint32_t on, uint32_t a, uint32
 // set.  Any claimant may clear any set bit: atomicAnd makes every clear
 // unique, so counts are transferred exactly once.
 __device__ __forceinline__ void claim_word(const ChainState &cs, uint32_t word) {
-  const uint32_t old = atomicAnd(&cs.hist[word], ~0x80008000u);
+  const uint32_t old = atoms_and(cs.hbase + 4u * word, ~0x80008000u);
   if (old & 0x80008000u) {
     const int n = (old & 0x8000u ? 1 : 0) + (old & 0x80000000u ? 1 : 0);
     const int i = atomicAdd(cs.nspill, n);
@@ -251,7 +255,6 @@ __device__ __noinline__ void lane_fast(const uint16_t *__restrict__ src,
   uint4 cX = ld_chunk(src, prv, row(y) + x0);
   uint4 cT1 = (kT1 && y >= 1) ? ld_chunk(src, prv, row(y - 1) + x0) : Z;
   uint4 cTS = (kTS && y >= py) ? ld_chunk(src, prv, row(y - py) + x0) : Z;
-  const uint32_t hbase = (uint32_t)__cvta_generic_to_shared(cs.hist);
   for (int64_t c = 0; c < nch; ++c) {
     int ny = y, nx = x0 + 8;
     if (nx == W) { nx = 0; ++ny; }
@@ -311,23 +314,25 @@ __device__ __noinline__ void lane_fast(const uint16_t *__restrict__ src,
       last[e] = lds_u16(la);
       sts_u16(la, prd[e]);
     }
+    // phase B: one unconditional atomic per event.  A first occurrence has
+    // last == 0x100, i.e. bin 0x100xx: it lands in the dummy row past the
+    // histogram and is excluded from every count.
     uint32_t flag = 0, fresh = 0, word[16];
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {  // phase B: pair increments
-      const uint32_t seen = last[e] != kUnseen;
-      fresh |= seen ^ 1u;
-      word[e] = last[e] * 128u + (prd[e] >> 1);  // bin = last * 256 + pred
-      flag |= atoms_add_if(seen, hbase + word[e] * 4u, 1u + (prd[e] & 1u) * 0xFFFFu);
+    for (int e = 0; e < 16; ++e) {
+      fresh |= last[e];
+      word[e] = last[e] * 128u + (prd[e] >> 1);  // bin = last * 256 + pred, 2 bins/word
+      flag |= atoms_add(cs.hbase + 4u * word[e], 1u + (prd[e] & 1u) * 0xFFFFu);
     }
-    if (fresh) {  // first occurrence of a key in this run
+    if (fresh & kUnseen) {  // first occurrence of a key in this run
 #pragma unroll
       for (int e = 0; e < 16; ++e)
         if (last[e] == kUnseen) cs.F[key[e]] = (uint8_t)prd[e];
     }
-    if (flag & 0x80008000u) {
+    if (flag & 0x80008000u) {  // some counter has crossed 0x8000: claim
 #pragma unroll
       for (int e = 0; e < 16; ++e)
-        if (last[e] != kUnseen) claim_word(cs, word[e]);
+        if (word[e] < (uint32_t)kHistWords) claim_word(cs, word[e]);
     }
     if (nx == 0) {
       Xh1 = Xh2 = T1h = TSh1 = TSh2 = Z;  // new row: left neighbours are 0
@@ -364,7 +369,7 @@ template <int PX>
 __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const JudgeParams P) {
   extern __shared__ uint4 smem_raw[];
   uint32_t *hist_w = reinterpret_cast<uint32_t *>(smem_raw);
-  uint32_t *last_w = hist_w + kHistWords;
+  uint32_t *last_w = hist_w + kHistWords + kDummyWords;
   uint32_t *spill_w = last_w + kLastWords * kJudgeThreads;
   __shared__ int s_item, s_nspill;
   int *s_first = reinterpret_cast<int *>(last_w) + 2048;
@@ -375,6 +380,7 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
   const int64_t nitems = P.npairs * P.S;
   ChainState cs;
   cs.hist = hist_w;
+  cs.hbase = (uint32_t)__cvta_generic_to_shared(hist_w);
   cs.lbase = (uint32_t)__cvta_generic_to_shared(last_w + tid);
   cs.F = P.fscratch + ((size_t)blockIdx.x * kJudgeThreads + tid) * 256;
   cs.spill = spill_w;
@@ -389,7 +395,7 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
       s_nspill = 0;
     }
     uint4 *h4 = reinterpret_cast<uint4 *>(hist_w);
-    for (int i = tid; i < kHistWords / 4; i += kJudgeThreads) h4[i] = make_uint4(0, 0, 0, 0);
+    for (int i = tid; i < (kHistWords + kDummyWords) / 4; i += kJudgeThreads) h4[i] = make_uint4(0, 0, 0, 0);
     for (int w = 0; w < kLastWords; ++w) Llane[w * kJudgeThreads] = kUnseen | (kUnseen << 16);
     __syncthreads();
     const int64_t item = s_item;
