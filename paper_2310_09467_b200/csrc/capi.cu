@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <algorithm>
 #include <string>
@@ -153,6 +154,17 @@ int build_lists(const uint8_t *specs, int k, bool halo, int temporal, CandLists 
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// Run-length weight (in 1/16) of the two warps that own a scheduler alone
+// (judge_kernel.cuh); tunable through PCBZ_LONE_WEIGHT for measurements.
+int lone_weight() {
+  static int w = [] {
+    const char *e = getenv("PCBZ_LONE_WEIGHT");
+    const int v = e ? atoi(e) : 20;
+    return v < 8 ? 8 : (v > 64 ? 64 : v);
+  }();
+  return w;
+}
+
 int make_plan(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *specs,
               int k, bool halo, int temporal, bool want_hist, Plan &pl) {
   int rc = validate_geometry(h, w, px, py);
@@ -176,6 +188,7 @@ int make_plan(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py, con
   // 8-pixel chunk path: rows of whole chunks and a pitch the fast kernel is
   // instantiated for (pointer alignment is re-checked in run_plan)
   jp.fast_px = (w % 8 == 0 && px <= kMaxFastPitch && g_fast_enabled) ? (int)px : 0;
+  jp.lone_weight = lone_weight();
   const int64_t items = jp.npairs * jp.S;
   pl.grid = (int)std::min<int64_t>(items, num_sms_cached());
   size_t off = 0;
@@ -225,7 +238,7 @@ int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double 
   ++launches;
   if (d_stream) {
     EmitParams ep{d_frames, d_halo, jp.nframes, jp.npix, jp.H, jp.W, jp.px, jp.py, d_sel, d_stream};
-    CUDA_TRY(launch_emit(ep, st));
+    CUDA_TRY(launch_emit_any(ep, st));
     ++launches;
   }
   g_launches = launches;
@@ -536,7 +549,7 @@ int pcbz_emit_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t nf
   CUDA_TRY(cudaMemcpyAsync(c.sel.p, sel, (size_t)nframes, cudaMemcpyHostToDevice, st));
   EmitParams ep{c.frames.as<uint16_t>(), halo_prev ? c.prev.as<uint16_t>() : nullptr, nframes,
                 h * w, (int)h, (int)w, (int)px, (int)py, c.sel.as<uint8_t>(), c.stream_out.as<uint8_t>()};
-  CUDA_TRY(launch_emit(ep, st));
+  CUDA_TRY(launch_emit_any(ep, st));
   CUDA_TRY(cudaMemcpyAsync(stream_out, c.stream_out.p, fb, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   return PCBZ_OK;

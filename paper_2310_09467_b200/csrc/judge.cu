@@ -78,9 +78,10 @@ __global__ void judge_select_kernel(const JudgeParams P, uint8_t *sel) {
 
 #define PCBZ_PX_LIST(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) \
   X(13) X(14) X(15) X(16)
-#define PCBZ_DECL(n)                             \
-  cudaError_t judge_configure_px##n();           \
-  void judge_launch_px##n(const JudgeParams &, int, cudaStream_t);
+#define PCBZ_DECL(n)                                               \
+  cudaError_t judge_configure_px##n();                             \
+  void judge_launch_px##n(const JudgeParams &, int, cudaStream_t); \
+  void emit_launch_px##n(const EmitParams &, int, cudaStream_t);
 PCBZ_PX_LIST(PCBZ_DECL)
 #undef PCBZ_DECL
 
@@ -105,6 +106,24 @@ cudaError_t launch_judge(const JudgeParams &p, int grid, cudaStream_t st) {
     PCBZ_PX_LIST(PCBZ_CASE)
 #undef PCBZ_CASE
     default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// Emission: 8-pixel chunk kernel when rows are whole chunks, the pitch has an
+// instantiation and the buffers are 16-byte aligned; per-pixel otherwise.
+cudaError_t launch_emit_any(const EmitParams &p, cudaStream_t st) {
+  const bool aligned = ((reinterpret_cast<uintptr_t>(p.frames) | reinterpret_cast<uintptr_t>(p.halo) |
+                         reinterpret_cast<uintptr_t>(p.stream)) & 15) == 0;
+  if (p.W % 8 != 0 || p.px < 1 || p.px > kMaxFastPitch || !aligned) return launch_emit(p, st);
+  const int64_t chunks = p.nframes * (p.npix / 8);
+  const int grid = (int)std::min<int64_t>((chunks + 255) / 256, 148 * 16);
+  switch (p.px) {
+#define PCBZ_CASE(n) \
+  case n: emit_launch_px##n(p, grid, st); break;
+    PCBZ_PX_LIST(PCBZ_CASE)
+#undef PCBZ_CASE
+    default: return launch_emit(p, st);
   }
   return cudaGetLastError();
 }

@@ -58,6 +58,7 @@ struct JudgeParams {
   int S;                    // segments per pair
   int direct;               // 1: S == 1 and no histogram output -> entropy in-CTA
   int fast_px;              // >0: 8-pixel chunk path instantiated for pitch_x; 0: generic
+  int lone_weight;          // run-length weight (x16) of warps alone on a scheduler
   double *ent;              // [nframes][k] (NaN = not scored)
   uint32_t *ghist;          // [nframes*k][65536] when !direct
   int16_t *segsum;          // [nframes*k][S][2][256] when !direct
@@ -78,7 +79,8 @@ struct EmitParams {
 cudaError_t launch_judge(const JudgeParams &p, int grid, cudaStream_t st);
 cudaError_t launch_finalize(const JudgeParams &p, cudaStream_t st);
 cudaError_t launch_select(const JudgeParams &p, uint8_t *sel, cudaStream_t st);
-cudaError_t launch_emit(const EmitParams &p, cudaStream_t st);
+cudaError_t launch_emit(const EmitParams &p, cudaStream_t st);       // per pixel, any shape
+cudaError_t launch_emit_any(const EmitParams &p, cudaStream_t st);   // chunked when possible
 cudaError_t launch_residual_image(const uint16_t *img, const uint16_t *prev, int64_t h, int64_t w,
                                   int spec, int px, int py, uint16_t *out, int big_endian,
                                   cudaStream_t st);

@@ -86,7 +86,7 @@ __device__ __forceinline__ uint32_t chain_event(const ChainState &cs, uint32_t k
   asm volatile("ld.shared.u16 %0, [%1];" : "=r"(last) : "r"(a));
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(pred));
   if (last == kUnseen) {
-    cs.F[key] = (uint8_t)pred;
+    cs.F[key * kJudgeThreads] = (uint8_t)pred;
     return ~0u;
   }
   const uint32_t bin = (last << 8) | pred;
@@ -213,144 +213,95 @@ __device__ __forceinline__ void claim_word(const ChainState &cs, uint32_t word) 
   }
 }
 
-// One lane's run of `nch` 8-pixel chunks starting at pixel a (a % 8 == 0),
-// for intra predictor ID and lenslet pitch PX (both compile-time).
-//
-// Per chunk the 16 stream bytes become 16 events (key, pred):
-//   e = 2i: (hi_i, lo_{i-1})     e = 2i + 1: (lo_i, hi_i)      (_kernels.py:187-202)
-// Phase A performs the 16 last-pred lookups/updates in stream order (each an
-// independent 16-bit load + store, no read-modify-write); phase B issues
-// the 16 histogram atomics.  A counter whose bit 15 is found set in an
-// atomic's returned word is claimed at the end of the chunk; the kernel
-// sweeps the histogram once more after the loop for any crossing nobody
-// observed.  First occurrences (pred -> first-pred row) are rare after a
-// run's warm-up and handled off the common path.
+#include "lane_fast.cuh"
+
+
+// ---------------------------------------------------------------------------
+// emission: selected residuals -> big-endian stream (core.py:228-237)
+// ---------------------------------------------------------------------------
+
+// Eight residuals of predictor ID at (y, x0..x0+7): the neighbour chunks are
+// loaded directly (adjacent threads load overlapping chunks, so these hit in
+// L1), lenslet-stride picks are static for the compile-time pitch PX.
 template <int PX, int ID>
-__device__ __noinline__ void lane_fast(const uint16_t *__restrict__ src,
-                                       const uint16_t *__restrict__ prv, int W, int py,
-                                       int64_t npix, int64_t a, int64_t nch, const PredCfg cfg,
-                                       const ChainState cs) {
+__device__ __forceinline__ void chunk_residuals(const uint16_t *__restrict__ src,
+                                                const uint16_t *__restrict__ prv, int W, int py,
+                                                int y, int x0, uint32_t (&r)[8]) {
   constexpr int GRP = ID == 0 ? -1 : (ID - 1) / 4;
   constexpr int F = ID == 0 ? 0 : (ID - 1) % 4 + 1;
-  constexpr bool kT1 = GRP == 0 || GRP == 2;  // row y-1   (pixel-adjacent B, C)
-  constexpr bool kTS = GRP == 1 || GRP == 2;  // row y-py  (lenslet B, C)
-  constexpr bool kXH = GRP >= 0;              // left history of row y
-  constexpr bool kXH2 = kTS && PX > 8;        // second chunk of history
-  if (nch <= 0) return;
-  const int64_t q = a > 0 ? a - 1 : npix - 1;  // wrap predecessor (_kernels.py:172-190)
-  uint32_t prev_lo = residual_at(src, prv, W, (int)(q / W), (int)(q % W), cfg) & 0xFFu;
-  int y = (int)(a / W), x0 = (int)(a % W);
+  constexpr bool kT1 = GRP == 0 || GRP == 2;
+  constexpr bool kTS = GRP == 1 || GRP == 2;
+  constexpr bool kXH2 = kTS && PX > 8;
   const uint4 Z = make_uint4(0, 0, 0, 0);
-  auto row = [&](int yy) -> int64_t { return (int64_t)yy * W; };
-  uint4 Xh1 = Z, Xh2 = Z, T1h = Z, TSh1 = Z, TSh2 = Z;
-  if (x0 > 0) {  // history of a run that starts mid-row
-    if (kXH) Xh1 = ld_chunk(src, prv, row(y) + x0 - 8);
-    if (kXH2 && x0 >= 16) Xh2 = ld_chunk(src, prv, row(y) + x0 - 16);
-    if (kT1 && y >= 1) T1h = ld_chunk(src, prv, row(y - 1) + x0 - 8);
-    if (kTS && y >= py) {
-      TSh1 = ld_chunk(src, prv, row(y - py) + x0 - 8);
-      if (kXH2 && x0 >= 16) TSh2 = ld_chunk(src, prv, row(y - py) + x0 - 16);
-    }
+  const int64_t row = (int64_t)y * W;
+  int X[8], T1[8], TS[8], H1[8], H2[8], S1[8], S2[8], t1h[8];
+  unpack8(ld_chunk(src, prv, row + x0), X);
+  if constexpr (GRP >= 0) unpack8(x0 >= 8 ? ld_chunk(src, prv, row + x0 - 8) : Z, H1);
+  if constexpr (kXH2) unpack8(x0 >= 16 ? ld_chunk(src, prv, row + x0 - 16) : Z, H2);
+  if constexpr (kT1) {
+    unpack8(y >= 1 ? ld_chunk(src, prv, row - W + x0) : Z, T1);
+    unpack8(y >= 1 && x0 >= 8 ? ld_chunk(src, prv, row - W + x0 - 8) : Z, t1h);
   }
-  uint4 cX = ld_chunk(src, prv, row(y) + x0);
-  uint4 cT1 = (kT1 && y >= 1) ? ld_chunk(src, prv, row(y - 1) + x0) : Z;
-  uint4 cTS = (kTS && y >= py) ? ld_chunk(src, prv, row(y - py) + x0) : Z;
-  for (int64_t c = 0; c < nch; ++c) {
-    int ny = y, nx = x0 + 8;
-    if (nx == W) { nx = 0; ++ny; }
-    uint4 nX = Z, nT1 = Z, nTS = Z;
-    if (c + 1 < nch) {  // prefetch the next chunk
-      nX = ld_chunk(src, prv, row(ny) + nx);
-      if (kT1 && ny >= 1) nT1 = ld_chunk(src, prv, row(ny - 1) + nx);
-      if (kTS && ny >= py) nTS = ld_chunk(src, prv, row(ny - py) + nx);
-    }
-    // ---- residuals of the 8 pixels (_kernels.py:179-186) --------------------
-    uint32_t r[8];
-    {
-      int X[8], T1[8], TS[8], H1[8], H2[8], S1[8], S2[8], t1h[8];
-      unpack8(cX, X);
-      if (kT1) { unpack8(cT1, T1); unpack8(T1h, t1h); }
-      if (kTS) { unpack8(cTS, TS); unpack8(TSh1, S1); }
-      if (kXH) unpack8(Xh1, H1);
-      if (kXH2) { unpack8(Xh2, H2); unpack8(TSh2, S2); }
+  if constexpr (kTS) {
+    const int64_t rs = row - (int64_t)py * W;
+    unpack8(y >= py ? ld_chunk(src, prv, rs + x0) : Z, TS);
+    unpack8(y >= py && x0 >= 8 ? ld_chunk(src, prv, rs + x0 - 8) : Z, S1);
+    if constexpr (kXH2) unpack8(y >= py && x0 >= 16 ? ld_chunk(src, prv, rs + x0 - 16) : Z, S2);
+  }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        if constexpr (GRP < 0) {
-          r[i] = (uint32_t)X[i];
-        } else {
-          int p = 0, p1 = 0;
-          if constexpr (kT1) {  // pixel-adjacent neighbours (1, 1)
-            p1 = pred_f<F>(i ? X[i - 1] : H1[7], T1[i], i ? T1[i - 1] : t1h[7]);
-          }
-          if constexpr (kTS) {  // lenslet-stride neighbours (PX, py)
-            const int qq = i - PX;
-            int A, C;
-            if (qq >= 0) { A = X[qq]; C = TS[qq]; }
-            else if (qq >= -8) { A = H1[qq + 8]; C = S1[qq + 8]; }
-            else { A = H2[qq + 16]; C = S2[qq + 16]; }
-            const int p2 = pred_f<F>(A, TS[i], C);
-            p = GRP == 2 ? ((p1 + p2) >> 1) : p2;  // phase group (_kernels.py:63-64)
-          } else {
-            p = p1;
-          }
-          r[i] = (uint32_t)(X[i] - p) & 0xFFFFu;
-        }
-      }
-    }
-    // ---- events ---------------------------------------------------------------
-    uint32_t key[16], prd[16];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      key[2 * i] = r[i] >> 8;
-      prd[2 * i] = i ? (r[i - 1] & 0xFFu) : prev_lo;
-      key[2 * i + 1] = r[i] & 0xFFu;
-      prd[2 * i + 1] = r[i] >> 8;
-    }
-    prev_lo = r[7] & 0xFFu;
-    uint32_t last[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {  // phase A: in stream order
-      const uint32_t la = cs.lbase + key[e] * 2u + (key[e] >> 1) * (4u * kJudgeThreads - 4u);
-      last[e] = lds_u16(la);
-      sts_u16(la, prd[e]);
-    }
-    // phase B: one unconditional atomic per event.  A first occurrence has
-    // last == 0x100, i.e. bin 0x100xx: it lands in the dummy row past the
-    // histogram and is excluded from every count.
-    uint32_t flag = 0, fresh = 0, word[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      fresh |= last[e];
-      word[e] = last[e] * 128u + (prd[e] >> 1);  // bin = last * 256 + pred, 2 bins/word
-      flag |= atoms_add(cs.hbase + 4u * word[e], 1u + (prd[e] & 1u) * 0xFFFFu);
-    }
-    if (fresh & kUnseen) {  // first occurrence of a key in this run
-#pragma unroll
-      for (int e = 0; e < 16; ++e)
-        if (last[e] == kUnseen) cs.F[key[e]] = (uint8_t)prd[e];
-    }
-    if (flag & 0x80008000u) {  // some counter has crossed 0x8000: claim
-#pragma unroll
-      for (int e = 0; e < 16; ++e)
-        if (word[e] < (uint32_t)kHistWords) claim_word(cs, word[e]);
-    }
-    if (nx == 0) {
-      Xh1 = Xh2 = T1h = TSh1 = TSh2 = Z;  // new row: left neighbours are 0
+  for (int i = 0; i < 8; ++i) {
+    if constexpr (GRP < 0) {
+      r[i] = (uint32_t)X[i];
     } else {
-      Xh2 = Xh1; Xh1 = cX; T1h = cT1; TSh2 = TSh1; TSh1 = cTS;
+      int p = 0, p1 = 0;
+      if constexpr (kT1) p1 = pred_f<F>(i ? X[i - 1] : H1[7], T1[i], i ? T1[i - 1] : t1h[7]);
+      if constexpr (kTS) {
+        const int qq = i - PX;
+        int A, C;
+        if (qq >= 0) { A = X[qq]; C = TS[qq]; }
+        else if (qq >= -8) { A = H1[qq + 8]; C = S1[qq + 8]; }
+        else { A = H2[qq + 16]; C = S2[qq + 16]; }
+        const int p2 = pred_f<F>(A, TS[i], C);
+        p = GRP == 2 ? ((p1 + p2) >> 1) : p2;
+      } else {
+        p = p1;
+      }
+      r[i] = (uint32_t)(X[i] - p) & 0xFFFFu;
     }
-    y = ny; x0 = nx;
-    cX = nX; cT1 = nT1; cTS = nTS;
   }
 }
 
 template <int PX, int... IDs>
-__device__ __forceinline__ void lane_fast_dispatch(int id, const uint16_t *src,
-                                                   const uint16_t *prv, int W, int py,
-                                                   int64_t npix, int64_t a, int64_t nch,
-                                                   const PredCfg &cfg, const ChainState &cs,
-                                                   std::integer_sequence<int, IDs...>) {
-  ((id == IDs ? lane_fast<PX, IDs>(src, prv, W, py, npix, a, nch, cfg, cs) : void()), ...);
+__device__ __forceinline__ void chunk_residuals_dispatch(int id, const uint16_t *src,
+                                                         const uint16_t *prv, int W, int py, int y,
+                                                         int x0, uint32_t (&r)[8],
+                                                         std::integer_sequence<int, IDs...>) {
+  ((id == IDs ? chunk_residuals<PX, IDs>(src, prv, W, py, y, x0, r) : void()), ...);
+}
+
+// one thread per 8-pixel chunk of every frame (W % 8 == 0, PX <= 16)
+template <int PX>
+__global__ void __launch_bounds__(256) emit_chunks_kernel(const EmitParams P) {
+  const int64_t cpf = P.npix / 8;  // chunks per frame
+  const int cpr = P.W / 8;         // chunks per row
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < P.nframes * cpf;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = c / cpf;
+    const int64_t k = c - f * cpf;
+    const int y = (int)(k / cpr), x0 = (int)(k - (int64_t)y * cpr) * 8;
+    const int spec = P.sel[f];
+    const uint16_t *src = P.frames + f * P.npix;
+    const uint16_t *prv = (spec & 0x80) ? prev_of(P.frames, P.halo, P.npix, f) : nullptr;
+    uint32_t r[8];
+    chunk_residuals_dispatch<PX>(spec & 0x7F, src, prv, P.W, P.py, y, x0, r,
+                                 std::make_integer_sequence<int, 13>{});
+    uint4 o;  // big-endian halves: swap the two bytes of every residual
+    o.x = __byte_perm(r[0] | (r[1] << 16), 0, 0x2301);
+    o.y = __byte_perm(r[2] | (r[3] << 16), 0, 0x2301);
+    o.z = __byte_perm(r[4] | (r[5] << 16), 0, 0x2301);
+    o.w = __byte_perm(r[6] | (r[7] << 16), 0, 0x2301);
+    *reinterpret_cast<uint4 *>(P.stream + 2 * (f * P.npix + k * 8)) = o;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -382,11 +333,21 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
   cs.hist = hist_w;
   cs.hbase = (uint32_t)__cvta_generic_to_shared(hist_w);
   cs.lbase = (uint32_t)__cvta_generic_to_shared(last_w + tid);
-  cs.F = P.fscratch + ((size_t)blockIdx.x * kJudgeThreads + tid) * 256;
+  // first-pred scratch of this CTA, key-major: F[key][lane]
+  const uint8_t *Fcta = P.fscratch + (size_t)blockIdx.x * kJudgeThreads * 256;
+  cs.F = P.fscratch + (size_t)blockIdx.x * kJudgeThreads * 256 + tid;
   cs.spill = spill_w;
   cs.nspill = &s_nspill;
   cs.err = P.err;
-  const uint8_t *Fcta = P.fscratch + (size_t)blockIdx.x * kJudgeThreads * 256;
+  // Run lengths per lane: 6 warps share 4 schedulers as [2, 2, 1, 1] (warp w
+  // on SMSP w % 4), so warps 2 and 3 progress faster; they get longer runs
+  // (weight P.lone_weight / 16 relative to the others) to finish together.
+  auto cum_weight = [&](int t) -> int64_t {
+    const int a = min(t, 64), b = max(0, min(t, 128) - 64), c = max(0, t - 128);
+    return 16 * (int64_t)(a + c) + (int64_t)P.lone_weight * b;
+  };
+  const int64_t w_total = cum_weight(kJudgeThreads);
+  const int64_t w_lo = cum_weight(tid), w_hi = cum_weight(tid + 1);
   uint32_t *Llane = last_w + tid;
 
   for (;;) {
@@ -412,10 +373,14 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
       // chunk-granular segments and runs
       const int64_t nchunk = P.npix / 8;
       const int64_t cb = nchunk * seg / P.S, ce = nchunk * (seg + 1) / P.S;
-      const int64_t ca = cb + (ce - cb) * tid / kJudgeThreads;
-      const int64_t cz = cb + (ce - cb) * (tid + 1) / kJudgeThreads;
-      lane_fast_dispatch<PX>(pr.spec & 0x7F, src, prv, P.W, P.py, P.npix, ca * 8, cz - ca, cfg, cs,
-                             std::make_integer_sequence<int, 13>{});
+      const int64_t ca = cb + (ce - cb) * w_lo / w_total;
+      const int64_t cz = cb + (ce - cb) * w_hi / w_total;
+      if (pr.spec & 0x80)
+        lane_fast_dispatch<PX, true>(pr.spec & 0x7F, src, prv, P.W, P.py, P.npix, ca * 8, cz - ca,
+                                     cfg, cs, std::make_integer_sequence<int, 13>{});
+      else
+        lane_fast_dispatch<PX, false>(pr.spec & 0x7F, src, prv, P.W, P.py, P.npix, ca * 8,
+                                      cz - ca, cfg, cs, std::make_integer_sequence<int, 13>{});
     } else {
       const int64_t sb = P.npix * seg / P.S, se = P.npix * (seg + 1) / P.S;
       const int64_t len = se - sb;
@@ -428,29 +393,39 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
     __syncthreads();
 
     // ---- stitch the 192 runs in stream order (segment-summary combine) -----
-    int my_first0 = -1, my_last0 = -1, my_first1 = -1, my_last1 = -1;
-    for (int v = tid, i = 0; v < 256; v += kJudgeThreads, ++i) {
-      int carried = -1, first = -1;
-      const uint32_t *col = last_w + (v >> 1) * kJudgeThreads;
-      const uint32_t sh = (v & 1) << 4;
-      for (int j = 0; j < kJudgeThreads; ++j) {
-        const uint32_t e = (col[j] >> sh) & 0xFFFFu;
-        const uint32_t f = Fcta[(size_t)j * 256 + v];
-        if (e != kUnseen) {
-          if (carried >= 0) hist_inc_now(cs, ((uint32_t)carried << 8) | f);
-          else first = (int)f;
-          carried = (int)e;
+    // One warp per key, 32 runs per step: the runs holding key v are found
+    // with a ballot; each pairs its first pred with the last pred of the
+    // previous run holding v (a shuffle within the step, a carry across).
+    {
+      const int warp = tid >> 5, lane = tid & 31;
+      int kf0 = -1, kl0 = -1, kf1 = -1, kl1 = -1;  // keys k = lane and k = 32 + lane
+      for (int v = warp, k = 0; v < 256; v += kJudgeThreads / 32, ++k) {
+        const uint32_t *col = last_w + (v >> 1) * kJudgeThreads;
+        const uint32_t sh = (v & 1) << 4;
+        int carry = -1, first = -1;
+        for (int b = 0; b < kJudgeThreads; b += 32) {
+          const int j = b + lane;
+          const int e = (int)((col[j] >> sh) & 0xFFFFu);
+          const int f = Fcta[(size_t)v * kJudgeThreads + j];
+          const uint32_t m = __ballot_sync(0xffffffffu, e != (int)kUnseen);
+          const uint32_t lower = m & ((1u << lane) - 1u);
+          const int from = __shfl_sync(0xffffffffu, e, lower ? 31 - __clz(lower) : 0);
+          const int before = lower ? from : carry;
+          if (e != (int)kUnseen && before >= 0) hist_inc_now(cs, ((uint32_t)before << 8) | (uint32_t)f);
+          if (m) {
+            if (first < 0) first = __shfl_sync(0xffffffffu, f, __ffs(m) - 1);
+            carry = __shfl_sync(0xffffffffu, e, 31 - __clz(m));
+          }
+        }
+        if (lane == (k & 31)) {
+          if (k < 32) { kf0 = first; kl0 = carry; }
+          else { kf1 = first; kl1 = carry; }
         }
       }
-      if (i == 0) { my_first0 = first; my_last0 = carried; }
-      else { my_first1 = first; my_last1 = carried; }
-    }
-    __syncthreads();
-    s_first[tid] = my_first0;
-    s_last[tid] = my_last0;
-    if (tid + kJudgeThreads < 256) {
-      s_first[tid + kJudgeThreads] = my_first1;
-      s_last[tid + kJudgeThreads] = my_last1;
+      __syncthreads();  // the last-pred tables are dead from here on
+      const int v0 = warp + lane * (kJudgeThreads / 32), v1 = v0 + 32 * (kJudgeThreads / 32);
+      if (v0 < 256) { s_first[v0] = kf0; s_last[v0] = kl0; }
+      if (v1 < 256) { s_first[v1] = kf1; s_last[v1] = kl1; }
     }
     __syncthreads();
 

@@ -22,3 +22,11 @@ void PCBZ_CAT(judge_launch_px, PCBZ_PX)(const JudgeParams &p, int grid, cudaStre
 }
 
 }  // namespace pcbz
+
+namespace pcbz {
+
+void PCBZ_CAT(emit_launch_px, PCBZ_PX)(const EmitParams &p, int grid, cudaStream_t st) {
+  if constexpr (PCBZ_PX > 0) emit_chunks_kernel<PCBZ_PX><<<grid, 256, 0, st>>>(p);
+}
+
+}  // namespace pcbz
