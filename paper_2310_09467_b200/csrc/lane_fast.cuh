@@ -1,39 +1,66 @@
 // lane_fast.cuh -- the hot loop of the judge: one lane's run of 8-pixel
-// chunks (included by judge_kernel.cuh; needs ChainState, claim_word,
-// ld/st/atom helpers from there; included inside namespace pcbz).
+// chunks (included by judge_kernel.cuh inside namespace pcbz; uses
+// ChainState, claim_word and the ld/st/atom helpers defined there).
 #pragma once
 
+// 16 zero bytes: rows above the frame are loaded from here (the reference's
+// out-of-bounds neighbours read 0, _kernels.py:33-35), so no select ever
+// waits on a load result.
+static __device__ const uint4 g_zero_chunk = {0u, 0u, 0u, 0u};
 
-// rows of one 8-pixel chunk: X = row y, T1 = row y-1, TS = row y-py
-struct ChunkRows {
-  uint4 X, T1, TS;
-};
-
-// Branch-free chunk load: rows above the frame read as 0 (the reference's
-// out-of-bounds neighbours, _kernels.py:33-35); TEMP forms (F - P) mod 2^16.
-template <bool TEMP>
-__device__ __forceinline__ uint4 ld_row(const uint16_t *__restrict__ s,
-                                        const uint16_t *__restrict__ p, int64_t off, bool ok) {
-  const int64_t o = ok ? off : 0;
-  uint4 a = __ldg(reinterpret_cast<const uint4 *>(s + o));
-  if constexpr (TEMP) {
-    const uint4 b = __ldg(reinterpret_cast<const uint4 *>(p + o));
-    a.x = sub16x2(a.x, b.x); a.y = sub16x2(a.y, b.y);
-    a.z = sub16x2(a.z, b.z); a.w = sub16x2(a.w, b.w);
-  }
-  if (!ok) a = make_uint4(0, 0, 0, 0);
-  return a;
+// 128-bit read-only load whose position in the instruction stream is pinned
+// (volatile asm is not sunk toward its use, so the next chunk's rows really
+// are in flight while the current chunk is processed).
+__device__ __forceinline__ uint4 ldg_v4_pinned(const uint16_t *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
 }
+
+// Raw rows of one 8-pixel chunk: X = row y, T1 = row y-1, TS = row y-py
+// (and the same rows of the previous frame for temporal candidates; the
+// modular delta is formed when the chunk is consumed, not when it is loaded).
+struct ChunkRows {
+  uint4 X, T1, TS, pX, pT1, pTS;
+};
 
 template <bool TEMP, bool NT1, bool NTS>
 __device__ __forceinline__ ChunkRows ld_chunk_rows(const uint16_t *s, const uint16_t *p, int W,
                                                    int py, int y, int x0) {
+  const uint16_t *z = reinterpret_cast<const uint16_t *>(&g_zero_chunk);
   const int64_t off = (int64_t)y * W + x0;
+  const int64_t o1 = off - W, os = off - (int64_t)py * W;
   ChunkRows c;
-  c.X = ld_row<TEMP>(s, p, off, true);
-  c.T1 = NT1 ? ld_row<TEMP>(s, p, off - W, y >= 1) : make_uint4(0, 0, 0, 0);
-  c.TS = NTS ? ld_row<TEMP>(s, p, off - (int64_t)py * W, y >= py) : make_uint4(0, 0, 0, 0);
+  c.X = ldg_v4_pinned(s + off);
+  if constexpr (NT1) c.T1 = ldg_v4_pinned(y >= 1 ? s + o1 : z);
+  if constexpr (NTS) c.TS = ldg_v4_pinned(y >= py ? s + os : z);
+  if constexpr (TEMP) {
+    c.pX = ldg_v4_pinned(p + off);
+    if constexpr (NT1) c.pT1 = ldg_v4_pinned(y >= 1 ? p + o1 : z);
+    if constexpr (NTS) c.pTS = ldg_v4_pinned(y >= py ? p + os : z);
+  }
   return c;
+}
+
+__device__ __forceinline__ uint4 sub16x2_4(const uint4 &a, const uint4 &b) {
+  return make_uint4(sub16x2(a.x, b.x), sub16x2(a.y, b.y), sub16x2(a.z, b.z), sub16x2(a.w, b.w));
+}
+
+// source rows of a chunk: the frame, or (F - P) mod 2^16 (predictors.py:116-120)
+template <bool TEMP, bool NT1, bool NTS>
+__device__ __forceinline__ void source_rows(const ChunkRows &c, uint4 &X, uint4 &T1, uint4 &TS) {
+  const uint4 Z = make_uint4(0, 0, 0, 0);
+  if constexpr (TEMP) {
+    X = sub16x2_4(c.X, c.pX);
+    T1 = NT1 ? sub16x2_4(c.T1, c.pT1) : Z;
+    TS = NTS ? sub16x2_4(c.TS, c.pTS) : Z;
+  } else {
+    X = c.X;
+    T1 = NT1 ? c.T1 : Z;
+    TS = NTS ? c.TS : Z;
+  }
 }
 
 // Left-neighbour history carried between chunks of one row (zero at a row start).
@@ -44,14 +71,14 @@ struct History {
 // Residuals of the 8 pixels of a chunk for compile-time predictor ID and
 // lenslet pitch PX (_kernels.py:46-66, 179-186).
 template <int PX, int ID>
-__device__ __forceinline__ void chunk_residuals8(const ChunkRows &c, const History &h,
-                                                 uint32_t (&r)[8]) {
+__device__ __forceinline__ void chunk_residuals8(const uint4 &cX, const uint4 &cT1, const uint4 &cTS,
+                                                 const History &h, uint32_t (&r)[8]) {
   constexpr int GRP = ID == 0 ? -1 : (ID - 1) / 4;
   constexpr int F = ID == 0 ? 0 : (ID - 1) % 4 + 1;
   constexpr bool kT1 = GRP == 0 || GRP == 2;
   constexpr bool kTS = GRP == 1 || GRP == 2;
   int X[8];
-  unpack8(c.X, X);
+  unpack8(cX, X);
   if constexpr (GRP < 0) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) r[i] = (uint32_t)X[i];
@@ -59,9 +86,9 @@ __device__ __forceinline__ void chunk_residuals8(const ChunkRows &c, const Histo
   } else {
     int T1[8], TS[8], H1[8], H2[8], S1[8], S2[8], t1h[8];
     unpack8(h.X1, H1);
-    if constexpr (kT1) { unpack8(c.T1, T1); unpack8(h.T1, t1h); }
+    if constexpr (kT1) { unpack8(cT1, T1); unpack8(h.T1, t1h); }
     if constexpr (kTS) {
-      unpack8(c.TS, TS); unpack8(h.S1, S1);
+      unpack8(cTS, TS); unpack8(h.S1, S1);
       if constexpr (PX > 8) { unpack8(h.X2, H2); unpack8(h.S2, S2); }
     }
 #pragma unroll
@@ -129,20 +156,9 @@ __device__ __forceinline__ void chunk_events(const ChainState &cs, const uint32_
   }
 }
 
-// Advance history past a chunk that ended at column x0 + 8.
-template <int PX, int ID>
-__device__ __forceinline__ void advance_history(History &h, const ChunkRows &c, bool row_end) {
-  const uint4 Z = make_uint4(0, 0, 0, 0);
-  if (row_end) {
-    h.X1 = h.X2 = h.T1 = h.S1 = h.S2 = Z;  // next chunk starts a row: left neighbours are 0
-  } else {
-    h.X2 = h.X1; h.X1 = c.X; h.T1 = c.T1; h.S2 = h.S1; h.S1 = c.TS;
-  }
-}
-
-// One lane's run of `nch` chunks starting at pixel a (a % 8 == 0).  Chunks are
-// processed in pairs with the next pair's rows already in flight (explicit
-// double buffering: the loads are consumed one pair later).
+// One lane's run of `nch` chunks starting at pixel a (a % 8 == 0).  The next
+// chunk's rows are issued at the top of each iteration (pinned loads) and
+// consumed one iteration later.
 template <int PX, int ID, bool TEMP>
 __device__ __noinline__ void lane_fast(const uint16_t *__restrict__ src,
                                        const uint16_t *__restrict__ prv, int W, int py,
@@ -156,48 +172,41 @@ __device__ __noinline__ void lane_fast(const uint16_t *__restrict__ src,
   uint32_t prev_lo = residual_at(src, prv, W, (int)(q / W), (int)(q % W), cfg) & 0xFFu;
   int y = (int)(a / W), x0 = (int)(a % W);
   History h;
-  {  // history of a run that starts mid-row
+  {  // history of a run that starts mid-row (rare: plain loads)
+    const uint4 Z = make_uint4(0, 0, 0, 0);
     const int64_t off = (int64_t)y * W + x0;
     const int64_t offs = off - (int64_t)py * W;
-    h.X1 = ld_row<TEMP>(src, prv, off - 8, GRP >= 0 && x0 >= 8);
-    h.X2 = ld_row<TEMP>(src, prv, off - 16, kTS && PX > 8 && x0 >= 16);
-    h.T1 = ld_row<TEMP>(src, prv, off - W - 8, kT1 && x0 >= 8 && y >= 1);
-    h.S1 = ld_row<TEMP>(src, prv, offs - 8, kTS && x0 >= 8 && y >= py);
-    h.S2 = ld_row<TEMP>(src, prv, offs - 16, kTS && PX > 8 && x0 >= 16 && y >= py);
+    auto row = [&](int64_t o, bool ok) -> uint4 {
+      if (!ok) return Z;
+      uint4 v = __ldg(reinterpret_cast<const uint4 *>(src + o));
+      if constexpr (TEMP) v = sub16x2_4(v, __ldg(reinterpret_cast<const uint4 *>(prv + o)));
+      return v;
+    };
+    h.X1 = row(off - 8, GRP >= 0 && x0 >= 8);
+    h.X2 = row(off - 16, kTS && PX > 8 && x0 >= 16);
+    h.T1 = row(off - W - 8, kT1 && x0 >= 8 && y >= 1);
+    h.S1 = row(offs - 8, kTS && x0 >= 8 && y >= py);
+    h.S2 = row(offs - 16, kTS && PX > 8 && x0 >= 16 && y >= py);
   }
-  // positions of chunks c (y, x0) and c + 1 (y1, x1)
-  auto step = [&](int &yy, int &xx) {
-    xx += 8;
-    if (xx == W) { xx = 0; ++yy; }
-  };
-  int y1 = y, x1 = x0;
-  step(y1, x1);
-  const int64_t last_c = nch - 1;
-  ChunkRows c0 = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, y, x0);
-  ChunkRows c1 = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, nch > 1 ? y1 : y,
-                                              nch > 1 ? x1 : x0);
-  for (int64_t c = 0; c < nch; c += 2) {
-    // rows of chunks c+2, c+3 (clamped to the run: never read past it)
-    int y2 = y1, x2 = x1;
-    step(y2, x2);
-    int y3 = y2, x3 = x2;
-    step(y3, x3);
-    const bool has2 = c + 2 <= last_c, has3 = c + 3 <= last_c;
-    const ChunkRows n0 = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, has2 ? y2 : y,
-                                                      has2 ? x2 : x0);
-    const ChunkRows n1 = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, has3 ? y3 : y,
-                                                      has3 ? x3 : x0);
+  ChunkRows cur = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, y, x0);
+  for (int64_t c = 0; c < nch; ++c) {
+    int y1 = y, x1 = x0 + 8;
+    if (x1 == W) { x1 = 0; ++y1; }
+    const bool more = c + 1 < nch;
+    const ChunkRows nxt = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, more ? y1 : y,
+                                                       more ? x1 : x0);
+    uint4 X, T1, TS;
+    source_rows<TEMP, kT1, kTS>(cur, X, T1, TS);
     uint32_t r[8];
-    chunk_residuals8<PX, ID>(c0, h, r);
+    chunk_residuals8<PX, ID>(X, T1, TS, h, r);
     chunk_events(cs, r, prev_lo);
-    advance_history<PX, ID>(h, c0, x1 == 0);
-    if (c + 1 <= last_c) {
-      chunk_residuals8<PX, ID>(c1, h, r);
-      chunk_events(cs, r, prev_lo);
-      advance_history<PX, ID>(h, c1, x2 == 0);
+    if (x1 == 0) {
+      h.X1 = h.X2 = h.T1 = h.S1 = h.S2 = make_uint4(0, 0, 0, 0);  // next chunk starts a row
+    } else {
+      h.X2 = h.X1; h.X1 = X; h.T1 = T1; h.S2 = h.S1; h.S1 = TS;
     }
-    y = y2; x0 = x2; y1 = y3; x1 = x3;
-    c0 = n0; c1 = n1;
+    y = y1; x0 = x1;
+    cur = nxt;
   }
 }
 
@@ -209,4 +218,3 @@ __device__ __forceinline__ void lane_fast_dispatch(int id, const uint16_t *src,
                                                    std::integer_sequence<int, IDs...>) {
   ((id == IDs ? lane_fast<PX, IDs, TEMP>(src, prv, W, py, npix, a, nch, cfg, cs) : void()), ...);
 }
-
