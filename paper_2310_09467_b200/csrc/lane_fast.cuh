@@ -117,10 +117,28 @@ __device__ __forceinline__ void chunk_residuals8(const uint4 &cX, const uint4 &c
 // 16-bit load + store each); phase B issues one unconditional shared atomic
 // per event -- a first occurrence (last == 0x100, bin 0x100xx) lands in the
 // dummy row past the histogram.  A counter found with bit 15 set in any
-// returned word is claimed at the end of the chunk; the kernel sweeps once
-// more after the loop for crossings nobody observed.
+// returned word is claimed one chunk later (the returned words of chunk c are
+// examined after chunk c+1's atomics are issued, so nothing waits on them);
+// the kernel sweeps once more after the loop for crossings nobody observed.
+//
+// Deferred state of the previous chunk: its returned words and its words.
+struct Pending {
+  uint32_t old[16], word[16];
+};
+
+__device__ __forceinline__ void settle_pending(const ChainState &cs, const Pending &pd) {
+  uint32_t flag = 0;
+#pragma unroll
+  for (int e = 0; e < 16; e += 2) flag |= pd.old[e] | pd.old[e + 1];
+  if (flag & 0x80008000u) {  // some counter has crossed 0x8000: claim
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      if (pd.word[e] < (uint32_t)kHistWords) claim_word(cs, pd.word[e]);
+  }
+}
+
 __device__ __forceinline__ void chunk_events(const ChainState &cs, const uint32_t (&r)[8],
-                                             uint32_t &prev_lo) {
+                                             uint32_t &prev_lo, Pending &pd) {
   uint32_t key[16], prd[16];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -137,22 +155,20 @@ __device__ __forceinline__ void chunk_events(const ChainState &cs, const uint32_
     last[e] = lds_u16(la);
     sts_u16(la, prd[e]);
   }
-  uint32_t flag = 0, fresh = 0, word[16];
+  uint32_t fresh = 0, word[16], old[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     fresh |= last[e];
     word[e] = last[e] * 128u + (prd[e] >> 1);  // bin = last * 256 + pred, 2 bins/word
-    flag |= atoms_add(cs.hbase + 4u * word[e], 1u + (prd[e] & 1u) * 0xFFFFu);
+    old[e] = atoms_add(cs.hbase + 4u * word[e], 1u + (prd[e] & 1u) * 0xFFFFu);
   }
+  settle_pending(cs, pd);  // previous chunk's returned words have long arrived
+#pragma unroll
+  for (int e = 0; e < 16; ++e) { pd.old[e] = old[e]; pd.word[e] = word[e]; }
   if (fresh & kUnseen) {  // first occurrence of a key in this run
 #pragma unroll
     for (int e = 0; e < 16; ++e)
       if (last[e] == kUnseen) cs.F[key[e] * kJudgeThreads] = (uint8_t)prd[e];
-  }
-  if (flag & 0x80008000u) {  // some counter has crossed 0x8000: claim
-#pragma unroll
-    for (int e = 0; e < 16; ++e)
-      if (word[e] < (uint32_t)kHistWords) claim_word(cs, word[e]);
   }
 }
 
@@ -189,6 +205,9 @@ __device__ __noinline__ void lane_fast(const uint16_t *__restrict__ src,
     h.S2 = row(offs - 16, kTS && PX > 8 && x0 >= 16 && y >= py);
   }
   ChunkRows cur = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, y, x0);
+  Pending pd;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) { pd.old[e] = 0; pd.word[e] = ~0u; }
   for (int64_t c = 0; c < nch; ++c) {
     int y1 = y, x1 = x0 + 8;
     if (x1 == W) { x1 = 0; ++y1; }
@@ -199,7 +218,7 @@ __device__ __noinline__ void lane_fast(const uint16_t *__restrict__ src,
     source_rows<TEMP, kT1, kTS>(cur, X, T1, TS);
     uint32_t r[8];
     chunk_residuals8<PX, ID>(X, T1, TS, h, r);
-    chunk_events(cs, r, prev_lo);
+    chunk_events(cs, r, prev_lo, pd);
     if (x1 == 0) {
       h.X1 = h.X2 = h.T1 = h.S1 = h.S2 = make_uint4(0, 0, 0, 0);  // next chunk starts a row
     } else {
@@ -208,6 +227,7 @@ __device__ __noinline__ void lane_fast(const uint16_t *__restrict__ src,
     y = y1; x0 = x1;
     cur = nxt;
   }
+  settle_pending(cs, pd);
 }
 
 template <int PX, bool TEMP, int... IDs>
