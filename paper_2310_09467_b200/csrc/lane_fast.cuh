@@ -148,27 +148,28 @@ __device__ __forceinline__ void chunk_events(const ChainState &cs, const uint32_
     prd[2 * i + 1] = r[i] >> 8;
   }
   prev_lo = r[7] & 0xFFu;
-  uint32_t last[16];
+  uint32_t last[16];  // last-pred codes (lt_code), kUnseenCode for a first occurrence
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     const uint32_t la = cs.lbase + key[e] * 2u + (key[e] >> 1) * (4u * kJudgeThreads - 4u);
     last[e] = lds_u16(la);
-    sts_u16(la, prd[e]);
+    sts_u16(la, lt_code(prd[e]));
   }
-  uint32_t fresh = 0, word[16], old[16];
+  // the previous chunk's returned words arrived long ago; examining them
+  // first frees their registers, so this chunk's atomics return straight
+  // into the pending state (no copies that would wait on them)
+  settle_pending(cs, pd);
+  uint32_t fresh = 0;
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     fresh |= last[e];
-    word[e] = last[e] * 128u + (prd[e] >> 1);  // bin = last * 256 + pred, 2 bins/word
-    old[e] = atoms_add(cs.hbase + 4u * word[e], 1u + (prd[e] & 1u) * 0xFFFFu);
+    pd.word[e] = hist_word(last[e], prd[e]);  // bin = last * 256 + pred, 2 bins/word
+    pd.old[e] = atoms_add(cs.hbase + 4u * pd.word[e], 1u + (prd[e] & 1u) * 0xFFFFu);
   }
-  settle_pending(cs, pd);  // previous chunk's returned words have long arrived
-#pragma unroll
-  for (int e = 0; e < 16; ++e) { pd.old[e] = old[e]; pd.word[e] = word[e]; }
-  if (fresh & kUnseen) {  // first occurrence of a key in this run
+  if (fresh & kUnseenCode) {  // first occurrence of a key in this run
 #pragma unroll
     for (int e = 0; e < 16; ++e)
-      if (last[e] == kUnseen) cs.F[key[e] * kJudgeThreads] = (uint8_t)prd[e];
+      if (last[e] == kUnseenCode) cs.F[key[e] * kJudgeThreads] = (uint8_t)prd[e];
   }
 }
 
