@@ -159,7 +159,7 @@ size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 int lone_weight() {
   static int w = [] {
     const char *e = getenv("PCBZ_LONE_WEIGHT");
-    const int v = e ? atoi(e) : 20;
+    const int v = e ? atoi(e) : 16;  // equal runs measured best (profiles/r01_notes.md)
     return v < 8 ? 8 : (v > 64 ? 64 : v);
   }();
   return w;

@@ -205,28 +205,55 @@ __device__ __noinline__ void lane_fast(const uint16_t *__restrict__ src,
     h.S1 = row(offs - 8, kTS && x0 >= 8 && y >= py);
     h.S2 = row(offs - 16, kTS && PX > 8 && x0 >= 16 && y >= py);
   }
-  ChunkRows cur = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, y, x0);
+  // Software pipeline: iteration c issues the rows of chunk c+2, computes the
+  // residuals of chunk c+1 and runs the events of chunk c -- two independent
+  // dependency chains the scheduler can interleave.
+  auto step = [&](int &yy, int &xx) {
+    xx += 8;
+    if (xx == W) { xx = 0; ++yy; }
+  };
+  auto advance = [&](const uint4 &X, const uint4 &T1, const uint4 &TS, bool row_start) {
+    if (row_start) {
+      h.X1 = h.X2 = h.T1 = h.S1 = h.S2 = make_uint4(0, 0, 0, 0);  // left neighbours are 0
+    } else {
+      h.X2 = h.X1; h.X1 = X; h.T1 = T1; h.S2 = h.S1; h.S1 = TS;
+    }
+  };
+  int y1 = y, x1 = x0;
+  step(y1, x1);  // chunk c+1
+  uint32_t r_cur[8];
+  ChunkRows raw_next;
+  {
+    const ChunkRows raw0 = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, y, x0);
+    raw_next = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, nch > 1 ? y1 : y, nch > 1 ? x1 : x0);
+    uint4 X, T1, TS;
+    source_rows<TEMP, kT1, kTS>(raw0, X, T1, TS);
+    chunk_residuals8<PX, ID>(X, T1, TS, h, r_cur);
+    advance(X, T1, TS, x1 == 0);
+  }
   Pending pd;
 #pragma unroll
   for (int e = 0; e < 16; ++e) { pd.old[e] = 0; pd.word[e] = ~0u; }
   for (int64_t c = 0; c < nch; ++c) {
-    int y1 = y, x1 = x0 + 8;
-    if (x1 == W) { x1 = 0; ++y1; }
-    const bool more = c + 1 < nch;
-    const ChunkRows nxt = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, more ? y1 : y,
-                                                       more ? x1 : x0);
-    uint4 X, T1, TS;
-    source_rows<TEMP, kT1, kTS>(cur, X, T1, TS);
-    uint32_t r[8];
-    chunk_residuals8<PX, ID>(X, T1, TS, h, r);
-    chunk_events(cs, r, prev_lo, pd);
-    if (x1 == 0) {
-      h.X1 = h.X2 = h.T1 = h.S1 = h.S2 = make_uint4(0, 0, 0, 0);  // next chunk starts a row
-    } else {
-      h.X2 = h.X1; h.X1 = X; h.T1 = T1; h.S2 = h.S1; h.S1 = TS;
+    int y2 = y1, x2 = x1;
+    step(y2, x2);  // chunk c+2
+    const bool has2 = c + 2 < nch;
+    const ChunkRows raw2 = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, has2 ? y2 : y,
+                                                        has2 ? x2 : x0);
+    // residuals of chunk c+1 (past the run's end they are computed on valid,
+    // clamped rows and never used)
+    uint32_t r_next[8];
+    {
+      uint4 X, T1, TS;
+      source_rows<TEMP, kT1, kTS>(raw_next, X, T1, TS);
+      chunk_residuals8<PX, ID>(X, T1, TS, h, r_next);
+      advance(X, T1, TS, x2 == 0);
     }
-    y = y1; x0 = x1;
-    cur = nxt;
+    chunk_events(cs, r_cur, prev_lo, pd);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r_cur[i] = r_next[i];
+    raw_next = raw2;
+    x1 = x2; y1 = y2;
   }
   settle_pending(cs, pd);
 }
