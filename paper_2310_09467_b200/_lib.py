@@ -63,7 +63,8 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
     global _lib
     with _lock:
         if _lib is None:
-            p = Path(path) if path else LIB_PATH
+            import os
+            p = Path(path) if path else Path(os.environ.get("PCBZ_LIB", LIB_PATH))
             if not p.exists():
                 raise ImportError(
                     f"{p} is missing: build it with `python -m paper_2310_09467_b200.build_native` "

@@ -57,16 +57,23 @@ def _stale(target: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
-def build_library(force: bool = False, verbose: bool = False, jobs: int | None = None) -> Path:
-    if not force and not _stale(LIB, _deps()):
-        return LIB
-    OUT_DIR.mkdir(exist_ok=True)
+def build_library(force: bool = False, verbose: bool = False, jobs: int | None = None,
+                  defines: tuple = (), out_dir: Path | None = None) -> Path:
+    """Compile and link libpcbz_b200.so.  `defines` / `out_dir` build an
+    experimental variant (e.g. ("PCBZ_SWIZZLE=0",)) into its own directory;
+    _lib.load() picks a variant up through the PCBZ_LIB environment variable."""
+    out = Path(out_dir) if out_dir else OUT_DIR
+    lib = out / LIB.name
+    if not force and not _stale(lib, _deps()):
+        return lib
+    out.mkdir(parents=True, exist_ok=True)
     nvcc = _nvcc()
+    dflags = [f"-D{d}" for d in defines]
 
     def compile_one(unit):
         src, extra, obj = unit
-        cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-c", str(CSRC / src),
-               "-o", str(OUT_DIR / obj)]
+        cmd = [nvcc, *NVCC_FLAGS, *dflags, *extra, "-I", str(ROOT / "include"), "-c",
+               str(CSRC / src), "-o", str(out / obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src} {extra}:\n{r.stdout}\n{r.stderr}")
@@ -75,17 +82,17 @@ def build_library(force: bool = False, verbose: bool = False, jobs: int | None =
     units = _units()
     with ThreadPoolExecutor(jobs or max(1, os.cpu_count() or 1)) as pool:
         logs = list(pool.map(compile_one, units))
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *[str(OUT_DIR / u[2]) for u in units],
+    tmp = lib.with_suffix(".so.tmp")
+    cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *[str(out / u[2]) for u in units],
            "-Xcompiler", "-fPIC"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    (OUT_DIR / "ptxas.log").write_text("\n".join(logs))
+    os.replace(tmp, lib)
+    (out / "ptxas.log").write_text("\n".join(logs))
     if verbose:
         print("\n".join(logs))
-    return LIB
+    return lib
 
 
 def build_oracle() -> Path | None:

@@ -74,9 +74,13 @@ __device__ __forceinline__ PairRef pair_ref(const JudgeParams &P, int64_t pair) 
 // marks a key not seen yet in a run and maps first occurrences to the dummy
 // row 0x8000 ^ (pred >> 1) past the histogram.
 constexpr uint32_t kUnseenCode = 0x8000;
+#ifndef PCBZ_SWIZZLE
+#define PCBZ_SWIZZLE 1
+#endif
+constexpr uint32_t kSwizzleMul = PCBZ_SWIZZLE ? 13u : 0u;
 
 __device__ __forceinline__ uint32_t lt_code(uint32_t pred) {
-  return (pred << 7) | ((pred * 13u) & 127u);
+  return (pred << 7) | ((pred * kSwizzleMul) & 127u);
 }
 __device__ __forceinline__ uint32_t hist_word(uint32_t code, uint32_t pred) {
   return code ^ (pred >> 1);
@@ -86,7 +90,7 @@ __device__ __forceinline__ uint32_t word_of_bin(uint32_t bin) {
 }
 __device__ __forceinline__ uint32_t bin_of_word(uint32_t word, uint32_t half) {
   const uint32_t last = word >> 7;
-  return (last << 8) | ((((word & 127u) ^ ((last * 13u) & 127u)) << 1) | half);
+  return (last << 8) | ((((word & 127u) ^ ((last * kSwizzleMul) & 127u)) << 1) | half);
 }
 __device__ __forceinline__ uint32_t bin_count16(const uint32_t *hist, uint32_t bin) {
   return (hist[word_of_bin(bin)] >> ((bin & 1u) << 4)) & 0xFFFFu;

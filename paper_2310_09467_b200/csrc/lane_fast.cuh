@@ -158,13 +158,21 @@ __device__ __forceinline__ void chunk_events(const ChainState &cs, const uint32_
   // the previous chunk's returned words arrived long ago; examining them
   // first frees their registers, so this chunk's atomics return straight
   // into the pending state (no copies that would wait on them)
-  settle_pending(cs, pd);
+#ifndef PCBZ_DEFER
+#define PCBZ_DEFER 1
+#endif
+  if constexpr (PCBZ_DEFER) settle_pending(cs, pd);
   uint32_t fresh = 0;
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     fresh |= last[e];
     pd.word[e] = hist_word(last[e], prd[e]);  // bin = last * 256 + pred, 2 bins/word
     pd.old[e] = atoms_add(cs.hbase + 4u * pd.word[e], 1u + (prd[e] & 1u) * 0xFFFFu);
+  }
+  if constexpr (!PCBZ_DEFER) {  // examine this chunk's returned words right away
+    settle_pending(cs, pd);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) pd.old[e] = 0;
   }
   if (fresh & kUnseenCode) {  // first occurrence of a key in this run
 #pragma unroll
@@ -204,6 +212,38 @@ __device__ __noinline__ void lane_fast(const uint16_t *__restrict__ src,
     h.T1 = row(off - W - 8, kT1 && x0 >= 8 && y >= 1);
     h.S1 = row(offs - 8, kTS && x0 >= 8 && y >= py);
     h.S2 = row(offs - 16, kTS && PX > 8 && x0 >= 16 && y >= py);
+  }
+#ifndef PCBZ_PIPELINE
+#define PCBZ_PIPELINE 0
+#endif
+  if constexpr (!PCBZ_PIPELINE) {
+    // plain form: iteration c issues the rows of chunk c+1, then computes the
+    // residuals and events of chunk c
+    ChunkRows cur = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, y, x0);
+    Pending pd;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) { pd.old[e] = 0; pd.word[e] = ~0u; }
+    for (int64_t c = 0; c < nch; ++c) {
+      int y1 = y, x1 = x0 + 8;
+      if (x1 == W) { x1 = 0; ++y1; }
+      const bool more = c + 1 < nch;
+      const ChunkRows nxt = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, more ? y1 : y,
+                                                         more ? x1 : x0);
+      uint4 X, T1, TS;
+      source_rows<TEMP, kT1, kTS>(cur, X, T1, TS);
+      uint32_t r[8];
+      chunk_residuals8<PX, ID>(X, T1, TS, h, r);
+      chunk_events(cs, r, prev_lo, pd);
+      if (x1 == 0) {
+        h.X1 = h.X2 = h.T1 = h.S1 = h.S2 = make_uint4(0, 0, 0, 0);  // next chunk starts a row
+      } else {
+        h.X2 = h.X1; h.X1 = X; h.T1 = T1; h.S2 = h.S1; h.S1 = TS;
+      }
+      y = y1; x0 = x1;
+      cur = nxt;
+    }
+    settle_pending(cs, pd);
+    return;
   }
   // Software pipeline: iteration c issues the rows of chunk c+2, computes the
   // residuals of chunk c+1 and runs the events of chunk c -- two independent

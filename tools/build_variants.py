@@ -1,0 +1,23 @@
+"""Build experimental variants of libpcbz_b200.so side by side for A/B runs
+(select one at run time with PCBZ_LIB=<path>)."""
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+from paper_2310_09467_b200 import build_native  # noqa: E402
+
+VARIANTS = {
+    "s0p0d0": ("PCBZ_SWIZZLE=0", "PCBZ_PIPELINE=0", "PCBZ_DEFER=0"),
+    "s0p0d1": ("PCBZ_SWIZZLE=0", "PCBZ_PIPELINE=0", "PCBZ_DEFER=1"),
+    "s1p0d1": ("PCBZ_SWIZZLE=1", "PCBZ_PIPELINE=0", "PCBZ_DEFER=1"),
+    "s1p1d1": ("PCBZ_SWIZZLE=1", "PCBZ_PIPELINE=1", "PCBZ_DEFER=1"),
+    "s0p1d1": ("PCBZ_SWIZZLE=0", "PCBZ_PIPELINE=1", "PCBZ_DEFER=1"),
+    "s1p0d0": ("PCBZ_SWIZZLE=1", "PCBZ_PIPELINE=0", "PCBZ_DEFER=0"),
+}
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(VARIANTS)
+    for n in names:
+        out = ROOT / "paper_2310_09467_b200" / "_native" / "variants" / n
+        print(n, build_native.build_library(force=True, defines=VARIANTS[n], out_dir=out), flush=True)
