@@ -37,12 +37,15 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found; the CUDA toolkit is required to build libpcbz_b200.so")
 
 
-def _units():
-    """(source, extra flags, object name) of every translation unit."""
+def _units(pitches=None):
+    """(source, extra flags, object name) of every translation unit; pitches
+    not in `pitches` (None = all) get an empty stub."""
     units = [("judge.cu", [], "judge.o"), ("aux_kernels.cu", [], "aux_kernels.o"),
              ("capi.cu", [], "capi.o")]
-    units += [("judge_px.cu", [f"-DPCBZ_PX={px}"], f"judge_px{px}.o")
-              for px in range(MAX_FAST_PITCH + 1)]
+    for px in range(MAX_FAST_PITCH + 1):
+        stub = pitches is not None and px not in pitches and px != 0
+        units.append(("judge_px.cu", [f"-DPCBZ_PX={px}"] + (["-DPCBZ_STUB=1"] if stub else []),
+                      f"judge_px{px}.o"))
     return units
 
 
@@ -58,7 +61,7 @@ def _stale(target: Path, deps) -> bool:
 
 
 def build_library(force: bool = False, verbose: bool = False, jobs: int | None = None,
-                  defines: tuple = (), out_dir: Path | None = None) -> Path:
+                  defines: tuple = (), out_dir: Path | None = None, pitches=None) -> Path:
     """Compile and link libpcbz_b200.so.  `defines` / `out_dir` build an
     experimental variant (e.g. ("PCBZ_SWIZZLE=0",)) into its own directory;
     _lib.load() picks a variant up through the PCBZ_LIB environment variable."""
@@ -79,7 +82,7 @@ def build_library(force: bool = False, verbose: bool = False, jobs: int | None =
             raise RuntimeError(f"nvcc failed for {src} {extra}:\n{r.stdout}\n{r.stderr}")
         return f"== {src} {' '.join(extra)}\n{r.stdout}{r.stderr}"
 
-    units = _units()
+    units = _units(pitches)
     with ThreadPoolExecutor(jobs or max(1, os.cpu_count() or 1)) as pool:
         logs = list(pool.map(compile_one, units))
     tmp = lib.with_suffix(".so.tmp")

@@ -1,10 +1,15 @@
-// judge_px.cu -- one instantiation of the histogram kernel per fast-path
-// pitch.  build_native.py compiles this file once per PCBZ_PX in
-// [0, kMaxFastPitch] (0 = generic path), in parallel.
+// judge_px.cu -- one instantiation of the histogram kernel (and the chunked
+// emission kernel) per fast-path pitch.  build_native.py compiles this file
+// once per PCBZ_PX in [0, kMaxFastPitch] (0 = generic path), in parallel.
+// PCBZ_STUB=1 builds an empty placeholder (experimental variant builds that
+// only need some pitches); the host never selects a stubbed pitch there.
 #include "judge_kernel.cuh"
 
 #ifndef PCBZ_PX
 #error "compile with -DPCBZ_PX=<pitch>"
+#endif
+#ifndef PCBZ_STUB
+#define PCBZ_STUB 0
 #endif
 
 #define PCBZ_CAT2(a, b) a##b
@@ -12,6 +17,11 @@
 
 namespace pcbz {
 
+#if PCBZ_STUB
+cudaError_t PCBZ_CAT(judge_configure_px, PCBZ_PX)() { return cudaSuccess; }
+void PCBZ_CAT(judge_launch_px, PCBZ_PX)(const JudgeParams &, int, cudaStream_t) {}
+void PCBZ_CAT(emit_launch_px, PCBZ_PX)(const EmitParams &, int, cudaStream_t) {}
+#else
 cudaError_t PCBZ_CAT(judge_configure_px, PCBZ_PX)() {
   return cudaFuncSetAttribute(judge_hist_kernel<PCBZ_PX>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kJudgeSmemBytes);
@@ -21,12 +31,9 @@ void PCBZ_CAT(judge_launch_px, PCBZ_PX)(const JudgeParams &p, int grid, cudaStre
   judge_hist_kernel<PCBZ_PX><<<grid, kJudgeThreads, kJudgeSmemBytes, st>>>(p);
 }
 
-}  // namespace pcbz
-
-namespace pcbz {
-
 void PCBZ_CAT(emit_launch_px, PCBZ_PX)(const EmitParams &p, int grid, cudaStream_t st) {
   if constexpr (PCBZ_PX > 0) emit_chunks_kernel<PCBZ_PX><<<grid, 256, 0, st>>>(p);
 }
+#endif
 
 }  // namespace pcbz

@@ -1,4 +1,4 @@
-"""Build experimental variants of libpcbz_b200.so side by side for A/B runs
+"""Build experimental variants (fast path for pitch 15 only, the C2 bench pitch) of libpcbz_b200.so side by side for A/B runs
 (select one at run time with PCBZ_LIB=<path>)."""
 import sys
 from pathlib import Path
@@ -20,4 +20,4 @@ if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
     for n in names:
         out = ROOT / "paper_2310_09467_b200" / "_native" / "variants" / n
-        print(n, build_native.build_library(force=True, defines=VARIANTS[n], out_dir=out), flush=True)
+        print(n, build_native.build_library(force=True, defines=VARIANTS[n], out_dir=out, pitches={15}), flush=True)
