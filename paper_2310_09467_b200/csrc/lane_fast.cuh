@@ -159,7 +159,7 @@ __device__ __forceinline__ void chunk_events(const ChainState &cs, const uint32_
   // first frees their registers, so this chunk's atomics return straight
   // into the pending state (no copies that would wait on them)
 #ifndef PCBZ_DEFER
-#define PCBZ_DEFER 1
+#define PCBZ_DEFER 0
 #endif
   if constexpr (PCBZ_DEFER) settle_pending(cs, pd);
   uint32_t fresh = 0;
