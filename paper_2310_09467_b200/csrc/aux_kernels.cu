@@ -80,7 +80,8 @@ __global__ void bwt_scatter_kernel(const uint8_t *s, int64_t n, int64_t nchunks,
 
 __global__ void __launch_bounds__(kEntropyThreads) entropy_u64_kernel(const uint64_t *counts, double total,
                                                                     double *out) {
-  __shared__ NpScratch scr;
+  extern __shared__ uint4 smem_raw[];
+  NpScratch &scr = *reinterpret_cast<NpScratch *>(smem_raw);
   auto get = [&](int bin) -> double { return (double)counts[bin]; };
   const double e = block_entropy(get, total, scr);
   if (threadIdx.x == 0) *out = e;
@@ -146,7 +147,15 @@ cudaError_t launch_counting_bwt(const uint8_t *s, int64_t n, uint8_t *out, uint3
 
 cudaError_t launch_entropy_u64(const uint64_t *counts, double total, double *out,
                                cudaStream_t st) {
-  entropy_u64_kernel<<<1, kEntropyThreads, 0, st>>>(counts, total, out);
+  static bool configured = false;
+  if (!configured) {
+    const cudaError_t e = cudaFuncSetAttribute(entropy_u64_kernel,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)sizeof(NpScratch));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  entropy_u64_kernel<<<1, kEntropyThreads, sizeof(NpScratch), st>>>(counts, total, out);
   return cudaGetLastError();
 }
 

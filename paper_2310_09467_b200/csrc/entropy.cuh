@@ -9,18 +9,23 @@
 // n < 8 -> sequential from -0.0; n <= 128 -> eight interleaved accumulators
 // combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then the n % 8 tail;
 // otherwise split at n/2 rounded down to a multiple of 8 and recurse (numpy
-// _core/src/umath/loops_utils.h.src; checked bit-for-bit against np.sum for
-// n = 1..65536 in tests/test_entropy_emulation.py).  Every term is rounded
-// exactly like numpy's (IEEE division, device log2, IEEE product), so the
-// device entropy equals the reference's whenever log2 rounds alike (both
-// are correctly rounded for nearly all arguments), and mathematically tied
-// candidates tie or break exactly as in the reference.
+// _core/src/umath/loops_utils.h.src; the leaf/fold decomposition below is
+// checked bit-for-bit against np.sum for n = 1..65536 in
+// tests/test_entropy_emulation.py).  Every term is rounded exactly like
+// numpy's (IEEE division, device log2, IEEE product -- explicit _rn
+// intrinsics so nvcc cannot contract them into FMAs), so the device entropy
+// equals the reference's whenever log2 rounds alike (both are correctly
+// rounded for nearly all arguments), and mathematically tied candidates tie
+// or break exactly as in the reference.
 //
 // Parallel form: thread t owns a run of 32-bin occupancy words; a block
 // scan of occupied counts gives every occupied bin its index in the
-// (virtual) compacted term array; the recursion's leaves -- index ranges of
-// at most 128 terms -- are evaluated by different threads walking the
-// occupancy bitmap; thread 0 folds the leaf sums in recursion order.
+// (virtual) compacted term array.  The recursion tree is built breadth-first
+// by one warp (ballot compaction per level); all leaves (index ranges of at
+// most 128 terms) are evaluated in parallel by walking the occupancy bitmap;
+// internal nodes are then folded bottom-up one level at a time.  Each
+// internal node's value is left + right exactly as in the recursion, so the
+// evaluation order across nodes does not matter.
 #pragma once
 #include <cstdint>
 
@@ -28,73 +33,66 @@
 
 namespace pcbz {
 
-constexpr int kNpLeafMax = 1024;  // leaves hold >= 64 terms once n > 128
-constexpr int kNpBlock = 128;     // numpy PW_BLOCKSIZE
-constexpr int kOccWords = 2048;   // 65536 bins / 32
+constexpr int kNpBlock = 128;      // numpy PW_BLOCKSIZE
+constexpr int kOccWords = 2048;    // 65536 bins / 32
+constexpr int kNpNodeMax = 2048;   // <= 1024 leaves (>= 64 terms each once n > 128) + internals
+constexpr int kNpLevelMax = 16;
+constexpr uint32_t kNpLeaf = 0xFFFFFFFFu;
 
 struct NpScratch {
   uint32_t off[kEntropyThreads + 1];  // compacted index of each thread's first term
   uint32_t occ[kOccWords];            // occupancy bitmap
-  uint32_t leaf_beg[kNpLeafMax];
-  uint32_t leaf_len[kNpLeafMax];
-  double leaf_sum[kNpLeafMax];
-  double result;
-  int nleaf;
+  uint32_t node_beg[kNpNodeMax];
+  uint32_t node_len[kNpNodeMax];
+  uint32_t node_child[kNpNodeMax];    // index of the left child (right = +1), or kNpLeaf
+  double node_sum[kNpNodeMax];
+  uint32_t level_start[kNpLevelMax + 1];
+  int nlevels;
 };
 
 __device__ __forceinline__ int occ_word_lo(int t) { return (kOccWords * t) / kEntropyThreads; }
 
-// leaves of numpy's pairwise recursion over n terms, in left-to-right order
-__device__ inline void np_enumerate_leaves(uint32_t n, NpScratch &S) {
-  uint32_t st_b[48], st_n[48];
-  int sp = 0, nl = 0;
-  st_b[sp] = 0; st_n[sp] = n; ++sp;
-  while (sp) {
-    --sp;
-    const uint32_t b = st_b[sp], m = st_n[sp];
-    if (m <= (uint32_t)kNpBlock) {
-      S.leaf_beg[nl] = b; S.leaf_len[nl] = m; ++nl;
-    } else {
-      uint32_t h = m / 2;
-      h -= h % 8;
-      st_b[sp] = b + h; st_n[sp] = m - h; ++sp;  // right half is popped after the left
-      st_b[sp] = b; st_n[sp] = h; ++sp;
-    }
+// Breadth-first recursion tree of numpy's pairwise sum over n terms; one warp.
+__device__ inline void np_build_tree(uint32_t n, NpScratch &S) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    S.node_beg[0] = 0;
+    S.node_len[0] = n;
+    S.level_start[0] = 0;
+    S.level_start[1] = 1;
   }
-  S.nleaf = nl;
-}
-
-// pairwise(a, n) = pairwise(left) + pairwise(right), from the leaf sums
-__device__ inline double np_fold(uint32_t n, const NpScratch &S) {
-  uint32_t st_n[48];
-  uint8_t st_state[48];
-  double st_left[48];
-  int sp = 1, leaf = 0;
-  double ret = 0.0;
-  st_n[0] = n; st_state[0] = 0;
-  while (sp) {
-    const int top = sp - 1;
-    const uint32_t m = st_n[top];
-    if (m <= (uint32_t)kNpBlock) {
-      ret = S.leaf_sum[leaf++];
-      --sp;
-      continue;
+  __syncwarp();
+  int L = 0;
+  for (;; ++L) {
+    const uint32_t start = S.level_start[L], end = S.level_start[L + 1];
+    uint32_t produced = 0;
+    for (uint32_t base = start; base < end; base += 32) {
+      const uint32_t i = base + lane;
+      const bool valid = i < end;
+      const uint32_t len = valid ? S.node_len[i] : 0;
+      const bool internal = valid && len > (uint32_t)kNpBlock;
+      const uint32_t m = __ballot_sync(0xffffffffu, internal);
+      if (internal) {
+        const uint32_t child = end + produced + 2 * __popc(m & ((1u << lane) - 1u));
+        uint32_t h = len / 2;
+        h -= h % 8;
+        const uint32_t b = S.node_beg[i];
+        S.node_beg[child] = b;
+        S.node_len[child] = h;
+        S.node_beg[child + 1] = b + h;
+        S.node_len[child + 1] = len - h;
+        S.node_child[i] = child;
+      } else if (valid) {
+        S.node_child[i] = kNpLeaf;
+      }
+      produced += 2 * __popc(m);
     }
-    uint32_t h = m / 2;
-    h -= h % 8;
-    if (st_state[top] == 0) {
-      st_state[top] = 1;
-      st_n[sp] = h; st_state[sp] = 0; ++sp;
-    } else if (st_state[top] == 1) {
-      st_left[top] = ret;
-      st_state[top] = 2;
-      st_n[sp] = m - h; st_state[sp] = 0; ++sp;
-    } else {
-      ret = st_left[top] + ret;
-      --sp;
-    }
+    __syncwarp();
+    if (produced == 0) break;
+    if (lane == 0) S.level_start[L + 2] = end + produced;
+    __syncwarp();
   }
-  return ret;
+  if (lane == 0) S.nlevels = L + 1;
 }
 
 // `get(bin)` returns the bin count as a double (0 = empty); all threads of
@@ -130,15 +128,18 @@ __device__ double block_entropy(Get get, double total, NpScratch &S) {
   }
   __syncthreads();
   S.off[t] = base + incl - cnt;
-  if (t == 0) {
-    S.off[kEntropyThreads] = n_all;
-    if (n_all > 0) np_enumerate_leaves(n_all, S);
-    else S.nleaf = 0;
+  if (t == 0) S.off[kEntropyThreads] = n_all;
+  if (n_all == 0 || !(total > 0.0)) {
+    __syncthreads();
+    return 0.0;
   }
+  if (t < 32) np_build_tree(n_all, S);
   __syncthreads();
-  const int nleaf = S.nleaf;
-  for (int L = t; L < nleaf; L += kEntropyThreads) {
-    const uint32_t beg = S.leaf_beg[L], len = S.leaf_len[L];
+  const int nodes = (int)S.level_start[S.nlevels];
+  // ---- leaves ---------------------------------------------------------------
+  for (int j = t; j < nodes; j += kEntropyThreads) {
+    if (S.node_child[j] != kNpLeaf) continue;
+    const uint32_t beg = S.node_beg[j], len = S.node_len[j];
     int r0 = 0, r1 = kEntropyThreads - 1;  // last thread range with off <= beg
     while (r0 < r1) {
       const int mid = (r0 + r1 + 1) >> 1;
@@ -156,8 +157,6 @@ __device__ double block_entropy(Get get, double total, NpScratch &S) {
       while (!bits) bits = S.occ[++w];
       const int bin = 32 * w + __ffs(bits) - 1;
       bits &= bits - 1;
-      // explicit IEEE ops: no FMA contraction may fuse the product into the
-      // running sum (numpy rounds p*log2(p) before summing)
       const double p = __ddiv_rn(get(bin), total);
       return __dmul_rn(p, log2(p));
     };
@@ -168,21 +167,28 @@ __device__ double block_entropy(Get get, double total, NpScratch &S) {
     } else {
       double r[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = next_term();
+      for (int q = 0; q < 8; ++q) r[q] = next_term();
       uint32_t i = 8;
       for (; i < len - (len % 8); i += 8) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], next_term());
+        for (int q = 0; q < 8; ++q) r[q] = __dadd_rn(r[q], next_term());
       }
-      res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+      res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
       for (; i < len; ++i) res = __dadd_rn(res, next_term());
     }
-    S.leaf_sum[L] = res;
+    S.node_sum[j] = res;
   }
   __syncthreads();
-  if (t == 0) S.result = (total > 0.0 && n_all > 0) ? -np_fold(n_all, S) : 0.0;
-  __syncthreads();
-  const double e = S.result;
+  // ---- internal nodes, deepest level first ----------------------------------
+  for (int L = S.nlevels - 2; L >= 0; --L) {
+    for (int j = (int)S.level_start[L] + t; j < (int)S.level_start[L + 1]; j += kEntropyThreads) {
+      const uint32_t c = S.node_child[j];
+      if (c != kNpLeaf) S.node_sum[j] = __dadd_rn(S.node_sum[c], S.node_sum[c + 1]);
+    }
+    __syncthreads();
+  }
+  const double e = -S.node_sum[0];
   __syncthreads();
   return e;
 }

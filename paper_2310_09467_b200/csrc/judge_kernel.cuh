@@ -472,12 +472,17 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
 
     if (P.direct) {
       // whole stream in this CTA: bucket seams (_kernels.py:125-133) ...
-      if (tid == 0) {
-        int carried = -1;
-        for (int v = 0; v < 256; ++v) {
-          if (s_first[v] < 0) continue;
-          if (carried >= 0) hist_inc_now(cs, ((uint32_t)carried << 8) | (uint32_t)s_first[v]);
-          carried = s_last[v];
+      if (tid < 32) {  // one warp: each non-empty bucket pairs with the previous one
+        int carry = -1;  // last pred of the highest non-empty key below this step
+        for (int b = 0; b < 256; b += 32) {
+          const int v = b + tid;
+          const int f = s_first[v], l = s_last[v];
+          const uint32_t m = __ballot_sync(0xffffffffu, f >= 0);
+          const uint32_t lower = m & ((1u << tid) - 1u);
+          const int from = __shfl_sync(0xffffffffu, l, lower ? 31 - __clz(lower) : 0);
+          const int before = lower ? from : carry;
+          if (f >= 0 && before >= 0) hist_inc_now(cs, ((uint32_t)before << 8) | (uint32_t)f);
+          if (m) carry = __shfl_sync(0xffffffffu, l, 31 - __clz(m));
         }
       }
       __syncthreads();
