@@ -1,12 +1,15 @@
 """Benchmark of the entropy-judgement stage (BASELINE.json metric:
 "entropy-judge GB/s raw uint16 LFM at 1/2/4/8 B200; % HBM peak; CR parity").
 
-Workload (BASELINE.json configs[1]): 100 independent
-synthetic 2048x2048 uint16 bead frames, pitch 15x15, three SNR levels
-(34 high: amp 20000 sigma 0 photon 0.05; 33 mid: amp 3000 sigma 100 photon
-0.05; 33 low: amp 3000 sigma 500 photon 0.01), seeds 0..99, generated
+Default workload (BASELINE.json configs[1]): 100
+independent synthetic 2048x2048 uint16 bead frames, pitch 15x15, three SNR
+levels (34 high: amp 20000 sigma 0 photon 0.05; 33 mid: amp 3000 sigma 100
+photon 0.05; 33 low: amp 3000 sigma 500 photon 0.01), seeds 0..99, generated
 bit-identically to the reference's synth.generate; 13 intra candidates
-(independent frames, temporal off).
+(independent frames, temporal off).  Other configurations for our own
+measurements: --workload c1 (one C1 frame), c3 (smooth-lenslet time series
+with temporal candidates, frames sharded over ranks with a one-frame halo),
+c4 (4096x4096 pitch 13 series).
 
 One step = judge + emission of the whole batch: per-candidate approximate-BWT
 pair histograms, fp64 entropies, argmin, selected big-endian residual streams.
@@ -15,7 +18,7 @@ resident in HBM.  `e2e` = same metric through the public host API with pinned
 host buffers (H2D of frames + D2H of streams and modes inside the timed
 region).  Inputs (839 MB) exceed the 126 MB L2, so no flush is needed.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload c2]
 """
 from __future__ import annotations
 
@@ -28,6 +31,7 @@ import sys
 import threading
 import time
 from concurrent.futures import ProcessPoolExecutor
+from dataclasses import dataclass
 from pathlib import Path
 
 import numpy as np
@@ -35,11 +39,9 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-H = W = 2048
-PITCH = 15
-N_FRAMES = 100
-CODES = list(range(13))
 METRIC = "entropy-judge GB/s raw uint16 LFM at 1/2/4/8 B200; % HBM peak; CR parity"
+INTRA = list(range(13))
+ALL26 = INTRA + [0x80 | i for i in INTRA]
 SNR_LEVELS = [  # (count, amplitude, sigma, photon) -- SURVEY.md §8(d) C2
     (34, 20000.0, 0.0, 0.05),
     (33, 3000.0, 100.0, 0.05),
@@ -47,15 +49,45 @@ SNR_LEVELS = [  # (count, amplitude, sigma, photon) -- SURVEY.md §8(d) C2
 ]
 
 
-def frame_params():
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    description: str
+    frames: int
+    height: int
+    width: int
+    pitch: int
+    codes: tuple
+    temporal: bool
+    series: bool      # True: one series sharded over ranks (strong), False: per-rank batch (weak)
+
+
+WORKLOADS = {
+    "c2": Workload("c2", "C2: 100 independent 2048x2048 uint16 bead frames, pitch 15x15, 3 SNR levels, "
+                   "13 intra candidates, judge + emission", 100, 2048, 2048, 15, tuple(INTRA), False, False),
+    "c1": Workload("c1", "C1: one 2048x2048 bead frame (amp 3000, sigma 20, photon 0.05), pitch 15x15, "
+                   "13 intra candidates, judge + emission", 1, 2048, 2048, 15, tuple(INTRA), False, False),
+    "c3": Workload("c3", "C3 prefix: 100-frame 2048x2048 smooth_lenslet series, pitch 15x15, drift 1, "
+                   "temporal on (26 candidates from frame 1), frames sharded over ranks with a 1-frame halo",
+                   100, 2048, 2048, 15, tuple(ALL26), True, True),
+    "c4": Workload("c4", "C4: 8-frame 4096x4096 smooth_lenslet series, pitch 13x13, drift 1, temporal on "
+                   "(26 candidates), frames sharded over ranks with a 1-frame halo",
+                   8, 4096, 4096, 13, tuple(ALL26), True, True),
+}
+
+
+def c2_params():
     from paper_2310_09467_b200.lfm_synth import SynthParams
     out, seed = [], 0
     for count, amp, sigma, photon in SNR_LEVELS:
         for _ in range(count):
-            out.append(SynthParams(W, H, PITCH, PITCH, mode="beads", signal_amplitude=amp,
+            out.append(SynthParams(2048, 2048, 15, 15, mode="beads", signal_amplitude=amp,
                                    noise_sigma=sigma, photon_scale=photon, frames=1, seed=seed))
             seed += 1
     return out
+
+
+frame_params = c2_params  # used by tools/
 
 
 def _gen_one(p):
@@ -63,20 +95,52 @@ def _gen_one(p):
     return generate_array(p)[0]
 
 
-def make_frames(n: int, workers: int) -> np.ndarray:
-    params = frame_params()[:n]
-    vol = np.empty((n, H, W), np.uint16)
-    with ProcessPoolExecutor(max(1, workers)) as ex:
-        for i, fr in enumerate(ex.map(_gen_one, params, chunksize=2)):
+_SERIES = {}
+
+
+def _gen_series_frame(t):
+    from paper_2310_09467_b200.lfm_synth import noisy_frame
+    base, p = _SERIES["base"], _SERIES["params"]
+    return noisy_frame(base, p, t)
+
+
+def series_params(wl: Workload):
+    from paper_2310_09467_b200.lfm_synth import SynthParams
+    return SynthParams(wl.width, wl.height, wl.pitch, wl.pitch, mode="smooth_lenslet",
+                       signal_amplitude=20000.0, noise_sigma=20.0, photon_scale=0.05,
+                       frames=wl.frames, drift=1.0, seed=0)
+
+
+def make_frames(wl: Workload, index: range, workers: int) -> np.ndarray:
+    """Frames `index` of the workload (C2: per-frame seeds; series: one scene)."""
+    vol = np.empty((len(index), wl.height, wl.width), np.uint16)
+    if wl.name == "c1":
+        from paper_2310_09467_b200.lfm_synth import SynthParams, generate_array
+        vol[0] = generate_array(SynthParams(2048, 2048, 15, 15, mode="beads", signal_amplitude=3000.0,
+                                            noise_sigma=20.0, photon_scale=0.05, seed=0))[0]
+        return vol
+    if not wl.series:
+        params = [c2_params()[i] for i in index]
+        with ProcessPoolExecutor(max(1, workers)) as ex:
+            for i, fr in enumerate(ex.map(_gen_one, params, chunksize=2)):
+                vol[i] = fr
+        return vol
+    from paper_2310_09467_b200.lfm_synth import scene
+    p = series_params(wl)
+    _SERIES["base"], _SERIES["params"] = scene(p), p   # inherited by forked workers
+    import multiprocessing as mpm
+    with ProcessPoolExecutor(max(1, workers), mp_context=mpm.get_context("fork")) as ex:
+        for i, fr in enumerate(ex.map(_gen_series_frame, list(index), chunksize=2)):
             vol[i] = fr
     return vol
 
 
-def config(extra=None):
-    c = {"workload": "C2: 100 independent 2048x2048 uint16 bead frames, pitch 15x15, 3 SNR levels, "
-                     "13 intra candidates, judge + emission",
-         "frames_per_gpu": N_FRAMES, "height": H, "width": W, "pitch": [PITCH, PITCH],
-         "candidates": len(CODES), "l2_policy": "inputs (839 MB/GPU) larger than L2 (126 MB), no flush"}
+def config(wl: Workload, extra=None):
+    nbytes = wl.frames * 2 * wl.height * wl.width
+    c = {"workload": wl.description, "frames": wl.frames, "height": wl.height, "width": wl.width,
+         "pitch": [wl.pitch, wl.pitch], "candidates": len(wl.codes), "temporal": wl.temporal,
+         "l2_policy": (f"inputs ({nbytes / 1e6:.0f} MB/GPU) larger than L2 (126 MB), no flush"
+                       if nbytes > 126e6 else "input smaller than L2: L2 flushed (256 MB write) before every step")}
     if extra:
         c.update(extra)
     return c
@@ -98,7 +162,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except OSError:
@@ -134,47 +198,57 @@ def measured_peak_hbm():
     return 6650.0, "fallback"
 
 
-def cpu_reference_sample(vol: np.ndarray, nthreads: int):
-    """Time the CPU port of the reference path (oracle, C, pthreads) on a
-    bounded sample; returns (GB/s raw, seconds, frames)."""
+def profile_json(name):
+    p = ROOT / "profiles" / name
+    return json.loads(p.read_text()) if p.exists() else None
+
+
+def cpu_reference_sample(wl: Workload, vol: np.ndarray, nthreads: int):
+    """Time the CPU port of the reference path (oracle: C restatement, pthreads
+    over (frame, candidate) like the reference's ThreadPool) on `vol`;
+    returns (GB/s raw, seconds, frames)."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle
-    oracle.select_batch(vol[:1, :64, :64], None, CODES, PITCH, PITCH, nthreads=1)   # load/warm
+    oracle.select_batch(vol[:1, :64, :64], None, INTRA, wl.pitch, wl.pitch, nthreads=1)   # load/warm
+    prevs = None
+    codes = list(wl.codes)
+    if wl.temporal:
+        prevs = np.concatenate([vol[:1], vol[:-1]])   # frame 0 scored against itself (timing only)
     t0 = time.perf_counter()
-    oracle.select_batch(vol, None, CODES, PITCH, PITCH, nthreads=nthreads)
+    oracle.select_batch(vol, prevs, codes, wl.pitch, wl.pitch, nthreads=nthreads)
     dt = time.perf_counter() - t0
-    return vol.shape[0] * 2 * H * W / dt / 1e9, dt, vol.shape[0]
+    return vol.shape[0] * 2 * wl.height * wl.width / dt / 1e9, dt, vol.shape[0]
 
 
-def run_reference(args):
+def run_reference(args, wl: Workload):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
-    sample_frames = int(os.environ.get("PCBZ_REF_SAMPLE_FRAMES", "16"))
-    vol = make_frames(sample_frames, cores)
+    nf = min(wl.frames, int(os.environ.get("PCBZ_REF_SAMPLE_FRAMES", str(wl.frames))))
+    vol = make_frames(wl, range(nf), cores)
     for _ in range(args.warmup):
-        cpu_reference_sample(vol[:max(1, sample_frames // 4)], cores)
+        cpu_reference_sample(wl, vol[:max(1, nf // 4)], cores)
     times = []
     for _ in range(args.steps):
-        _, dt, _ = cpu_reference_sample(vol, cores)
+        _, dt, _ = cpu_reference_sample(wl, vol, cores)
         times.append(dt)
     t = statistics.mean(times)
-    v = sample_frames * 2 * H * W / t / 1e9
-    sample = f"{sample_frames} of the 100 C2 frames per step, judge (13 candidates) + emission"
+    v = nf * 2 * wl.height * wl.width / t / 1e9
+    sample = (f"{nf} of the {wl.frames} workload frames per step, judge ({len(wl.codes)} candidates) "
+              f"+ emission, C port of the reference path on {cores} threads")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
-        "config": config({"sample_frames_per_step": sample_frames}),
-        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+        "scaling": "strong" if wl.series else "weak", "vs_baseline": None, "dtype": "u16",
+        "data": "synthetic", "config": config(wl, {"sample_frames_per_step": nf}),
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
     return 0
 
 
-def run_gpu(args):
+def run_gpu(args, wl: Workload):
     import torch
     import torch.distributed as dist
 
@@ -188,14 +262,29 @@ def run_gpu(args):
 
     from paper_2310_09467_b200 import LensletGeometry, pipeline
     from paper_2310_09467_b200.device import DeviceJudge, collect_timing, set_profiling
+    from paper_2310_09467_b200.shard import plan_frame_shards
 
     cores = os.cpu_count() or 1
-    host = make_frames(N_FRAMES, max(1, cores // world))
-    pinned = torch.empty((N_FRAMES, H, W), dtype=torch.uint16).pin_memory()
+    H, W = wl.height, wl.width
+    if wl.series:   # strong scaling: this rank's shard of the series (+ halo frame)
+        shard = plan_frame_shards(wl.frames, world, wl.temporal)[rank]
+        first = shard.halo if shard.halo is not None else shard.begin
+        host_all = make_frames(wl, range(first, shard.end), max(1, cores // world))
+        host = host_all[shard.begin - first:]
+        halo_np = host_all[0] if shard.halo is not None else None
+    else:           # weak scaling: every rank judges its own full batch
+        host = make_frames(wl, range(wl.frames), max(1, cores // world))
+        halo_np = None
+    nloc = host.shape[0]
+    pinned = torch.empty((nloc, H, W), dtype=torch.uint16).pin_memory()
     pinned.numpy()[...] = host
     frames = pinned.to(dev)
-    judge = DeviceJudge((N_FRAMES, H, W), (PITCH, PITCH), CODES, temporal=False, device=dev)
+    halo = torch.from_numpy(halo_np).to(dev) if halo_np is not None else None
+    judge = DeviceJudge((nloc, H, W), (wl.pitch, wl.pitch), wl.codes, temporal=wl.temporal, device=dev)
     stream = torch.cuda.current_stream(dev)
+    raw_bytes_local = nloc * 2 * H * W
+    small = raw_bytes_local <= 126e6
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if small else None
 
     def barrier():
         if world > 1:
@@ -209,44 +298,67 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
     # ---- device-resident timed region ----------------------------------------
     for _ in range(args.warmup):
-        judge(frames)
+        judge(frames, halo)
     barrier()
     set_profiling(True)
     collect_timing()
+    step_ms = []
     with ClockSampler(local) as clk:
         barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            judge(frames)
-        e1.record(stream)
+        if small:   # inputs fit in L2: flush it between steps (outside the timed events)
+            for _ in range(args.steps):
+                flush_buf.fill_(1)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                judge(frames, halo)
+                e1.record(stream)
+                e1.synchronize()
+                step_ms.append(e0.elapsed_time(e1))
+            ms_local = sum(step_ms) / len(step_ms)
+        else:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                judge(frames, halo)
+            e1.record(stream)
+            barrier()
+            ms_local = e0.elapsed_time(e1) / args.steps
         barrier()
     set_profiling(False)
-    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    ms = max_over_ranks(ms_local)
     hist_ms_sum, judge_ms_sum, launches = collect_timing()
     hist_ms = max_over_ranks(hist_ms_sum / args.steps)
-    raw_bytes = N_FRAMES * 2 * H * W
-    value = world * raw_bytes / (ms * 1e-3) / 1e9
+    raw_bytes = sum_over_ranks(raw_bytes_local)
+    value = raw_bytes / (ms * 1e-3) / 1e9
 
     # ---- end to end through the public host API (pinned buffers) -------------
-    geo = LensletGeometry(PITCH, PITCH)
+    geo = LensletGeometry(wl.pitch, wl.pitch)
     vol_np = pinned.numpy()
-    ent_h = torch.empty((N_FRAMES, len(CODES)), dtype=torch.float64).pin_memory().numpy()
-    sel_h = torch.empty(N_FRAMES, dtype=torch.uint8).pin_memory().numpy()
-    stream_h = torch.empty((N_FRAMES, 2 * H * W), dtype=torch.uint8).pin_memory().numpy()
+    codes = list(wl.codes)
+    ent_h = torch.empty((nloc, len(codes)), dtype=torch.float64).pin_memory().numpy()
+    sel_h = torch.empty(nloc, dtype=torch.uint8).pin_memory().numpy()
+    stream_h = torch.empty((nloc, 2 * H * W), dtype=torch.uint8).pin_memory().numpy()
     out = (ent_h, sel_h, stream_h)
-    pipeline.judge_volume(vol_np, geo, CODES, False, out=out)
+    pipeline.judge_volume(vol_np, geo, codes, wl.temporal, halo=halo_np, out=out)
     e2e_steps = max(1, min(args.steps, 5))
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        pipeline.judge_volume(vol_np, geo, CODES, False, out=out)
-    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
-    e2e_value = world * raw_bytes / e2e_s / 1e9
-    # parity spot check of the e2e output against the device-resident run
+    with ClockSampler(local) as clk_e2e:
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            pipeline.judge_volume(vol_np, geo, codes, wl.temporal, halo=halo_np, out=out)
+        e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
+    e2e_value = raw_bytes / e2e_s / 1e9
     if not np.array_equal(sel_h, judge.sel.cpu().numpy()):
         raise RuntimeError("e2e and device-resident selections differ")
 
@@ -256,35 +368,46 @@ def run_gpu(args):
         return 0
 
     peak, peak_kind = measured_peak_hbm()
-    alg_bytes_hist = raw_bytes            # the histogram kernel reads every frame once
+    alg_bytes_hist = raw_bytes_local * (2 if wl.temporal else 1)  # frames (+ previous frames) read once
     achieved = alg_bytes_hist / (hist_ms * 1e-3) / 1e9
-    stage_bytes = 2 * raw_bytes           # stage: read frames + write streams
     traffic = None
-    tf = ROOT / "profiles" / "latest_hist_traffic.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+    tf = profile_json("latest_hist_traffic.json")
+    if tf and tf.get("workload", "").startswith("bench.py C2") and wl.name == "c2":
+        traffic = tf.get("bytes_per_launch")
+    events = sum((len(codes) if (f > 0 or halo_np is not None or not wl.temporal) else 13)
+                 for f in range(nloc)) * (2 * H * W)
+    ev_rate = events / (hist_ms * 1e-3)
+    roof = profile_json("smem_roof.json")
     res = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if wl.series else "weak",
         "vs_baseline": None, "dtype": "u16", "data": "synthetic (reference synth.generate, bit-identical)",
-        "config": config({"parallelism": f"frames x{world} (replicas, no collective)" if world > 1 else "single GPU"}),
+        "config": config(wl, {"parallelism": (f"frame shards x{world} (1-frame halo, no collective)" if wl.series
+                                              else f"replicas x{world} (no collective)") if world > 1 else "single GPU"}),
         "roofline": {"bound": "hbm", "kernel": "judge_hist_kernel", "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                     "peak_kind": peak_kind, "hist_kernel_ms": hist_ms,
-                     "algorithmic_bytes_per_launch": alg_bytes_hist,
-                     "stage_frac": (stage_bytes / (ms * 1e-3) / 1e9) / peak,
-                     "events_per_s": N_FRAMES * len(CODES) * (2 * H * W) / (hist_ms * 1e-3)},
-        "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": raw_bytes,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "hist_kernel_ms": hist_ms, "algorithmic_bytes_per_launch": alg_bytes_hist,
+                     "stage_frac": (raw_bytes_local * (3 if wl.temporal else 2) / (ms * 1e-3) / 1e9) / peak},
+        "secondary_roofline": {
+            "bound": "shared-memory atomics (one per stream byte per candidate)",
+            "achieved": ev_rate, "unit": "pair increments/s",
+            "peak": roof["atoms_random_lane_ops_per_s"] if roof else None,
+            "frac": ev_rate / roof["atoms_random_lane_ops_per_s"] if roof else None,
+            "peak_source": "profiles/smem_roof.json (microbenchmark, random 32-bit words)" if roof else None},
+        "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": raw_bytes_local,
                 "d2h_bytes_per_step": stream_h.nbytes + ent_h.nbytes + sel_h.nbytes,
-                "api": "paper_2310_09467_b200.pipeline.judge_volume (pcbz_judge_host)"},
+                "api": "paper_2310_09467_b200.pipeline.judge_volume (pcbz_judge_host)",
+                "clocks": clk_e2e.summary()},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline:
-        sample = int(os.environ.get("PCBZ_CPU_SAMPLE_FRAMES", "16"))
-        v, dt, nf = cpu_reference_sample(host[:sample], cores)
+        nf = min(nloc, int(os.environ.get("PCBZ_CPU_SAMPLE_FRAMES", "100")))
+        v, dt, nfr = cpu_reference_sample(wl, host[:nf], cores)
         res["cpu_baseline"] = {"value": v, "unit": "GB/s", "cores": cores, "kind": "port",
-                               "sample": f"{nf} C2 frames, judge (13 candidates) + emission, {dt:.2f} s wall"}
+                               "sample": f"{nfr} frames of the workload, judge ({len(codes)} candidates) + "
+                                         f"emission, C port of the reference path, {dt:.2f} s wall"}
     print(json.dumps(res), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -297,11 +420,13 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
     if args.impl == "reference":
-        return run_reference(args)
-    return run_gpu(args)
+        return run_reference(args, wl)
+    return run_gpu(args, wl)
 
 
 if __name__ == "__main__":

@@ -19,7 +19,7 @@ from paper_2310_09467_b200.device import DeviceJudge, collect_timing, set_profil
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 52
 params = bench.frame_params()
 pick = [params[i] for i in np.linspace(0, len(params) - 1, n).astype(int)]
-vol = bench.make_frames(0, 1)  # warm the process pool path (no frames)
+
 from concurrent.futures import ProcessPoolExecutor  # noqa: E402
 with ProcessPoolExecutor(os.cpu_count() or 1) as ex:
     vol = np.stack(list(ex.map(bench._gen_one, pick)))
