@@ -304,7 +304,7 @@ int pcbz_last_timing(float *hist_ms, float *total_ms, int *launches) {
 
 size_t pcbz_judge_workspace_size(int64_t nframes, int64_t h, int64_t w, int k, int want_hist) {
   std::vector<uint8_t> specs(std::max(k, 1));
-  for (int i = 0; i < k; ++i) specs[i] = (uint8_t)i;  // shape-only plan
+  for (int i = 0; i < k; ++i) specs[i] = (uint8_t)(i < 13 ? i : (0x80 | (i - 13)));  // shape-only plan
   Plan pl;
   if (make_plan(nframes, h, w, 1, 1, specs.data(), k, true, 1, want_hist != 0, pl)) return 0;
   return pl.ws_bytes;

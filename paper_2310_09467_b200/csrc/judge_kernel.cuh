@@ -62,17 +62,18 @@ __device__ __forceinline__ PairRef pair_ref(const JudgeParams &P, int64_t pair) 
 // ---------------------------------------------------------------------------
 //
 // Bin b = last * 256 + pred (pair (last, pred), first byte high) lives in the
-// (pred & 1) half of word
-//     word(b) = last << 7 | ((13 * last) & 127) ^ (pred >> 1),
-// a bijection within each 128-word row.  A plain last * 128 + (pred >> 1)
-// puts the bank (word % 32) entirely in bits 1..5 of pred, which are skewed
-// for real residual streams (many lanes of a warp then hit the same banks);
-// mixing in 13 * last cuts the measured average conflict degree of the
-// histogram atomics from ~5.6 to ~4 (tools/sim_conflicts.py).  The last-pred
-// tables store the code lt_code(pred) = pred << 7 | (13 * pred & 127), so
-// word = code ^ (pred >> 1) costs the hot loop nothing extra; kUnseenCode
-// marks a key not seen yet in a run and maps first occurrences to the dummy
-// row 0x8000 ^ (pred >> 1) past the histogram.
+// (pred >> 7) half of word
+//     word(b) = last << 7 | ((13 * last) & 127) ^ (pred & 127),
+// a bijection within each 128-word row.  A plain last * 128 + (pred & 127)
+// puts the bank (word % 32) entirely in the low bits of pred, which are
+// skewed for real residual streams (many lanes of a warp then hit the same
+// banks); mixing in 13 * last cuts the measured average conflict degree of
+// the histogram atomics from ~5.6 to ~4 (tools/sim_conflicts.py).  The
+// last-pred tables store the code lt_code(pred) = pred << 7 | (13 * pred &
+// 127), so the hot loop forms the word with one 3-input LOP3,
+// code ^ (pred & 127), and the increment as 1 + (pred >> 7) * 0xFFFF.
+// kUnseenCode marks a key not seen yet in a run and maps first occurrences
+// to the dummy row 0x8000 ^ (pred & 127) past the histogram.
 constexpr uint32_t kUnseenCode = 0x8000;
 #ifndef PCBZ_SWIZZLE
 #define PCBZ_SWIZZLE 1
@@ -83,17 +84,20 @@ __device__ __forceinline__ uint32_t lt_code(uint32_t pred) {
   return (pred << 7) | ((pred * kSwizzleMul) & 127u);
 }
 __device__ __forceinline__ uint32_t hist_word(uint32_t code, uint32_t pred) {
-  return code ^ (pred >> 1);
+  return code ^ (pred & 127u);
 }
+__device__ __forceinline__ uint32_t pred_half(uint32_t pred) { return (pred >> 7) & 1u; }
+__device__ __forceinline__ uint32_t pred_inc(uint32_t pred) { return 1u + (pred >> 7) * 0xFFFFu; }
 __device__ __forceinline__ uint32_t word_of_bin(uint32_t bin) {
   return hist_word(lt_code(bin >> 8), bin & 0xFFu);
 }
+__device__ __forceinline__ uint32_t bin_half(uint32_t bin) { return pred_half(bin & 0xFFu); }
 __device__ __forceinline__ uint32_t bin_of_word(uint32_t word, uint32_t half) {
   const uint32_t last = word >> 7;
-  return (last << 8) | ((((word & 127u) ^ ((last * kSwizzleMul) & 127u)) << 1) | half);
+  return (last << 8) | (half << 7) | ((word & 127u) ^ ((last * kSwizzleMul) & 127u));
 }
 __device__ __forceinline__ uint32_t bin_count16(const uint32_t *hist, uint32_t bin) {
-  return (hist[word_of_bin(bin)] >> ((bin & 1u) << 4)) & 0xFFFFu;
+  return (hist[word_of_bin(bin)] >> (bin_half(bin) << 4)) & 0xFFFFu;
 }
 
 // ---------------------------------------------------------------------------
@@ -129,7 +133,7 @@ __device__ __forceinline__ uint32_t chain_event(const ChainState &cs, uint32_t k
     return ~0u;
   }
   const uint32_t bin = ((code >> 7) << 8) | pred;
-  const uint32_t inc = 1u << ((pred & 1u) << 4);
+  const uint32_t inc = pred_inc(pred);
   const uint32_t old = atomicAdd(&cs.hist[hist_word(code, pred)], inc);
   flag |= old ^ (old + inc);
   return bin;
@@ -139,7 +143,7 @@ __device__ __forceinline__ uint32_t chain_event(const ChainState &cs, uint32_t k
 // exactly one claimant per crossing; counts are never lost or doubled.
 __device__ __forceinline__ void claim_spill(const ChainState &cs, uint32_t bin) {
   if (bin == ~0u) return;
-  const uint32_t m = 0x8000u << ((bin & 1u) << 4);
+  const uint32_t m = 0x8000u << (bin_half(bin) << 4);
   const uint32_t old = atomicAnd(&cs.hist[word_of_bin(bin)], ~m);
   if (old & m) {
     const int i = atomicAdd(cs.nspill, 1);
@@ -150,7 +154,7 @@ __device__ __forceinline__ void claim_spill(const ChainState &cs, uint32_t bin) 
 
 // increment outside the hot loop (stitching): claim immediately
 __device__ __forceinline__ void hist_inc_now(const ChainState &cs, uint32_t bin) {
-  const uint32_t inc = 1u << ((bin & 1u) << 4);
+  const uint32_t inc = pred_inc(bin & 0xFFu);
   const uint32_t old = atomicAdd(&cs.hist[word_of_bin(bin)], inc);
   if ((old ^ (old + inc)) & 0x80008000u) claim_spill(cs, bin);
 }

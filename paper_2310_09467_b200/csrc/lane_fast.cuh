@@ -167,7 +167,7 @@ __device__ __forceinline__ void chunk_events(const ChainState &cs, const uint32_
   for (int e = 0; e < 16; ++e) {
     fresh |= last[e];
     pd.word[e] = hist_word(last[e], prd[e]);  // bin = last * 256 + pred, 2 bins/word
-    pd.old[e] = atoms_add(cs.hbase + 4u * pd.word[e], 1u + (prd[e] & 1u) * 0xFFFFu);
+    pd.old[e] = atoms_add(cs.hbase + 4u * pd.word[e], pred_inc(prd[e]));
   }
   if constexpr (!PCBZ_DEFER) {  // examine this chunk's returned words right away
     settle_pending(cs, pd);
