@@ -83,18 +83,29 @@ constexpr uint32_t kSwizzleMul = PCBZ_SWIZZLE ? 13u : 0u;
 __device__ __forceinline__ uint32_t lt_code(uint32_t pred) {
   return (pred << 7) | ((pred * kSwizzleMul) & 127u);
 }
-__device__ __forceinline__ uint32_t hist_word(uint32_t code, uint32_t pred) {
-  return code ^ (pred & 127u);
+// PCBZ_HALF_MSB selects which bit of pred picks the 16-bit half of a word:
+// 1 -> pred >> 7 (column pred & 127), 0 -> pred & 1 (column pred >> 1).
+#ifndef PCBZ_HALF_MSB
+#define PCBZ_HALF_MSB 0
+#endif
+__device__ __forceinline__ uint32_t pred_col(uint32_t pred) {
+  return PCBZ_HALF_MSB ? (pred & 127u) : (pred >> 1);
 }
-__device__ __forceinline__ uint32_t pred_half(uint32_t pred) { return (pred >> 7) & 1u; }
-__device__ __forceinline__ uint32_t pred_inc(uint32_t pred) { return 1u + (pred >> 7) * 0xFFFFu; }
+__device__ __forceinline__ uint32_t hist_word(uint32_t code, uint32_t pred) {
+  return code ^ pred_col(pred);
+}
+__device__ __forceinline__ uint32_t pred_half(uint32_t pred) {
+  return PCBZ_HALF_MSB ? ((pred >> 7) & 1u) : (pred & 1u);
+}
+__device__ __forceinline__ uint32_t pred_inc(uint32_t pred) { return 1u + pred_half(pred) * 0xFFFFu; }
 __device__ __forceinline__ uint32_t word_of_bin(uint32_t bin) {
   return hist_word(lt_code(bin >> 8), bin & 0xFFu);
 }
 __device__ __forceinline__ uint32_t bin_half(uint32_t bin) { return pred_half(bin & 0xFFu); }
 __device__ __forceinline__ uint32_t bin_of_word(uint32_t word, uint32_t half) {
   const uint32_t last = word >> 7;
-  return (last << 8) | (half << 7) | ((word & 127u) ^ ((last * kSwizzleMul) & 127u));
+  const uint32_t col = (word & 127u) ^ ((last * kSwizzleMul) & 127u);
+  return (last << 8) | (PCBZ_HALF_MSB ? ((half << 7) | col) : ((col << 1) | half));
 }
 __device__ __forceinline__ uint32_t bin_count16(const uint32_t *hist, uint32_t bin) {
   return (hist[word_of_bin(bin)] >> (bin_half(bin) << 4)) & 0xFFFFu;

@@ -8,12 +8,9 @@ sys.path.insert(0, str(ROOT))
 from paper_2310_09467_b200 import build_native  # noqa: E402
 
 VARIANTS = {
-    "s0p0d0": ("PCBZ_SWIZZLE=0", "PCBZ_PIPELINE=0", "PCBZ_DEFER=0"),
-    "s0p0d1": ("PCBZ_SWIZZLE=0", "PCBZ_PIPELINE=0", "PCBZ_DEFER=1"),
-    "s1p0d1": ("PCBZ_SWIZZLE=1", "PCBZ_PIPELINE=0", "PCBZ_DEFER=1"),
-    "s1p1d1": ("PCBZ_SWIZZLE=1", "PCBZ_PIPELINE=1", "PCBZ_DEFER=1"),
-    "s0p1d1": ("PCBZ_SWIZZLE=0", "PCBZ_PIPELINE=1", "PCBZ_DEFER=1"),
-    "s1p0d0": ("PCBZ_SWIZZLE=1", "PCBZ_PIPELINE=0", "PCBZ_DEFER=0"),
+    "half_lsb": ("PCBZ_HALF_MSB=0",),
+    "half_msb": ("PCBZ_HALF_MSB=1",),
+    "half_lsb_noswz": ("PCBZ_HALF_MSB=0", "PCBZ_SWIZZLE=0"),
 }
 
 if __name__ == "__main__":
