@@ -123,14 +123,27 @@ int validate_specs(const uint8_t *specs, int k) {
 // Work decomposition: segments per pair so that the persistent grid sees
 // about two waves of items, while no segment exceeds kMaxSegPixels.
 int choose_segments(int64_t npairs, int64_t npix, bool want_hist) {
-  const int64_t nsm = num_sms_cached();
-  int64_t s = (2 * nsm + npairs - 1) / npairs;
-  const int64_t max_by_len = std::max<int64_t>(1, npix / (64 * kJudgeThreads));
-  s = std::min(s, max_by_len);
-  s = std::max<int64_t>(s, (npix + kMaxSegPixels - 1) / kMaxSegPixels);
-  if (s > 4096) s = 4096;
   (void)want_hist;
-  return (int)std::max<int64_t>(1, s);
+  const int64_t nsm = num_sms_cached();
+  const int64_t s_min = std::max<int64_t>(1, (npix + kMaxSegPixels - 1) / kMaxSegPixels);
+  const int64_t s_max = std::max<int64_t>(s_min, std::min<int64_t>(4096, npix / (64 * kJudgeThreads)));
+  // Items are pulled dynamically by one CTA per SM; pick the segment count
+  // whose item count fills the last wave best (ties -> fewer segments, i.e.
+  // less stitching and no global flush), considering only splits that give
+  // each segment >= 64 pixels per lane.
+  int64_t best = s_min;
+  double best_eff = -1.0;
+  for (int64_t s = s_min; s <= std::min(s_max, s_min + 2 * nsm); ++s) {
+    const int64_t items = npairs * s;
+    const int64_t waves = (items + nsm - 1) / nsm;
+    const double eff = (double)items / (double)(waves * nsm);
+    if (eff > best_eff + 0.01) {
+      best_eff = eff;
+      best = s;
+    }
+    if (items >= 8 * nsm && eff > 0.95) break;
+  }
+  return (int)best;
 }
 
 struct Plan {

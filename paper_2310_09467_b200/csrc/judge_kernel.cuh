@@ -86,7 +86,7 @@ __device__ __forceinline__ uint32_t lt_code(uint32_t pred) {
 // PCBZ_HALF_MSB selects which bit of pred picks the 16-bit half of a word:
 // 1 -> pred >> 7 (column pred & 127), 0 -> pred & 1 (column pred >> 1).
 #ifndef PCBZ_HALF_MSB
-#define PCBZ_HALF_MSB 0
+#define PCBZ_HALF_MSB 1  // A/B on 100 C2 frames: 0.1948 vs 0.1964 ms/frame (profiles/r01_notes.md)
 #endif
 __device__ __forceinline__ uint32_t pred_col(uint32_t pred) {
   return PCBZ_HALF_MSB ? (pred & 127u) : (pred >> 1);
