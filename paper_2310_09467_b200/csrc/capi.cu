@@ -91,6 +91,7 @@ struct DevBuf {
 
 struct HostCtx {
   cudaStream_t stream = nullptr;
+  cudaStream_t s_in = nullptr, s_out = nullptr;  // pcbz_judge_host copy streams
   DevBuf frames, prev, out, ent, sel, stream_out, hist, ws, scratch, bytes;
   int init() {
     if (stream) return PCBZ_OK;
@@ -218,7 +219,8 @@ int make_plan(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py, con
 
 // Enqueue the whole judge (+ optional emission) on `st`.
 int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double *d_ent,
-             uint8_t *d_sel, uint8_t *d_stream, uint32_t *d_hist, void *d_ws, cudaStream_t st) {
+             uint8_t *d_sel, uint8_t *d_stream, uint32_t *d_hist, void *d_ws, cudaStream_t st,
+             int *d_err_shared = nullptr) {
   JudgeParams &jp = pl.jp;
   char *ws = static_cast<char *>(d_ws);
   jp.frames = d_frames;
@@ -227,7 +229,8 @@ int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double 
     jp.fast_px = 0;  // 128-bit loads need 16-byte aligned frames
   jp.ent = d_ent;
   jp.counter = reinterpret_cast<int *>(ws + pl.off_counter);
-  jp.err = reinterpret_cast<int *>(ws + pl.off_err);
+  // a caller running several plans can collect all error flags in one word
+  jp.err = d_err_shared ? d_err_shared : reinterpret_cast<int *>(ws + pl.off_err);
   jp.fscratch = reinterpret_cast<uint8_t *>(ws + pl.off_fscratch);
   if (!jp.direct) {
     jp.segsum = reinterpret_cast<int16_t *>(ws + pl.off_segsum);
@@ -340,32 +343,91 @@ int pcbz_judge_device(const uint16_t *d_frames, const uint16_t *d_halo_prev, int
                   d_workspace, static_cast<cudaStream_t>(stream));
 }
 
+// Frames per pipeline chunk of pcbz_judge_host: uploads of chunk i+1,
+// the judge of chunk i and downloads of chunk i-1 overlap on three streams.
+int64_t host_chunk_frames(int64_t nframes) {
+  static const int64_t forced = [] {
+    const char *e = getenv("PCBZ_HOST_CHUNK");
+    return (int64_t)(e ? atoll(e) : 0);
+  }();
+  if (forced > 0) return std::min(forced, nframes);
+  if (nframes < 8) return nframes;  // too few frames to pay for a pipeline
+  return (nframes + 5) / 6;         // ~6 chunks: short fill/drain, large launches
+}
+
 int pcbz_judge_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t nframes, int64_t h,
                     int64_t w, int64_t px, int64_t py, const uint8_t *specs, int k, int temporal,
                     double *ent_out, uint8_t *sel_out, uint8_t *stream_out) {
   HostCtx &c = g_ctx;
   int rc = c.init();
   if (rc) return rc;
-  Plan pl;
-  rc = make_plan(nframes, h, w, px, py, specs, k, halo_prev != nullptr, temporal, false, pl);
+  Plan full;  // validates the whole call up front
+  rc = make_plan(nframes, h, w, px, py, specs, k, halo_prev != nullptr, temporal, false, full);
   if (rc) return rc;
-  const size_t fbytes = (size_t)nframes * h * w * 2;
+  const int64_t npix = h * w;
+  const size_t fbytes = (size_t)nframes * npix * 2;
+  const int64_t chunk = host_chunk_frames(nframes);
+  const int64_t nchunks = (nframes + chunk - 1) / chunk;
+  // workspace for the largest chunk plan (all chunks run on one stream)
+  size_t ws_bytes = 0;
+  for (int64_t a = 0; a < nframes; a += chunk) {
+    Plan pl;
+    rc = make_plan(std::min(chunk, nframes - a), h, w, px, py, specs, k,
+                   a > 0 ? temporal != 0 : halo_prev != nullptr, temporal, false, pl);
+    if (rc) return rc;
+    ws_bytes = std::max(ws_bytes, pl.ws_bytes);
+  }
   if ((rc = c.frames.ensure(fbytes)) || (rc = c.ent.ensure((size_t)nframes * k * 8)) ||
-      (rc = c.sel.ensure((size_t)nframes)) || (rc = c.ws.ensure(pl.ws_bytes)))
+      (rc = c.sel.ensure((size_t)nframes)) || (rc = c.ws.ensure(ws_bytes + 256)))
     return rc;
-  if (halo_prev && (rc = c.prev.ensure((size_t)h * w * 2))) return rc;
+  if (halo_prev && (rc = c.prev.ensure((size_t)npix * 2))) return rc;
   if (stream_out && (rc = c.stream_out.ensure(fbytes))) return rc;
+  if (!c.s_in) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&c.s_in, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c.s_out, cudaStreamNonBlocking));
+  }
   cudaStream_t st = c.stream;
-  CUDA_TRY(cudaMemcpyAsync(c.frames.p, frames, fbytes, cudaMemcpyHostToDevice, st));
-  if (halo_prev) CUDA_TRY(cudaMemcpyAsync(c.prev.p, halo_prev, (size_t)h * w * 2, cudaMemcpyHostToDevice, st));
-  rc = run_plan(pl, c.frames.as<uint16_t>(), halo_prev ? c.prev.as<uint16_t>() : nullptr,
-                c.ent.as<double>(), c.sel.as<uint8_t>(), stream_out ? c.stream_out.as<uint8_t>() : nullptr,
-                nullptr, c.ws.p, st);
-  if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(ent_out, c.ent.p, (size_t)nframes * k * 8, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(sel_out, c.sel.p, (size_t)nframes, cudaMemcpyDeviceToHost, st));
-  if (stream_out) CUDA_TRY(cudaMemcpyAsync(stream_out, c.stream_out.p, fbytes, cudaMemcpyDeviceToHost, st));
-  return check_err_flag(pl, c.ws.p, st);
+  int *d_err = reinterpret_cast<int *>(c.ws.as<char>() + ws_bytes);  // shared by all chunks
+  char *ws = c.ws.as<char>();
+  CUDA_TRY(cudaMemsetAsync(d_err, 0, 4, st));
+  std::vector<cudaEvent_t> ev(2 * nchunks);
+  for (auto &e : ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (halo_prev)
+    CUDA_TRY(cudaMemcpyAsync(c.prev.p, halo_prev, (size_t)npix * 2, cudaMemcpyHostToDevice, c.s_in));
+  const uint16_t *d_frames = c.frames.as<uint16_t>();
+  for (int64_t i = 0; i < nchunks; ++i) {
+    const int64_t a = i * chunk, n = std::min(chunk, nframes - a);
+    const size_t off = (size_t)a * npix;
+    CUDA_TRY(cudaMemcpyAsync(c.frames.as<uint16_t>() + off, frames + off, (size_t)n * npix * 2,
+                             cudaMemcpyHostToDevice, c.s_in));
+    CUDA_TRY(cudaEventRecord(ev[2 * i], c.s_in));
+    CUDA_TRY(cudaStreamWaitEvent(st, ev[2 * i], 0));
+    // the previous frame of chunk i's first frame: the halo (chunk 0) or frame a-1
+    const uint16_t *d_halo = a > 0 ? (temporal ? d_frames + off - npix : nullptr)
+                                   : (halo_prev ? c.prev.as<uint16_t>() : nullptr);
+    Plan pl;
+    rc = make_plan(n, h, w, px, py, specs, k, d_halo != nullptr, temporal, false, pl);
+    if (rc) return rc;
+    rc = run_plan(pl, d_frames + off, d_halo, c.ent.as<double>() + a * k, c.sel.as<uint8_t>() + a,
+                  stream_out ? c.stream_out.as<uint8_t>() + 2 * off : nullptr, nullptr, ws, st, d_err);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(ev[2 * i + 1], st));
+    CUDA_TRY(cudaStreamWaitEvent(c.s_out, ev[2 * i + 1], 0));
+    CUDA_TRY(cudaMemcpyAsync(ent_out + a * k, c.ent.as<double>() + a * k, (size_t)n * k * 8,
+                             cudaMemcpyDeviceToHost, c.s_out));
+    CUDA_TRY(cudaMemcpyAsync(sel_out + a, c.sel.as<uint8_t>() + a, (size_t)n, cudaMemcpyDeviceToHost,
+                             c.s_out));
+    if (stream_out)
+      CUDA_TRY(cudaMemcpyAsync(stream_out + 2 * off, c.stream_out.as<uint8_t>() + 2 * off,
+                               (size_t)n * npix * 2, cudaMemcpyDeviceToHost, c.s_out));
+  }
+  int flag = 0;
+  CUDA_TRY(cudaMemcpyAsync(&flag, d_err, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaStreamSynchronize(c.s_out));
+  for (auto &e : ev) cudaEventDestroy(e);
+  if (flag) return fail(PCBZ_E_INTERNAL, "judge kernel reported internal error %d", flag);
+  return PCBZ_OK;
 }
 
 int pcbz_select_predictor(const uint16_t *frame, const uint16_t *prev, int64_t h, int64_t w,

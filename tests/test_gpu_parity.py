@@ -296,3 +296,25 @@ def test_device_judge_26_candidates_series():
             assert_entropy(got, want)
         assert sel[f] == best
         assert streams[f].tobytes() == oracle.emit_stream(vol[f + 1], vol[f], best, 15, 15)
+
+
+def test_host_pipeline_chunks_series():
+    """pcbz_judge_host splits >= 8 frames into overlapped chunks; chunk
+    boundaries must be invisible (temporal halo = last frame of the previous
+    chunk)."""
+    p = SynthParams(96, 80, 15, 15, mode="smooth_lenslet", noise_sigma=20.0, photon_scale=0.05,
+                    frames=13, drift=1.0, seed=8)
+    vol = generate_array(p)
+    codes = list(range(13)) + [0x80 | i for i in range(13)]
+    ent, sel, streams = pipeline.judge_volume(vol, LensletGeometry(15, 15), codes, temporal=True)
+    prev = None
+    for f in range(vol.shape[0]):
+        cands = codes if prev is not None else list(range(13))
+        entries, best, _ = oracle.select_predictor(vol[f], prev, cands, 15, 15)
+        got = {c: e for c, e in zip(codes, ent[f]) if not np.isnan(e)}
+        assert sorted(got) == cands
+        for c, want in entries:
+            assert_entropy(got[c], want)
+        assert sel[f] == best
+        assert streams[f].tobytes() == oracle.emit_stream(vol[f], prev, best, 15, 15)
+        prev = vol[f]
