@@ -129,6 +129,44 @@ PCBZ_API int pcbz_reconstruct_host(const uint16_t *residuals, const uint16_t *ha
                           int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *sel,
                           uint16_t *frames_out);
 
+/* Band sharding of the judge across ranks (no reference counterpart: the
+ * reference judges a frame in one process, criterion.py:136-173; this splits
+ * the same computation so N GPUs share one frame -- SURVEY §8(e)).
+ *
+ * Every (frame, candidate) stream is cut into nbands contiguous pixel bands.
+ * Rank `band` runs pcbz_judge_band_device on its band and produces
+ *   d_hist_out    [nframes*k][65536] u32 partial pair counts (zeroed here)
+ *   d_summary_out [nframes*k][S][2][256] i16 first/last pred per key of each
+ *                 of its S segments (-1 = key absent); S, the summary bytes and
+ *                 the workspace bytes come from pcbz_band_layout, identical on
+ *                 every rank for identical arguments.
+ * The caller then SUMS the histograms over ranks (e.g. an NCCL all-reduce)
+ * and GATHERS the summaries in band order into [nbands][nframes*k][S][2][256];
+ * pcbz_judge_merge_device adds the seams between segments and buckets in
+ * stream order, takes the entropies and the argmin (identical to
+ * pcbz_judge_device on the whole frames, bit for bit).  Emission is
+ * band-local too: pcbz_emit_band_device writes [nframes][2*(end-begin)] bytes
+ * for the pixel range pcbz_band_range returns; concatenating the bands of a
+ * frame gives its full stream.  Frames (and the halo) must be resident on
+ * every rank. */
+PCBZ_API int pcbz_band_layout(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py,
+                     const uint8_t *specs, int k, int temporal, int has_halo, int nbands,
+                     int *segments_per_band, size_t *summary_bytes, size_t *workspace_bytes);
+PCBZ_API int pcbz_band_range(int64_t h, int64_t w, int nbands, int band, int64_t *pix_begin,
+                    int64_t *pix_end);
+PCBZ_API int pcbz_judge_band_device(const uint16_t *d_frames, const uint16_t *d_halo_prev, int64_t nframes,
+                           int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *specs, int k,
+                           int temporal, int band, int nbands, uint32_t *d_hist_out,
+                           int16_t *d_summary_out, void *d_workspace, size_t workspace_bytes,
+                           void *stream);
+PCBZ_API int pcbz_judge_merge_device(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py,
+                            const uint8_t *specs, int k, int temporal, int has_halo, int nbands,
+                            uint32_t *d_hist_inout, const int16_t *d_summaries, double *d_ent_out,
+                            uint8_t *d_sel_out, void *stream);
+PCBZ_API int pcbz_emit_band_device(const uint16_t *d_frames, const uint16_t *d_halo_prev, int64_t nframes,
+                          int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *d_sel,
+                          int band, int nbands, uint8_t *d_stream_out, void *stream);
+
 /* Testing hook: force the number of segments each (frame, candidate) stream
  * is split into (0 = automatic).  Outputs must not depend on it. */
 PCBZ_API int pcbz_set_segment_override(int segments);

@@ -49,6 +49,16 @@ SIGNATURES = {
     "pcbz_emit_host": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp]),
     "pcbz_reconstruct_host": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp,
                                        _vp]),
+    "pcbz_band_layout": (_c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _c_int, _c_int,
+                                  _c_int, _c_int, _vp, _vp, _vp]),
+    "pcbz_band_range": (_c_int, [_c_i64, _c_i64, _c_int, _c_int, _vp, _vp]),
+    "pcbz_judge_band_device": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp,
+                                        _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _c_size,
+                                        _vp]),
+    "pcbz_judge_merge_device": (_c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _c_int,
+                                         _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp]),
+    "pcbz_emit_band_device": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp,
+                                       _c_int, _c_int, _vp, _vp]),
     "pcbz_set_segment_override": (_c_int, [_c_int]),
     "pcbz_set_profiling": (_c_int, [_c_int]),
     "pcbz_last_timing": (_c_int, [_vp, _vp, _vp]),

@@ -9,10 +9,11 @@ namespace pcbz {
 
 // Selected residual stream, row-major, high byte first (core.py:228-237).
 __global__ void emit_kernel(const EmitParams P) {
-  const int64_t total = P.nframes * P.npix;
+  const int64_t span = P.pix1 - P.pix0;
+  const int64_t total = P.nframes * span;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t f = t / P.npix, k = t - f * P.npix;
+    const int64_t f = t / span, k = P.pix0 + (t - f * span);
     const int spec = P.sel[f];
     const uint16_t *src = P.frames + f * P.npix;
     const uint16_t *prv = (spec & 0x80) ? prev_of(P.frames, P.halo, P.npix, f) : nullptr;
@@ -99,7 +100,7 @@ static int grid_for(int64_t n, int threads) {
 
 
 cudaError_t launch_emit(const EmitParams &p, cudaStream_t st) {
-  emit_kernel<<<grid_for(p.nframes * p.npix, 256), 256, 0, st>>>(p);
+  emit_kernel<<<grid_for(p.nframes * (p.pix1 - p.pix0), 256), 256, 0, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -179,8 +179,27 @@ int lone_weight() {
   return w;
 }
 
+// workspace offsets of a plan whose S / direct are set
+void layout_workspace(Plan &pl, int64_t nframes, int k, bool want_hist) {
+  const JudgeParams &jp = pl.jp;
+  const int64_t items = jp.npairs * jp.S;
+  pl.grid = (int)std::min<int64_t>(items, num_sms_cached());
+  size_t off = 0;
+  pl.off_counter = off; off = align_up(off + 4);
+  pl.off_err = off; off = align_up(off + 4);
+  pl.off_fscratch = off; off = align_up(off + (size_t)pl.grid * kJudgeThreads * 256);
+  if (!jp.direct) {
+    // band calls keep the summaries in caller memory
+    const size_t sums = jp.nbands > 1 ? 0 : (size_t)nframes * k * jp.S * 512 * sizeof(int16_t);
+    pl.off_segsum = off; off = align_up(off + sums);
+    pl.off_ghist = off; off = align_up(off + (want_hist ? 0 : (size_t)nframes * k * 65536 * 4));
+  }
+  pl.ws_bytes = off;
+}
+
 int make_plan(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *specs,
-              int k, bool halo, int temporal, bool want_hist, Plan &pl) {
+              int k, bool halo, int temporal, bool want_hist, Plan &pl, int nbands = 1,
+              int band = 0) {
   int rc = validate_geometry(h, w, px, py);
   if (rc) return rc;
   rc = validate_specs(specs, k);
@@ -193,28 +212,48 @@ int make_plan(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py, con
   jp.npix = h * w;
   jp.H = (int)h; jp.W = (int)w; jp.px = (int)px; jp.py = (int)py;
   jp.npairs = jp.cl.kA + (nframes - 1) * jp.cl.kB;
-  jp.S = g_seg_override > 0 ? (int)std::min<int64_t>(g_seg_override, jp.npix)
-                            : choose_segments(jp.npairs, jp.npix, want_hist);
-  if ((jp.npix + jp.S - 1) / jp.S > kMaxSegPixels)
+  if (nbands < 1 || band < 0 || band >= nbands || nbands > jp.npix)
+    return fail(PCBZ_E_INVALID, "band %d of %d invalid for %lld pixels", band, nbands, (long long)jp.npix);
+  jp.band = band;
+  jp.nbands = nbands;
+  jp.nslots = nframes * k;
+  const int64_t band_pix = (jp.npix + nbands - 1) / nbands;
+  jp.S = g_seg_override > 0 ? (int)std::min<int64_t>(g_seg_override, band_pix)
+                            : choose_segments(jp.npairs, band_pix, want_hist);
+  if ((jp.npix + (int64_t)jp.S * nbands - 1) / ((int64_t)jp.S * nbands) > kMaxSegPixels)
     return fail(PCBZ_E_INVALID, "segment override %d leaves segments above %lld pixels", jp.S,
                 (long long)kMaxSegPixels);
-  jp.direct = (jp.S == 1 && !want_hist) ? 1 : 0;
+  jp.direct = (jp.S == 1 && nbands == 1 && !want_hist) ? 1 : 0;
   // 8-pixel chunk path: rows of whole chunks and a pitch the fast kernel is
   // instantiated for (pointer alignment is re-checked in run_plan)
   jp.fast_px = (w % 8 == 0 && px <= kMaxFastPitch && g_fast_enabled) ? (int)px : 0;
   jp.lone_weight = lone_weight();
-  const int64_t items = jp.npairs * jp.S;
-  pl.grid = (int)std::min<int64_t>(items, num_sms_cached());
-  size_t off = 0;
-  pl.off_counter = off; off = align_up(off + 4);
-  pl.off_err = off; off = align_up(off + 4);
-  pl.off_fscratch = off; off = align_up(off + (size_t)pl.grid * kJudgeThreads * 256);
-  if (!jp.direct) {
-    pl.off_segsum = off; off = align_up(off + (size_t)nframes * k * jp.S * 512 * sizeof(int16_t));
-    pl.off_ghist = off; off = align_up(off + (want_hist ? 0 : (size_t)nframes * k * 65536 * 4));
-  }
-  pl.ws_bytes = off;
+  layout_workspace(pl, nframes, k, want_hist);
   return PCBZ_OK;
+}
+
+// Workspace bytes of any plan of this shape: the segment count depends on
+// how many (frame, candidate) pairs are scored, which depends on the
+// candidate lists (temporal specs are not scored on a halo-less frame 0), so
+// take the maximum over every list size.
+size_t workspace_upper_bound(int64_t nframes, int64_t h, int64_t w, int k, bool want_hist,
+                             int nbands) {
+  const int64_t npix = h * w;
+  const int64_t band_pix = (npix + nbands - 1) / nbands;
+  size_t best = 0;
+  for (int ka = 1; ka <= k; ++ka)
+    for (int kb = ka; kb <= k; ++kb) {
+      Plan pl;
+      JudgeParams &jp = pl.jp;
+      jp.npairs = ka + (nframes - 1) * kb;
+      jp.nbands = nbands;
+      jp.S = g_seg_override > 0 ? (int)std::min<int64_t>(g_seg_override, band_pix)
+                                : choose_segments(jp.npairs, band_pix, want_hist);
+      jp.direct = (jp.S == 1 && nbands == 1 && !want_hist) ? 1 : 0;
+      layout_workspace(pl, nframes, k, want_hist);
+      best = std::max(best, pl.ws_bytes);
+    }
+  return best;
 }
 
 // Enqueue the whole judge (+ optional emission) on `st`.
@@ -253,7 +292,8 @@ int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double 
   CUDA_TRY(launch_select(jp, d_sel, st));
   ++launches;
   if (d_stream) {
-    EmitParams ep{d_frames, d_halo, jp.nframes, jp.npix, jp.H, jp.W, jp.px, jp.py, d_sel, d_stream};
+    EmitParams ep{d_frames, d_halo, jp.nframes, jp.npix, jp.H, jp.W, jp.px, jp.py, d_sel, d_stream,
+                  0, jp.npix};
     CUDA_TRY(launch_emit_any(ep, st));
     ++launches;
   }
@@ -319,11 +359,8 @@ int pcbz_last_timing(float *hist_ms, float *total_ms, int *launches) {
 }
 
 size_t pcbz_judge_workspace_size(int64_t nframes, int64_t h, int64_t w, int k, int want_hist) {
-  std::vector<uint8_t> specs(std::max(k, 1));
-  for (int i = 0; i < k; ++i) specs[i] = (uint8_t)(i < 13 ? i : (0x80 | (i - 13)));  // shape-only plan
-  Plan pl;
-  if (make_plan(nframes, h, w, 1, 1, specs.data(), k, true, 1, want_hist != 0, pl)) return 0;
-  return pl.ws_bytes;
+  if (nframes < 1 || h < 1 || w < 1 || k < 1 || k > PCBZ_MAX_CANDIDATES) return 0;
+  return workspace_upper_bound(nframes, h, w, k, want_hist != 0, 1);
 }
 
 int pcbz_judge_device(const uint16_t *d_frames, const uint16_t *d_halo_prev, int64_t nframes,
@@ -623,7 +660,8 @@ int pcbz_emit_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t nf
   if (halo_prev) CUDA_TRY(cudaMemcpyAsync(c.prev.p, halo_prev, (size_t)h * w * 2, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(c.sel.p, sel, (size_t)nframes, cudaMemcpyHostToDevice, st));
   EmitParams ep{c.frames.as<uint16_t>(), halo_prev ? c.prev.as<uint16_t>() : nullptr, nframes,
-                h * w, (int)h, (int)w, (int)px, (int)py, c.sel.as<uint8_t>(), c.stream_out.as<uint8_t>()};
+                h * w, (int)h, (int)w, (int)px, (int)py, c.sel.as<uint8_t>(), c.stream_out.as<uint8_t>(),
+                0, h * w};
   CUDA_TRY(launch_emit_any(ep, st));
   CUDA_TRY(cudaMemcpyAsync(stream_out, c.stream_out.p, fb, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -650,6 +688,114 @@ int pcbz_reconstruct_host(const uint16_t *residuals, const uint16_t *halo_prev, 
                               nframes, h, w, (int)px, (int)py, c.sel.as<uint8_t>(), c.out.as<uint16_t>(), st));
   CUDA_TRY(cudaMemcpyAsync(frames_out, c.out.p, fb, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  return PCBZ_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// band sharding: every stream cut into nbands contiguous pixel bands (one per
+// rank); partial histograms + segment summaries are combined by the caller's
+// collective (sum / gather) and finished by pcbz_judge_merge_device
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+int pcbz_band_layout(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py,
+                     const uint8_t *specs, int k, int temporal, int has_halo, int nbands,
+                     int *segments_per_band, size_t *summary_bytes, size_t *workspace_bytes) {
+  Plan pl;
+  int rc = make_plan(nframes, h, w, px, py, specs, k, has_halo != 0, temporal, true, pl, nbands, 0);
+  if (rc) return rc;
+  if (segments_per_band) *segments_per_band = pl.jp.S;
+  if (summary_bytes) *summary_bytes = (size_t)nframes * k * pl.jp.S * 512 * sizeof(int16_t);
+  if (workspace_bytes) *workspace_bytes = pl.ws_bytes;
+  return PCBZ_OK;
+}
+
+int pcbz_band_range(int64_t h, int64_t w, int nbands, int band, int64_t *pix_begin,
+                    int64_t *pix_end) {
+  const int64_t npix = h * w;
+  if (h < 1 || w < 1 || nbands < 1 || band < 0 || band >= nbands)
+    return fail(PCBZ_E_INVALID, "band %d of %d invalid for a %lldx%lld frame", band, nbands,
+                (long long)h, (long long)w);
+  // 8-pixel granules when possible, so every band emits with the chunk kernel
+  const int64_t g = npix % 8 == 0 ? 8 : 1, n = npix / g;
+  *pix_begin = g * (n * band / nbands);
+  *pix_end = g * (n * (band + 1) / nbands);
+  return PCBZ_OK;
+}
+
+int pcbz_judge_band_device(const uint16_t *d_frames, const uint16_t *d_halo_prev, int64_t nframes,
+                           int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *specs, int k,
+                           int temporal, int band, int nbands, uint32_t *d_hist_out,
+                           int16_t *d_summary_out, void *d_workspace, size_t workspace_bytes,
+                           void *stream) {
+  int rc = check_device();
+  if (rc) return rc;
+  if (!d_hist_out || !d_summary_out) return fail(PCBZ_E_INVALID, "band judge needs histogram and summary outputs");
+  Plan pl;
+  rc = make_plan(nframes, h, w, px, py, specs, k, d_halo_prev != nullptr, temporal, true, pl,
+                 nbands, band);
+  if (rc) return rc;
+  if (workspace_bytes < pl.ws_bytes)
+    return fail(PCBZ_E_INVALID, "workspace too small: %zu < %zu bytes", workspace_bytes, pl.ws_bytes);
+  JudgeParams &jp = pl.jp;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char *ws = static_cast<char *>(d_workspace);
+  jp.frames = d_frames;
+  jp.halo = d_halo_prev;
+  if ((reinterpret_cast<uintptr_t>(d_frames) | reinterpret_cast<uintptr_t>(d_halo_prev)) & 15) jp.fast_px = 0;
+  jp.ent = nullptr;
+  jp.counter = reinterpret_cast<int *>(ws + pl.off_counter);
+  jp.err = reinterpret_cast<int *>(ws + pl.off_err);
+  jp.fscratch = reinterpret_cast<uint8_t *>(ws + pl.off_fscratch);
+  jp.ghist = d_hist_out;
+  // the kernel writes band 0's slot of the summary array: point it at this band
+  jp.segsum = d_summary_out - (size_t)band * jp.nslots * jp.S * 512;
+  CUDA_TRY(cudaMemsetAsync(ws, 0, pl.off_fscratch, st));
+  CUDA_TRY(cudaMemsetAsync(d_hist_out, 0, (size_t)jp.nslots * 65536 * 4, st));
+  CUDA_TRY(launch_judge(jp, pl.grid, st));
+  g_launches = 1;
+  return PCBZ_OK;
+}
+
+int pcbz_judge_merge_device(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py,
+                            const uint8_t *specs, int k, int temporal, int has_halo, int nbands,
+                            uint32_t *d_hist_inout, const int16_t *d_summaries, double *d_ent_out,
+                            uint8_t *d_sel_out, void *stream) {
+  int rc = check_device();
+  if (rc) return rc;
+  Plan pl;
+  rc = make_plan(nframes, h, w, px, py, specs, k, has_halo != 0, temporal, true, pl, nbands, 0);
+  if (rc) return rc;
+  JudgeParams &jp = pl.jp;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  jp.ghist = d_hist_inout;
+  jp.segsum = const_cast<int16_t *>(d_summaries);
+  jp.ent = d_ent_out;
+  CUDA_TRY(cudaMemsetAsync(d_ent_out, 0xFF, (size_t)nframes * k * sizeof(double), st));  // NaN
+  CUDA_TRY(launch_finalize(jp, st));
+  CUDA_TRY(launch_select(jp, d_sel_out, st));
+  g_launches = 2;
+  return PCBZ_OK;
+}
+
+int pcbz_emit_band_device(const uint16_t *d_frames, const uint16_t *d_halo_prev, int64_t nframes,
+                          int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *d_sel,
+                          int band, int nbands, uint8_t *d_stream_out, void *stream) {
+  int rc = check_device();
+  if (rc) return rc;
+  if ((rc = validate_geometry(h, w, px, py))) return rc;
+  if (nframes < 1) return fail(PCBZ_E_INVALID, "at least one frame is required");
+  int64_t p0 = 0, p1 = 0;
+  if ((rc = pcbz_band_range(h, w, nbands, band, &p0, &p1))) return rc;
+  g_launches = 0;
+  if (p1 == p0) return PCBZ_OK;
+  EmitParams ep{d_frames, d_halo_prev, nframes, h * w, (int)h, (int)w, (int)px, (int)py, d_sel,
+                d_stream_out, p0, p1};
+  CUDA_TRY(launch_emit_any(ep, static_cast<cudaStream_t>(stream)));
+  g_launches = 1;
   return PCBZ_OK;
 }
 

@@ -18,15 +18,17 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
   int *s_last = s_first + 256;
   const PairRef pr = pair_ref(P, blockIdx.x);
   uint32_t *G = P.ghist + (size_t)pr.slot * 65536;
-  const int16_t *sum = P.segsum + (size_t)pr.slot * P.S * 512;
   for (int v = threadIdx.x; v < 256; v += kEntropyThreads) {
     int carried = -1, first = -1;
-    for (int s = 0; s < P.S; ++s) {
-      const int f = sum[(size_t)s * 512 + v];
-      if (f < 0) continue;
-      if (carried >= 0) atomicAdd(&G[(carried << 8) | f], 1u);
-      else first = f;
-      carried = sum[(size_t)s * 512 + 256 + v];
+    for (int b = 0; b < P.nbands; ++b) {
+      const int16_t *sum = P.segsum + ((size_t)b * P.nslots + pr.slot) * P.S * 512;
+      for (int s = 0; s < P.S; ++s) {
+        const int f = sum[(size_t)s * 512 + v];
+        if (f < 0) continue;
+        if (carried >= 0) atomicAdd(&G[(carried << 8) | f], 1u);
+        else first = f;
+        carried = sum[(size_t)s * 512 + 256 + v];
+      }
     }
     s_first[v] = first;
     s_last[v] = carried;
@@ -115,8 +117,9 @@ cudaError_t launch_judge(const JudgeParams &p, int grid, cudaStream_t st) {
 cudaError_t launch_emit_any(const EmitParams &p, cudaStream_t st) {
   const bool aligned = ((reinterpret_cast<uintptr_t>(p.frames) | reinterpret_cast<uintptr_t>(p.halo) |
                          reinterpret_cast<uintptr_t>(p.stream)) & 15) == 0;
-  if (p.W % 8 != 0 || p.px < 1 || p.px > kMaxFastPitch || !aligned) return launch_emit(p, st);
-  const int64_t chunks = p.nframes * (p.npix / 8);
+  if (p.W % 8 != 0 || p.px < 1 || p.px > kMaxFastPitch || !aligned || (p.pix0 | p.pix1) % 8)
+    return launch_emit(p, st);
+  const int64_t chunks = p.nframes * ((p.pix1 - p.pix0) / 8);
   const int grid = (int)std::min<int64_t>((chunks + 255) / 256, 148 * 16);
   switch (p.px) {
 #define PCBZ_CASE(n) \

@@ -55,13 +55,15 @@ struct JudgeParams {
   int H, W, px, py;
   CandLists cl;
   int64_t npairs;           // scored (frame, candidate) pairs
-  int S;                    // segments per pair
+  int S;                    // segments per pair (per band)
+  int band, nbands;         // this call's band of a stream cut into nbands * S segments
+  int64_t nslots;           // nframes * k (segment-summary stride of one band)
   int direct;               // 1: S == 1 and no histogram output -> entropy in-CTA
   int fast_px;              // >0: 8-pixel chunk path instantiated for pitch_x; 0: generic
   int lone_weight;          // run-length weight (x16) of warps alone on a scheduler
   double *ent;              // [nframes][k] (NaN = not scored)
   uint32_t *ghist;          // [nframes*k][65536] when !direct
-  int16_t *segsum;          // [nframes*k][S][2][256] when !direct
+  int16_t *segsum;          // [nbands][nframes*k][S][2][256] when !direct
   uint8_t *fscratch;        // [gridDim.x][kJudgeThreads][256]
   int *counter;             // dynamic item counter (zeroed before launch)
   int *err;                 // sticky error flag
@@ -72,7 +74,8 @@ struct EmitParams {
   int64_t nframes, npix;
   int H, W, px, py;
   const uint8_t *sel;       // [nframes] selected predictor byte
-  uint8_t *stream;          // [nframes][2*npix] big-endian residual bytes
+  uint8_t *stream;          // [nframes][2*(pix1-pix0)] big-endian residual bytes
+  int64_t pix0, pix1;       // emitted pixel range of every frame (a band; 0, npix = all)
 };
 
 // launchers (judge.cu)

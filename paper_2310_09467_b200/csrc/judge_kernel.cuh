@@ -336,12 +336,13 @@ __device__ __forceinline__ void chunk_residuals_dispatch(int id, const uint16_t 
 // one thread per 8-pixel chunk of every frame (W % 8 == 0, PX <= 16)
 template <int PX>
 __global__ void __launch_bounds__(256) emit_chunks_kernel(const EmitParams P) {
-  const int64_t cpf = P.npix / 8;  // chunks per frame
-  const int cpr = P.W / 8;         // chunks per row
+  const int64_t cpf = (P.pix1 - P.pix0) / 8;  // emitted chunks per frame
+  const int64_t c0 = P.pix0 / 8;
+  const int cpr = P.W / 8;                    // chunks per row
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < P.nframes * cpf;
        c += (int64_t)gridDim.x * blockDim.x) {
     const int64_t f = c / cpf;
-    const int64_t k = c - f * cpf;
+    const int64_t kb = c - f * cpf, k = c0 + kb;
     const int y = (int)(k / cpr), x0 = (int)(k - (int64_t)y * cpr) * 8;
     const int spec = P.sel[f];
     const uint16_t *src = P.frames + f * P.npix;
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(256) emit_chunks_kernel(const EmitParams P) {
     o.y = __byte_perm(r[2] | (r[3] << 16), 0, 0x2301);
     o.z = __byte_perm(r[4] | (r[5] << 16), 0, 0x2301);
     o.w = __byte_perm(r[6] | (r[7] << 16), 0, 0x2301);
-    *reinterpret_cast<uint4 *>(P.stream + 2 * (f * P.npix + k * 8)) = o;
+    *reinterpret_cast<uint4 *>(P.stream + 2 * (f * (P.pix1 - P.pix0) + kb * 8)) = o;
   }
 }
 
@@ -418,6 +419,8 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
 
     const int64_t pair = item / P.S;
     const int seg = (int)(item % P.S);
+    // global segment of the stream: bands are contiguous runs of S segments
+    const int64_t gseg = (int64_t)P.band * P.S + seg, gtot = (int64_t)P.nbands * P.S;
     const PairRef pr = pair_ref(P, pair);
     const uint16_t *src = P.frames + pr.frame * P.npix;
     const uint16_t *prv = (pr.spec & 0x80) ? prev_of(P.frames, P.halo, P.npix, pr.frame) : nullptr;
@@ -426,7 +429,7 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
     if constexpr (PX > 0) {
       // chunk-granular segments and runs
       const int64_t nchunk = P.npix / 8;
-      const int64_t cb = nchunk * seg / P.S, ce = nchunk * (seg + 1) / P.S;
+      const int64_t cb = nchunk * gseg / gtot, ce = nchunk * (gseg + 1) / gtot;
       const int64_t ca = cb + (ce - cb) * w_lo / w_total;
       const int64_t cz = cb + (ce - cb) * w_hi / w_total;
       if (pr.spec & 0x80)
@@ -436,7 +439,7 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
         lane_fast_dispatch<PX, false>(pr.spec & 0x7F, src, prv, P.W, P.py, P.npix, ca * 8,
                                       cz - ca, cfg, cs, std::make_integer_sequence<int, 13>{});
     } else {
-      const int64_t sb = P.npix * seg / P.S, se = P.npix * (seg + 1) / P.S;
+      const int64_t sb = P.npix * gseg / gtot, se = P.npix * (gseg + 1) / gtot;
       const int64_t len = se - sb;
       lane_generic(src, prv, cfg, P.W, P.npix, sb + len * tid / kJudgeThreads,
                    sb + len * (tid + 1) / kJudgeThreads, cs);
@@ -527,7 +530,7 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
       }
       const int ns = min(s_nspill, kSpillCap);
       for (int i = tid; i < ns; i += kJudgeThreads) atomicAdd(&G[spill_w[i]], kSpill);
-      int16_t *sum = P.segsum + ((size_t)pr.slot * P.S + seg) * 512;
+      int16_t *sum = P.segsum + (((size_t)P.band * P.nslots + pr.slot) * P.S + seg) * 512;
       for (int v = tid; v < 256; v += kJudgeThreads) {
         sum[v] = (int16_t)s_first[v];
         sum[256 + v] = (int16_t)s_last[v];

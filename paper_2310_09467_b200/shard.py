@@ -55,6 +55,32 @@ def judge_shard(vol: np.ndarray, shard: FrameShard, geo, codes, temporal: bool, 
     return judge_fn(frames, halo, geo, codes, temporal)
 
 
+def band_collective(partial_fn, summaries_out, merge_fn, emit_fn, nbands: int, group=None):
+    """Within-frame band sharding: the one exchange step of a
+    band-split judge.  partial_fn() -> (hist [P, 65536] int32, summary [n]
+    int16) for this rank's band; the histograms are SUMMED in place over the
+    group and the summaries GATHERED in rank (= band) order into
+    summaries_out [nbands, n]; merge_fn() then finishes entropies and modes
+    (identical on every rank) and emit_fn() writes this rank's band of the
+    streams.  Backend-agnostic: NCCL on device tensors, gloo on CPU tensors
+    (tests/test_sharding.py drives it with the oracle's band restatement)."""
+    import torch
+    import torch.distributed as dist
+
+    hist, summary = partial_fn()
+    if nbands > 1:
+        dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
+        if summary.is_cuda:  # NCCL: one gather straight into the band-ordered buffer
+            dist.all_gather_into_tensor(summaries_out.view(-1), summary, group=group)
+        else:  # gloo has no int16: move the (even-length) summaries as int32 pairs
+            dist.all_gather(list(summaries_out.view(torch.int32).unbind(0)),
+                            summary.view(torch.int32), group=group)
+    else:
+        summaries_out[0].copy_(summary)
+    ent, sel = merge_fn()
+    return ent, sel, emit_fn()
+
+
 def compress_sharded(vol: np.ndarray, geo, codes, temporal: bool, block_size: int,
                      rank: int, world: int, judge_fn=None, group=None):
     """Every rank judges and bzip2-codes its shard; rank 0 gathers the per-frame

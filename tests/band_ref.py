@@ -1,0 +1,108 @@
+"""Test infrastructure: numpy restatement of the band-sharded judge
+(include/pcbz_b200.h "band sharding") over the oracle's byte streams, used as
+each rank's stand-in for the device kernels in the CPU gloo tests.
+
+The chain of a candidate's byte stream s (reference _kernels.py:136-154):
+event j has key s[j] and pred s[j-1] (s[-1] for j = 0); each event pairs
+with the previous event of the same key, and the first/last pred of each
+key's bucket are stitched across buckets (_kernels.py:125-133).  A band of
+pixels [p0, p1) owns events [2*p0, 2*p1); its S segments each contribute
+their in-segment pairs plus a (first, last) pred per key, merged in order.
+"""
+import numpy as np
+
+import oracle
+
+
+def band_range(h, w, nbands, band):
+    """Same split as pcbz_band_range: 8-pixel granules when h*w % 8 == 0."""
+    npix = h * w
+    g = 8 if npix % 8 == 0 else 1
+    n = npix // g
+    return g * (n * band // nbands), g * (n * (band + 1) // nbands)
+
+
+def slot_streams(frames, halo, codes, temporal, px, py):
+    """Byte stream of every scored (frame, candidate) slot, None if unscored
+    (temporal specs need a previous frame, pipeline.py:67-73)."""
+    out = []
+    prev = halo
+    for f in range(frames.shape[0]):
+        for c in codes:
+            scored = not c & 0x80 or (temporal and prev is not None)
+            out.append(np.frombuffer(oracle.emit_stream(frames[f], prev, c, px, py), np.uint8)
+                       if scored else None)
+        prev = frames[f]
+    return out
+
+
+def _segment(s, j0, j1, hist):
+    """Chain over events [j0, j1): in-segment pairs into hist, (first, last)."""
+    first = np.full(256, -1, np.int16)
+    last = np.full(256, -1, np.int16)
+    if j1 <= j0:
+        return first, last
+    keys = s[j0:j1].astype(np.int64)
+    preds = s[np.arange(j0, j1) - 1].astype(np.int64)  # index -1 wraps to the last byte
+    order = np.argsort(keys, kind="stable")
+    ks, ps = keys[order], preds[order]
+    same = ks[1:] == ks[:-1]
+    np.add.at(hist, (ps[:-1][same] << 8) | ps[1:][same], 1)
+    starts = np.flatnonzero(np.r_[True, ~same])
+    ends = np.r_[starts[1:] - 1, ks.size - 1]
+    first[ks[starts]] = ps[starts]
+    last[ks[ends]] = ps[ends]
+    return first, last
+
+
+def band_partial(streams, npix, p0, p1, S):
+    """(hist [P, 65536] int32, summary [P, S, 2, 256] int16) of one band."""
+    P = len(streams)
+    hist = np.zeros((P, 65536), np.int64)
+    summ = np.full((P, S, 2, 256), -1, np.int16)
+    for slot, s in enumerate(streams):
+        if s is None:
+            continue
+        for t in range(S):
+            a = p0 + (p1 - p0) * t // S
+            b = p0 + (p1 - p0) * (t + 1) // S
+            summ[slot, t, 0], summ[slot, t, 1] = _segment(s, 2 * a, 2 * b, hist[slot])
+    return hist.astype(np.int32), summ
+
+
+def merge(hist_sum, summaries, streams, codes, nframes, npix, temporal, has_halo):
+    """Seams across segments and buckets, entropies (numpy's, criterion.py:86-96)
+    and the argmin over (entropy, byte) (criterion.py:171-173)."""
+    k = len(codes)
+    ent = np.full((nframes, k), np.nan)
+    hist = hist_sum.astype(np.int64).copy()
+    for slot, s in enumerate(streams):
+        if s is None:
+            continue
+        seq = summaries[:, slot].reshape(-1, 2, 256)  # band-major, then segment
+        fb = np.full(256, -1)
+        lb = np.full(256, -1)
+        for v in range(256):
+            carried = first = -1
+            for f, l in zip(seq[:, 0, v], seq[:, 1, v]):
+                if f < 0:
+                    continue
+                if carried >= 0:
+                    hist[slot, (carried << 8) | f] += 1
+                else:
+                    first = f
+                carried = l
+            fb[v], lb[v] = first, carried
+        carried = -1
+        for v in range(256):
+            if fb[v] < 0:
+                continue
+            if carried >= 0:
+                hist[slot, (carried << 8) | fb[v]] += 1
+            carried = lb[v]
+        ent[slot // k, slot % k] = oracle.entropy2d(hist[slot], 2 * npix - 1)
+    sel = np.zeros(nframes, np.uint8)
+    for f in range(nframes):
+        scored = [i for i in range(k) if not np.isnan(ent[f, i])]
+        sel[f] = codes[min(scored, key=lambda i: (ent[f, i], codes[i]))]
+    return ent, sel, hist

@@ -79,3 +79,109 @@ def test_two_rank_container_equals_single_process():
         assert p.exitcode == 0
     want, _ = oracle.compress_stack(vol, 6, 5)
     assert sha(data) == sha(want)
+
+
+# ---- within-frame band sharding ------------------------------------------------
+
+import band_ref  # noqa: E402
+
+
+def _band_case():
+    vol = generate_array(SynthParams(40, 32, 6, 5, mode="smooth_lenslet", noise_sigma=30.0,
+                                     photon_scale=0.05, frames=3, drift=0.5, seed=11))
+    codes = list(range(13)) + [0x80 | i for i in range(13)]
+    return vol, codes
+
+
+@pytest.mark.parametrize("nbands,S", [(1, 1), (2, 1), (3, 2), (5, 3), (8, 1)])
+def test_band_algebra_equals_whole_stream(nbands, S):
+    """Partial band histograms + gathered summaries merge to the reference's
+    whole-stream histogram, entropies and modes (oracle on full frames)."""
+    vol, codes = _band_case()
+    F, H, W = vol.shape
+    streams = band_ref.slot_streams(vol, None, codes, True, 6, 5)
+    parts = [band_ref.band_partial(streams, H * W, *band_ref.band_range(H, W, nbands, b), S)
+             for b in range(nbands)]
+    hsum = sum(p[0].astype(np.int64) for p in parts)
+    summaries = np.stack([p[1] for p in parts])
+    ent, sel, hist = band_ref.merge(hsum, summaries, streams, codes, F, H * W, True, False)
+    want_ent, want_sel, _ = oracle_judge(vol, None, LensletGeometry(6, 5), codes, True)
+    for slot, s in enumerate(streams):
+        if s is not None:
+            assert np.array_equal(hist[slot], oracle.bwt_pair_hist(s))
+    assert np.array_equal(np.isnan(ent), np.isnan(want_ent))
+    assert np.array_equal(ent[~np.isnan(ent)], want_ent[~np.isnan(want_ent)])
+    assert np.array_equal(sel, want_sel)
+
+
+def test_band_ranges_partition_and_match_abi():
+    from paper_2310_09467_b200 import _lib
+    import ctypes
+    lib = _lib.load()
+    for (h, w) in [(40, 32), (7, 9), (2048, 2048), (1, 3)]:
+        for n in (1, 2, 3, 8):
+            if n > h * w:
+                continue
+            ranges = [band_ref.band_range(h, w, n, b) for b in range(n)]
+            assert ranges[0][0] == 0 and ranges[-1][1] == h * w
+            assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+            for b, (p0, p1) in enumerate(ranges):
+                x0, x1 = ctypes.c_int64(), ctypes.c_int64()
+                assert lib.pcbz_band_range(h, w, n, b, ctypes.byref(x0), ctypes.byref(x1)) == 0
+                assert (x0.value, x1.value) == (p0, p1)
+    assert lib.pcbz_band_range(4, 4, 2, 2, ctypes.byref(x0), ctypes.byref(x1)) == _lib.PCBZ_E_INVALID
+
+
+def _band_worker(rank, world, port, vol, codes, out):
+    import torch
+
+    from paper_2310_09467_b200.shard import band_collective
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    F, H, W = vol.shape
+    S = 2
+    streams = band_ref.slot_streams(vol, None, codes, True, 6, 5)
+    p0, p1 = band_ref.band_range(H, W, world, rank)
+    h, s = band_ref.band_partial(streams, H * W, p0, p1, S)
+    hist = torch.from_numpy(h)
+    summary = torch.from_numpy(s.reshape(-1).copy())
+    summaries = torch.empty((world, summary.numel()), dtype=torch.int16)
+
+    def merge_fn():
+        e, sl, _ = band_ref.merge(hist.numpy(), summaries.numpy().reshape(world, len(streams), S, 2, 256),
+                                  streams, codes, F, H * W, True, False)
+        merge_fn.sel = sl
+        return e, sl
+
+    def emit_fn():
+        prev, rows = None, []
+        for f in range(F):
+            full = np.frombuffer(oracle.emit_stream(vol[f], prev, int(merge_fn.sel[f]), 6, 5), np.uint8)
+            rows.append(full[2 * p0:2 * p1])
+            prev = vol[f]
+        return np.stack(rows)
+
+    ent, sel, band_stream = band_collective(lambda: (hist, summary), summaries, merge_fn, emit_fn,
+                                            world, None)
+    out.put((rank, ent, sel, band_stream))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_band_sharded_judge_equals_oracle():
+    vol, codes = _band_case()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_band_worker, args=(r, 2, port, vol, codes, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    want_ent, want_sel, want_streams = oracle_judge(vol, None, LensletGeometry(6, 5), codes, True)
+    for _, ent, sel, _ in res:
+        assert np.array_equal(ent, want_ent, equal_nan=True)
+        assert np.array_equal(sel, want_sel)
+    assert np.array_equal(np.concatenate([r[3] for r in res], axis=1), want_streams)
