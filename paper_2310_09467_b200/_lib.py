@@ -61,6 +61,8 @@ SIGNATURES = {
                                        _c_int, _c_int, _vp, _vp]),
     "pcbz_set_segment_override": (_c_int, [_c_int]),
     "pcbz_set_profiling": (_c_int, [_c_int]),
+    "pcbz_set_item_trace": (_c_int, [_c_int]),
+    "pcbz_item_trace": (_c_i64, [_vp, _c_i64, _vp]),
     "pcbz_last_timing": (_c_int, [_vp, _vp, _vp]),
 }
 

@@ -83,9 +83,19 @@ __global__ void __launch_bounds__(kEntropyThreads) entropy_u64_kernel(const uint
                                                                     double *out) {
   extern __shared__ uint4 smem_raw[];
   NpScratch &scr = *reinterpret_cast<NpScratch *>(smem_raw);
-  auto get = [&](int bin) -> double { return (double)counts[bin]; };
-  const double e = block_entropy(get, total, scr);
+  auto get = [&](int bin) -> uint64_t { return counts[bin]; };
+  const double e = block_entropy(get, total, scr, nullptr);
   if (threadIdx.x == 0) *out = e;
+}
+
+__global__ void term_table_kernel(double total, double *terms) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < kTermTable; c += gridDim.x * blockDim.x)
+    terms[c] = c == 0 ? 0.0 : np_term((double)c, total);
+}
+
+cudaError_t launch_term_table(double total, double *terms, cudaStream_t st) {
+  term_table_kernel<<<64, 256, 0, st>>>(total, terms);
+  return cudaGetLastError();
 }
 
 static int grid_for(int64_t n, int threads) {

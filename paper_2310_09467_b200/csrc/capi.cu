@@ -27,6 +27,12 @@ struct TimedCall { cudaEvent_t e0, e1, e2; int launches; };
 thread_local std::vector<TimedCall> g_timed;
 thread_local int g_seg_override = 0;
 thread_local bool g_fast_enabled = true;
+// per-item trace of the last profiled judge (tools/trace_items.py)
+thread_local bool g_trace_on = false;
+thread_local uint64_t *g_trace_dev = nullptr;
+thread_local size_t g_trace_cap = 0;
+thread_local int64_t g_trace_items = 0;
+thread_local int g_trace_segments = 0;
 
 int fail(int code, const char *fmt, ...) {
   char buf[512];
@@ -92,6 +98,7 @@ struct DevBuf {
 struct HostCtx {
   cudaStream_t stream = nullptr;
   cudaStream_t s_in = nullptr, s_out = nullptr;  // pcbz_judge_host copy streams
+  cudaStream_t s_comp2 = nullptr;                // its second compute stream
   DevBuf frames, prev, out, ent, sel, stream_out, hist, ws, scratch, bytes;
   int init() {
     if (stream) return PCBZ_OK;
@@ -121,38 +128,51 @@ int validate_specs(const uint8_t *specs, int k) {
   return PCBZ_OK;
 }
 
-// Work decomposition: segments per pair so that the persistent grid sees
-// about two waves of items, while no segment exceeds kMaxSegPixels.
+// Work decomposition: segments per (frame, candidate) stream.  Items are
+// pulled dynamically by one CTA per SM; item costs differ by candidate (up to
+// ~1.8x, temporal phase predictors dearest), so the tail shrinks with the
+// item size, while every extra segment adds a histogram flush, a stitch and
+// the finalize pass.  Measured (profiles/r01_notes.md, tools/sweep_segments.py,
+// tools/trace_items.py): the fewest power-of-two segments giving >= 8 waves
+// of items win (C2 1300 pairs and C3: S = 1, no flush / finalize; C4 4096^2
+// x 195 pairs: S = 8; C1: S = 8); items below ~512K pixels lose to per-item
+// overhead.
 int choose_segments(int64_t npairs, int64_t npix, bool want_hist) {
   (void)want_hist;
+  static const int64_t target_waves = [] {
+    const char *e = getenv("PCBZ_TARGET_WAVES");
+    const int64_t v = e ? atoll(e) : 8;
+    return v < 1 ? 1 : v;
+  }();
   const int64_t nsm = num_sms_cached();
   const int64_t s_min = std::max<int64_t>(1, (npix + kMaxSegPixels - 1) / kMaxSegPixels);
-  const int64_t s_max = std::max<int64_t>(s_min, std::min<int64_t>(4096, npix / (64 * kJudgeThreads)));
-  // Items are pulled dynamically by one CTA per SM; pick the segment count
-  // whose item count fills the last wave best (ties -> fewer segments, i.e.
-  // less stitching and no global flush), considering only splits that give
-  // each segment >= 64 pixels per lane.
-  int64_t best = s_min;
-  double best_eff = -1.0;
-  for (int64_t s = s_min; s <= std::min(s_max, s_min + 2 * nsm); ++s) {
-    const int64_t items = npairs * s;
-    const int64_t waves = (items + nsm - 1) / nsm;
-    const double eff = (double)items / (double)(waves * nsm);
-    if (eff > best_eff + 0.01) {
-      best_eff = eff;
-      best = s;
-    }
-    if (items >= 8 * nsm && eff > 0.95) break;
-  }
-  return (int)best;
+  const int64_t s_cap = std::max<int64_t>(s_min, std::min<int64_t>(4096, npix / kMinItemPixels));
+  int64_t s = 1;
+  while (s < s_min) s <<= 1;
+  while (npairs * s < target_waves * nsm && 2 * s <= s_cap) s <<= 1;
+  return (int)std::max<int64_t>(s_min, std::min<int64_t>(s, s_cap));
 }
 
 struct Plan {
   JudgeParams jp{};
   int grid = 0;
   size_t ws_bytes = 0;
-  size_t off_counter = 0, off_err = 0, off_fscratch = 0, off_segsum = 0, off_ghist = 0;
+  size_t off_counter = 0, off_err = 0, off_terms = 0, off_fscratch = 0, off_segsum = 0, off_ghist = 0;
 };
+
+// Relative cost class of scoring one predictor byte (per-item trace,
+// profiles/r01_notes.md): temporal specs load two frames, the phase group
+// three neighbourhoods; identity is cheapest.
+int cost_class(uint8_t b) {
+  const int id = b & 0x7F;
+  const int grp = id == 0 ? 0 : 1 + (id - 1) / 4;  // 0 identity, 1 pixel, 2 lenslet, 3 phase
+  return (b & 0x80 ? 4 : 0) + grp;
+}
+
+void order_by_cost(const uint8_t *bytes, int n, uint8_t *ord) {
+  for (int i = 0; i < n; ++i) ord[i] = (uint8_t)i;
+  std::stable_sort(ord, ord + n, [&](uint8_t a, uint8_t b) { return cost_class(bytes[a]) > cost_class(bytes[b]); });
+}
 
 int build_lists(const uint8_t *specs, int k, bool halo, int temporal, CandLists &cl) {
   memset(&cl, 0, sizeof cl);
@@ -163,6 +183,8 @@ int build_lists(const uint8_t *specs, int k, bool halo, int temporal, CandLists 
     if (!t || temporal) { cl.byteB[cl.kB] = specs[i]; cl.idxB[cl.kB++] = (uint8_t)i; }
   }
   if (cl.kA == 0) return fail(PCBZ_E_INVALID, "no usable candidate for a frame without a previous frame");
+  order_by_cost(cl.byteA, cl.kA, cl.ordA);
+  order_by_cost(cl.byteB, cl.kB, cl.ordB);
   return PCBZ_OK;
 }
 
@@ -187,6 +209,7 @@ void layout_workspace(Plan &pl, int64_t nframes, int k, bool want_hist) {
   size_t off = 0;
   pl.off_counter = off; off = align_up(off + 4);
   pl.off_err = off; off = align_up(off + 4);
+  pl.off_terms = off; off = align_up(off + (jp.nbands > 1 ? 0 : kTermTable * sizeof(double)));
   pl.off_fscratch = off; off = align_up(off + (size_t)pl.grid * kJudgeThreads * 256);
   if (!jp.direct) {
     // band calls keep the summaries in caller memory
@@ -197,9 +220,12 @@ void layout_workspace(Plan &pl, int64_t nframes, int k, bool want_hist) {
   pl.ws_bytes = off;
 }
 
+// sched_pairs: pairs competing for the SMs when the segment count is chosen
+// (0 = this plan's own; the chunked host pipeline passes the whole call's,
+// since consecutive chunks overlap on two compute streams)
 int make_plan(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *specs,
               int k, bool halo, int temporal, bool want_hist, Plan &pl, int nbands = 1,
-              int band = 0) {
+              int band = 0, int64_t sched_pairs = 0) {
   int rc = validate_geometry(h, w, px, py);
   if (rc) return rc;
   rc = validate_specs(specs, k);
@@ -219,7 +245,7 @@ int make_plan(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py, con
   jp.nslots = nframes * k;
   const int64_t band_pix = (jp.npix + nbands - 1) / nbands;
   jp.S = g_seg_override > 0 ? (int)std::min<int64_t>(g_seg_override, band_pix)
-                            : choose_segments(jp.npairs, band_pix, want_hist);
+                            : choose_segments(sched_pairs > 0 ? sched_pairs : jp.npairs, band_pix, want_hist);
   if ((jp.npix + (int64_t)jp.S * nbands - 1) / ((int64_t)jp.S * nbands) > kMaxSegPixels)
     return fail(PCBZ_E_INVALID, "segment override %d leaves segments above %lld pixels", jp.S,
                 (long long)kMaxSegPixels);
@@ -271,6 +297,7 @@ int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double 
   // a caller running several plans can collect all error flags in one word
   jp.err = d_err_shared ? d_err_shared : reinterpret_cast<int *>(ws + pl.off_err);
   jp.fscratch = reinterpret_cast<uint8_t *>(ws + pl.off_fscratch);
+  jp.terms = reinterpret_cast<const double *>(ws + pl.off_terms);
   if (!jp.direct) {
     jp.segsum = reinterpret_cast<int16_t *>(ws + pl.off_segsum);
     jp.ghist = d_hist ? d_hist : reinterpret_cast<uint32_t *>(ws + pl.off_ghist);
@@ -281,7 +308,22 @@ int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double 
     cudaEventRecord(tc.e0, st);
   }
   int launches = 0;
-  CUDA_TRY(cudaMemsetAsync(ws, 0, pl.off_fscratch, st));   // counter + err
+  jp.trace = nullptr;
+  if (g_trace_on) {
+    const int64_t items = jp.npairs * jp.S;
+    if ((size_t)items * 2 > g_trace_cap) {
+      if (g_trace_dev) cudaFree(g_trace_dev);
+      g_trace_cap = 0;
+      CUDA_TRY(cudaMalloc(&g_trace_dev, (size_t)items * 16));
+      g_trace_cap = (size_t)items * 2;
+    }
+    jp.trace = g_trace_dev;
+    g_trace_items = items;
+    g_trace_segments = jp.S;
+  }
+  CUDA_TRY(cudaMemsetAsync(ws, 0, pl.off_terms, st));   // counter + err
+  CUDA_TRY(launch_term_table((double)(2 * jp.npix - 1), reinterpret_cast<double *>(ws + pl.off_terms), st));
+  ++launches;
   CUDA_TRY(cudaMemsetAsync(d_ent, 0xFF, (size_t)jp.nframes * jp.cl.k * sizeof(double), st));  // NaN
   if (!jp.direct)
     CUDA_TRY(cudaMemsetAsync(jp.ghist, 0, (size_t)jp.nframes * jp.cl.k * 65536 * 4, st));
@@ -388,8 +430,10 @@ int64_t host_chunk_frames(int64_t nframes) {
     return (int64_t)(e ? atoll(e) : 0);
   }();
   if (forced > 0) return std::min(forced, nframes);
-  if (nframes < 8) return nframes;  // too few frames to pay for a pipeline
-  return (nframes + 5) / 6;         // ~6 chunks: short fill/drain, large launches
+  if (nframes < 16) return nframes;  // too few frames to pay for a pipeline
+  // ~10 chunks of >= 8 frames: measured best on C2 (chunk 4/6/8/10/13 frames:
+  // 25.4/32.6/35.8/36.6/35.2 GB/s e2e, profiles/r01_notes.md)
+  return std::max<int64_t>(8, (nframes + 9) / 10);
 }
 
 int pcbz_judge_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t nframes, int64_t h,
@@ -405,46 +449,58 @@ int pcbz_judge_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t n
   const size_t fbytes = (size_t)nframes * npix * 2;
   const int64_t chunk = host_chunk_frames(nframes);
   const int64_t nchunks = (nframes + chunk - 1) / chunk;
-  // workspace for the largest chunk plan (all chunks run on one stream)
+  // Chunks alternate between two compute streams (one workspace each), so the
+  // last, partly filled wave of chunk i overlaps the start of chunk i+1; the
+  // segment count is planned for the whole call's pairs accordingly.
+  auto chunk_plan = [&](int64_t a, Plan &pl) {
+    const int64_t n = std::min(chunk, nframes - a);
+    return make_plan(n, h, w, px, py, specs, k, a > 0 ? temporal != 0 : halo_prev != nullptr,
+                     temporal, false, pl, 1, 0, full.jp.npairs);
+  };
   size_t ws_bytes = 0;
   for (int64_t a = 0; a < nframes; a += chunk) {
     Plan pl;
-    rc = make_plan(std::min(chunk, nframes - a), h, w, px, py, specs, k,
-                   a > 0 ? temporal != 0 : halo_prev != nullptr, temporal, false, pl);
-    if (rc) return rc;
+    if ((rc = chunk_plan(a, pl))) return rc;
     ws_bytes = std::max(ws_bytes, pl.ws_bytes);
   }
+  ws_bytes = align_up(ws_bytes);
+  const int nws = nchunks > 1 ? 2 : 1;
   if ((rc = c.frames.ensure(fbytes)) || (rc = c.ent.ensure((size_t)nframes * k * 8)) ||
-      (rc = c.sel.ensure((size_t)nframes)) || (rc = c.ws.ensure(ws_bytes + 256)))
+      (rc = c.sel.ensure((size_t)nframes)) || (rc = c.ws.ensure(nws * ws_bytes + 256)))
     return rc;
   if (halo_prev && (rc = c.prev.ensure((size_t)npix * 2))) return rc;
   if (stream_out && (rc = c.stream_out.ensure(fbytes))) return rc;
   if (!c.s_in) {
     CUDA_TRY(cudaStreamCreateWithFlags(&c.s_in, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&c.s_out, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c.s_comp2, cudaStreamNonBlocking));
   }
-  cudaStream_t st = c.stream;
-  int *d_err = reinterpret_cast<int *>(c.ws.as<char>() + ws_bytes);  // shared by all chunks
-  char *ws = c.ws.as<char>();
-  CUDA_TRY(cudaMemsetAsync(d_err, 0, 4, st));
-  std::vector<cudaEvent_t> ev(2 * nchunks);
+  cudaStream_t comp[2] = {c.stream, c.s_comp2};
+  int *d_err = reinterpret_cast<int *>(c.ws.as<char>() + nws * ws_bytes);  // shared by all chunks
+  std::vector<cudaEvent_t> ev(2 * nchunks + 1);
   for (auto &e : ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // both compute streams start after the error word is cleared
+  CUDA_TRY(cudaMemsetAsync(d_err, 0, 4, comp[0]));
+  CUDA_TRY(cudaEventRecord(ev[2 * nchunks], comp[0]));
+  CUDA_TRY(cudaStreamWaitEvent(comp[1], ev[2 * nchunks], 0));
   if (halo_prev)
     CUDA_TRY(cudaMemcpyAsync(c.prev.p, halo_prev, (size_t)npix * 2, cudaMemcpyHostToDevice, c.s_in));
   const uint16_t *d_frames = c.frames.as<uint16_t>();
   for (int64_t i = 0; i < nchunks; ++i) {
     const int64_t a = i * chunk, n = std::min(chunk, nframes - a);
     const size_t off = (size_t)a * npix;
+    cudaStream_t st = comp[i & 1];
+    char *ws = c.ws.as<char>() + (i & 1) * ws_bytes;
     CUDA_TRY(cudaMemcpyAsync(c.frames.as<uint16_t>() + off, frames + off, (size_t)n * npix * 2,
                              cudaMemcpyHostToDevice, c.s_in));
     CUDA_TRY(cudaEventRecord(ev[2 * i], c.s_in));
     CUDA_TRY(cudaStreamWaitEvent(st, ev[2 * i], 0));
-    // the previous frame of chunk i's first frame: the halo (chunk 0) or frame a-1
+    // the previous frame of chunk i's first frame: the halo (chunk 0) or frame
+    // a-1, uploaded earlier on the same (in-order) copy stream
     const uint16_t *d_halo = a > 0 ? (temporal ? d_frames + off - npix : nullptr)
                                    : (halo_prev ? c.prev.as<uint16_t>() : nullptr);
     Plan pl;
-    rc = make_plan(n, h, w, px, py, specs, k, d_halo != nullptr, temporal, false, pl);
-    if (rc) return rc;
+    if ((rc = chunk_plan(a, pl))) return rc;
     rc = run_plan(pl, d_frames + off, d_halo, c.ent.as<double>() + a * k, c.sel.as<uint8_t>() + a,
                   stream_out ? c.stream_out.as<uint8_t>() + 2 * off : nullptr, nullptr, ws, st, d_err);
     if (rc) return rc;
@@ -459,9 +515,8 @@ int pcbz_judge_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t n
                                (size_t)n * npix * 2, cudaMemcpyDeviceToHost, c.s_out));
   }
   int flag = 0;
-  CUDA_TRY(cudaMemcpyAsync(&flag, d_err, 4, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  CUDA_TRY(cudaStreamSynchronize(c.s_out));
+  CUDA_TRY(cudaStreamSynchronize(c.s_out));  // every chunk's judge precedes its D2H
+  CUDA_TRY(cudaMemcpy(&flag, d_err, 4, cudaMemcpyDeviceToHost));
   for (auto &e : ev) cudaEventDestroy(e);
   if (flag) return fail(PCBZ_E_INTERNAL, "judge kernel reported internal error %d", flag);
   return PCBZ_OK;
@@ -753,10 +808,20 @@ int pcbz_judge_band_device(const uint16_t *d_frames, const uint16_t *d_halo_prev
   jp.ghist = d_hist_out;
   // the kernel writes band 0's slot of the summary array: point it at this band
   jp.segsum = d_summary_out - (size_t)band * jp.nslots * jp.S * 512;
+  TimedCall tc{nullptr, nullptr, nullptr, 1};
+  if (g_profile) {
+    cudaEventCreate(&tc.e0); cudaEventCreate(&tc.e1); cudaEventCreate(&tc.e2);
+    cudaEventRecord(tc.e0, st);
+  }
   CUDA_TRY(cudaMemsetAsync(ws, 0, pl.off_fscratch, st));
   CUDA_TRY(cudaMemsetAsync(d_hist_out, 0, (size_t)jp.nslots * 65536 * 4, st));
   CUDA_TRY(launch_judge(jp, pl.grid, st));
   g_launches = 1;
+  if (g_profile) {
+    cudaEventRecord(tc.e1, st);
+    cudaEventRecord(tc.e2, st);
+    g_timed.push_back(tc);
+  }
   return PCBZ_OK;
 }
 
@@ -774,10 +839,15 @@ int pcbz_judge_merge_device(int64_t nframes, int64_t h, int64_t w, int64_t px, i
   jp.ghist = d_hist_inout;
   jp.segsum = const_cast<int16_t *>(d_summaries);
   jp.ent = d_ent_out;
+  double *terms = nullptr;  // stream-ordered scratch: this entry point has no workspace
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&terms), kTermTable * sizeof(double), st));
+  CUDA_TRY(launch_term_table((double)(2 * jp.npix - 1), terms, st));
+  jp.terms = terms;
   CUDA_TRY(cudaMemsetAsync(d_ent_out, 0xFF, (size_t)nframes * k * sizeof(double), st));  // NaN
   CUDA_TRY(launch_finalize(jp, st));
   CUDA_TRY(launch_select(jp, d_sel_out, st));
-  g_launches = 2;
+  CUDA_TRY(cudaFreeAsync(terms, st));
+  g_launches = 3;
   return PCBZ_OK;
 }
 
@@ -797,6 +867,28 @@ int pcbz_emit_band_device(const uint16_t *d_frames, const uint16_t *d_halo_prev,
   CUDA_TRY(launch_emit_any(ep, static_cast<cudaStream_t>(stream)));
   g_launches = 1;
   return PCBZ_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// Testing / tuning hook: while on, every judge call on this thread records
+// (smid << 48 | start ns, end ns) per work item; pcbz_item_trace copies the
+// last call's records (item = pair * S + segment) and returns the item count.
+int pcbz_set_item_trace(int on) {
+  g_trace_on = on != 0;
+  return PCBZ_OK;
+}
+
+int64_t pcbz_item_trace(uint64_t *out, int64_t max_items, int *segments) {
+  if (!g_trace_dev || g_trace_items == 0) return 0;
+  const int64_t n = std::min(max_items, g_trace_items);
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(PCBZ_E_CUDA, "trace sync failed");
+  if (cudaMemcpy(out, g_trace_dev, (size_t)n * 16, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(PCBZ_E_CUDA, "trace copy failed");
+  if (segments) *segments = g_trace_segments;
+  return n;
 }
 
 }  // extern "C"

@@ -18,8 +18,8 @@
 // rounded for nearly all arguments), and mathematically tied candidates tie
 // or break exactly as in the reference.
 //
-// Parallel form: thread t owns a run of 32-bin occupancy words; a block
-// scan of occupied counts gives every occupied bin its index in the
+// Parallel form: an occupancy bitmap (warp ballots); thread t owns a run of
+// 32-bin occupancy words; a block scan of occupied counts gives every occupied bin its index in the
 // (virtual) compacted term array.  The recursion tree is built breadth-first
 // by one warp (ballot compaction per level); all leaves (index ranges of at
 // most 128 terms) are evaluated in parallel by walking the occupancy bitmap;
@@ -95,22 +95,37 @@ __device__ inline void np_build_tree(uint32_t n, NpScratch &S) {
   if (lane == 0) S.nlevels = L + 1;
 }
 
-// `get(bin)` returns the bin count as a double (0 = empty); all threads of
-// the block (kEntropyThreads) must call this.
+// One term of numpy's sum, rounded like numpy: p = c / total (IEEE
+// division), p * log2(p) (IEEE product) -- explicit _rn so nothing contracts.
+__device__ __forceinline__ double np_term(double c, double total) {
+  const double p = __ddiv_rn(c, total);
+  return __dmul_rn(p, log2(p));
+}
+
+// terms[c] = np_term(c, total) for c < kTermTable (judge.cuh; one table per
+// call: every pair of a judge call has the same total 2*H*W - 1), so the
+// per-bin divide and log2 become one L2-resident load; identical bits by
+// construction.
+
+// `get(bin)` returns the bin count (integer; 0 = empty); all threads of the
+// block (kEntropyThreads) must call this.  `terms` may be null.
 template <typename Get>
-__device__ double block_entropy(Get get, double total, NpScratch &S) {
+__device__ double block_entropy(Get get, double total, NpScratch &S, const double *terms) {
   const int t = threadIdx.x;
+  // occupancy bitmap: one warp per 32-bin word (lane j reads bin 32w + j,
+  // so the reads are bank-conflict free), a ballot makes the word
+  {
+    const int lane = t & 31;
+    for (int w = t >> 5; w < kOccWords; w += kEntropyThreads / 32) {
+      const bool occ = total > 0.0 && get(32 * w + lane) != 0;
+      const uint32_t bits = __ballot_sync(0xffffffffu, occ);
+      if (lane == 0) S.occ[w] = bits;
+    }
+  }
+  __syncthreads();
   const int w_lo = occ_word_lo(t), w_hi = occ_word_lo(t + 1);
   uint32_t cnt = 0;
-  for (int w = w_lo; w < w_hi; ++w) {
-    uint32_t bits = 0;
-    if (total > 0.0) {
-#pragma unroll 8
-      for (int j = 0; j < 32; ++j) bits |= (get(32 * w + j) > 0.0 ? 1u : 0u) << j;
-    }
-    S.occ[w] = bits;
-    cnt += __popc(bits);
-  }
+  for (int w = w_lo; w < w_hi; ++w) cnt += __popc(S.occ[w]);
   uint32_t incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -157,8 +172,8 @@ __device__ double block_entropy(Get get, double total, NpScratch &S) {
       while (!bits) bits = S.occ[++w];
       const int bin = 32 * w + __ffs(bits) - 1;
       bits &= bits - 1;
-      const double p = __ddiv_rn(get(bin), total);
-      return __dmul_rn(p, log2(p));
+      const uint64_t c = get(bin);
+      return (terms && c < (uint64_t)kTermTable) ? __ldg(terms + c) : np_term((double)c, total);
     };
     double res;
     if (len < 8) {

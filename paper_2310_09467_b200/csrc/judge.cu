@@ -18,17 +18,34 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
   int *s_last = s_first + 256;
   const PairRef pr = pair_ref(P, blockIdx.x);
   uint32_t *G = P.ghist + (size_t)pr.slot * 65536;
+  // the pair's segment summaries in stream order, staged in the (not yet
+  // used) count buffer when they fit: 16-byte loads instead of a dependent
+  // chain of 2-byte loads per key
+  const int nseg = P.nbands * P.S;
+  const bool staged = nseg * 512 <= 65536;
+  if (staged) {
+    uint4 *dst = reinterpret_cast<uint4 *>(c16);
+    for (int b = 0; b < P.nbands; ++b) {
+      const uint4 *src = reinterpret_cast<const uint4 *>(
+          P.segsum + ((size_t)b * P.nslots + pr.slot) * P.S * 512);
+      for (int i = threadIdx.x; i < P.S * 64; i += kEntropyThreads) dst[b * P.S * 64 + i] = __ldcg(src + i);
+    }
+    __syncthreads();
+  }
+  auto seg_sum = [&](int g) -> const int16_t * {
+    if (staged) return reinterpret_cast<const int16_t *>(c16) + (size_t)g * 512;
+    const int b = g / P.S, s = g - b * P.S;
+    return P.segsum + (((size_t)b * P.nslots + pr.slot) * P.S + s) * 512;
+  };
   for (int v = threadIdx.x; v < 256; v += kEntropyThreads) {
     int carried = -1, first = -1;
-    for (int b = 0; b < P.nbands; ++b) {
-      const int16_t *sum = P.segsum + ((size_t)b * P.nslots + pr.slot) * P.S * 512;
-      for (int s = 0; s < P.S; ++s) {
-        const int f = sum[(size_t)s * 512 + v];
-        if (f < 0) continue;
-        if (carried >= 0) atomicAdd(&G[(carried << 8) | f], 1u);
-        else first = f;
-        carried = sum[(size_t)s * 512 + 256 + v];
-      }
+    for (int g = 0; g < nseg; ++g) {
+      const int16_t *sum = seg_sum(g);
+      const int f = sum[v];
+      if (f < 0) continue;
+      if (carried >= 0) atomicAdd(&G[(carried << 8) | f], 1u);
+      else first = f;
+      carried = sum[256 + v];
     }
     s_first[v] = first;
     s_last[v] = carried;
@@ -44,17 +61,34 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
   }
   __threadfence();
   __syncthreads();
-  // stage saturated u16 copies of the counts in shared memory
-  for (int b = threadIdx.x; b < 65536; b += kEntropyThreads) {
-    const uint32_t c = __ldcg(G + b);
-    c16[b] = (uint16_t)(c < 0xFFFFu ? c : 0xFFFFu);
+  // stage saturated u16 copies of the counts in shared memory: 16-byte loads,
+  // eight in flight per thread before any store (the loop is latency bound)
+  {
+    const uint4 *G4 = reinterpret_cast<const uint4 *>(G);
+    uint2 *c4 = reinterpret_cast<uint2 *>(c16);
+    auto sat = [](uint32_t c) -> uint32_t { return c < 0xFFFFu ? c : 0xFFFFu; };
+    constexpr int kUnroll = 8;
+    for (int b0 = threadIdx.x; b0 < 16384; b0 += kEntropyThreads * kUnroll) {
+      uint4 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int b = b0 + u * kEntropyThreads;
+        v[u] = b < 16384 ? __ldcg(G4 + b) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int b = b0 + u * kEntropyThreads;
+        if (b < 16384)
+          c4[b] = make_uint2(sat(v[u].x) | (sat(v[u].y) << 16), sat(v[u].z) | (sat(v[u].w) << 16));
+      }
+    }
   }
   __syncthreads();
-  auto get = [&](int bin) -> double {
+  auto get = [&](int bin) -> uint64_t {
     const uint32_t c = c16[bin];
-    return (double)(c < 0xFFFFu ? c : __ldcg(G + bin));
+    return c < 0xFFFFu ? c : __ldcg(G + bin);
   };
-  const double e = block_entropy(get, (double)(2 * P.npix - 1), scr);
+  const double e = block_entropy(get, (double)(2 * P.npix - 1), scr, P.terms);
   if (threadIdx.x == 0) P.ent[pr.slot] = e;
 }
 

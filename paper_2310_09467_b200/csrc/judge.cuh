@@ -15,8 +15,10 @@ constexpr uint32_t kUnseen = 0x100;            // per-lane "key not seen yet" ma
 constexpr uint32_t kSpill = 0x8000;            // u16 bin spill threshold
 constexpr int kSpillCap = 512;                 // spill list entries per CTA
 constexpr int64_t kMaxSegPixels = 8000000;     // 2 events/pixel / kSpill < kSpillCap
+constexpr int64_t kMinItemPixels = 1 << 19;    // smaller work items lose to per-item overhead
 constexpr int kEntropyThreads = 192;           // all entropy reductions use this shape
 constexpr int kMaxFastPitch = 16;              // fast path: pitch_x <= 16 (template parameter)
+constexpr int kTermTable = 65536;              // precomputed entropy terms per call (entropy.cuh)
 
 constexpr size_t kJudgeSmemBytes =
     (size_t)(kHistWords + kDummyWords + kLastWords * kJudgeThreads + kSpillCap) * sizeof(uint32_t);
@@ -46,6 +48,9 @@ struct CandLists {
   int kA, kB;
   uint8_t byteA[32], idxA[32];
   uint8_t byteB[32], idxB[32];
+  // dispatch order of each list (positions, most expensive candidate first)
+  // so the tail of the dynamic schedule holds the cheapest items
+  uint8_t ordA[32], ordB[32];
 };
 
 struct JudgeParams {
@@ -62,10 +67,12 @@ struct JudgeParams {
   int fast_px;              // >0: 8-pixel chunk path instantiated for pitch_x; 0: generic
   int lone_weight;          // run-length weight (x16) of warps alone on a scheduler
   double *ent;              // [nframes][k] (NaN = not scored)
+  const double *terms;      // [65536] entropy terms of this call's total (entropy.cuh)
   uint32_t *ghist;          // [nframes*k][65536] when !direct
   int16_t *segsum;          // [nbands][nframes*k][S][2][256] when !direct
   uint8_t *fscratch;        // [gridDim.x][kJudgeThreads][256]
   int *counter;             // dynamic item counter (zeroed before launch)
+  uint64_t *trace;          // optional [items][2]: (smid << 48 | start ns, end ns)
   int *err;                 // sticky error flag
 };
 
@@ -93,6 +100,7 @@ cudaError_t launch_pair_hist(const uint8_t *s, int64_t n, uint32_t *hist, cudaSt
 cudaError_t launch_counting_bwt(const uint8_t *s, int64_t n, uint8_t *out, uint32_t *scratch,
                                 size_t scratch_words, cudaStream_t st);
 size_t counting_bwt_scratch_words(int64_t n);
+cudaError_t launch_term_table(double total, double *terms, cudaStream_t st);
 cudaError_t launch_entropy_u64(const uint64_t *counts, double total, double *out, cudaStream_t st);
 cudaError_t launch_reconstruct(const uint16_t *res, const uint16_t *halo, int64_t nframes,
                                int64_t h, int64_t w, int px, int py, const uint8_t *sel,

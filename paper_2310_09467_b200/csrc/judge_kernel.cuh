@@ -44,13 +44,14 @@ struct PairRef {
 __device__ __forceinline__ PairRef pair_ref(const JudgeParams &P, int64_t pair) {
   PairRef r;
   if (pair < P.cl.kA) {
+    const int j = P.cl.ordA[pair];
     r.frame = 0;
-    r.spec = P.cl.byteA[pair];
-    r.slot = P.cl.idxA[pair];
+    r.spec = P.cl.byteA[j];
+    r.slot = P.cl.idxA[j];
   } else {
     const int64_t q = pair - P.cl.kA;
     r.frame = 1 + q / P.cl.kB;
-    const int j = (int)(q % P.cl.kB);
+    const int j = P.cl.ordB[q % P.cl.kB];
     r.spec = P.cl.byteB[j];
     r.slot = r.frame * P.cl.k + P.cl.idxB[j];
   }
@@ -371,6 +372,18 @@ __global__ void __launch_bounds__(256) emit_chunks_kernel(const EmitParams P) {
 // bitmap (words [0, 2048)), first/last per key ([2048, 2560)) and the
 // entropy scratch ([2560, ...)).
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
+
 template <int PX>
 __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const JudgeParams P) {
   extern __shared__ uint4 smem_raw[];
@@ -416,6 +429,8 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
     __syncthreads();
     const int64_t item = s_item;
     if (item >= nitems) break;
+    uint64_t t_start = 0;
+    if (P.trace && tid == 0) t_start = globaltimer_ns();
 
     const int64_t pair = item / P.S;
     const int seg = (int)(item % P.S);
@@ -512,13 +527,13 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
       for (int i = tid; i < ns; i += kJudgeThreads)
         atomicOr(&spilled[spill_w[i] >> 5], 1u << (spill_w[i] & 31));
       __syncthreads();
-      auto get = [&](int bin) -> double {
+      auto get = [&](int bin) -> uint64_t {
         uint32_t c = bin_count16(hist_w, (uint32_t)bin);
         if (spilled[bin >> 5] & (1u << (bin & 31)))
           for (int i = 0; i < ns; ++i) c += spill_w[i] == (uint32_t)bin ? kSpill : 0u;
-        return (double)c;
+        return c;
       };
-      const double e = block_entropy(get, (double)(2 * P.npix - 1), scr);
+      const double e = block_entropy(get, (double)(2 * P.npix - 1), scr, P.terms);
       if (tid == 0) P.ent[pr.slot] = e;
     } else {
       // flush into the pair's global histogram and publish the summary
@@ -537,6 +552,10 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
       }
     }
     __syncthreads();
+    if (P.trace && tid == 0) {
+      P.trace[2 * item] = ((uint64_t)smid() << 48) | (t_start & 0xFFFFFFFFFFFFull);
+      P.trace[2 * item + 1] = globaltimer_ns();
+    }
   }
 }
 

@@ -55,6 +55,40 @@ def judge_shard(vol: np.ndarray, shard: FrameShard, geo, codes, temporal: bool, 
     return judge_fn(frames, halo, geo, codes, temporal)
 
 
+def band_range(h: int, w: int, nbands: int, band: int):
+    """Pixel range [begin, end) of `band` (pcbz_band_range's split: 8-pixel
+    granules when h*w % 8 == 0, so every band emits with the chunk kernel)."""
+    if h < 1 or w < 1 or not 0 <= band < nbands:
+        raise ValueError(f"band {band} of {nbands} invalid for a {h}x{w} frame")
+    npix = h * w
+    g = 8 if npix % 8 == 0 else 1
+    n = npix // g
+    return g * (n * band // nbands), g * (n * (band + 1) // nbands)
+
+
+def band_rows(h: int, w: int, py: int, nbands: int, band: int):
+    """Row ranges of every frame (and of the halo) rank `band` must hold:
+    its band's rows plus py + 1 rows above them (lenslet-stride and
+    pixel-adjacent neighbours, reference _kernels.py:56-66), and for band 0
+    also the last py + 1 rows, whose last pixel's low byte is the wrapped
+    predecessor of stream byte 0 (_kernels.py:172-190).  Sorted, merged
+    [(r0, r1), ...]."""
+    p0, p1 = band_range(h, w, nbands, band)
+    if p1 == p0:
+        return []
+    rows = [(max(0, p0 // w - py - 1), (p1 - 1) // w + 1)]
+    if band == 0:
+        rows.append((max(0, h - py - 1), h))
+    rows.sort()
+    merged = [rows[0]]
+    for a, b in rows[1:]:
+        if a <= merged[-1][1]:
+            merged[-1] = (merged[-1][0], max(merged[-1][1], b))
+        else:
+            merged.append((a, b))
+    return merged
+
+
 def band_collective(partial_fn, summaries_out, merge_fn, emit_fn, nbands: int, group=None):
     """Within-frame band sharding: the one exchange step of a
     band-split judge.  partial_fn() -> (hist [P, 65536] int32, summary [n]

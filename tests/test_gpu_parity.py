@@ -299,11 +299,11 @@ def test_device_judge_26_candidates_series():
 
 
 def test_host_pipeline_chunks_series():
-    """pcbz_judge_host splits >= 8 frames into overlapped chunks; chunk
-    boundaries must be invisible (temporal halo = last frame of the previous
-    chunk)."""
+    """pcbz_judge_host splits >= 16 frames into chunks (here 8 + 8 + 4) that
+    alternate between two compute streams; chunk boundaries must be
+    invisible (temporal halo = last frame of the previous chunk)."""
     p = SynthParams(96, 80, 15, 15, mode="smooth_lenslet", noise_sigma=20.0, photon_scale=0.05,
-                    frames=13, drift=1.0, seed=8)
+                    frames=20, drift=1.0, seed=8)
     vol = generate_array(p)
     codes = list(range(13)) + [0x80 | i for i in range(13)]
     ent, sel, streams = pipeline.judge_volume(vol, LensletGeometry(15, 15), codes, temporal=True)
@@ -320,7 +320,23 @@ def test_host_pipeline_chunks_series():
         prev = vol[f]
 
 
-def _run_bands(vol_t, halo_t, shape, pitch, codes, temporal, nbands):
+def _band_view(vol_t, halo_t, shape, pitch, nbands, band, seed):
+    """What rank `band` holds: only shard.band_rows of every frame (and of the
+    halo) are real, every other row is random garbage."""
+    import torch
+    from paper_2310_09467_b200.shard import band_rows
+    F, H, W = shape
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    junk = lambda t: torch.randint(0, 65536, t.shape, generator=g, dtype=torch.int32).to(torch.uint16).cuda()
+    v, h = junk(vol_t), (junk(halo_t) if halo_t is not None else None)
+    for r0, r1 in band_rows(H, W, pitch[1], nbands, band):
+        v[:, r0:r1] = vol_t[:, r0:r1]
+        if h is not None:
+            h[r0:r1] = halo_t[r0:r1]
+    return v, h
+
+
+def _run_bands(vol_t, halo_t, shape, pitch, codes, temporal, nbands, rows_only=False):
     """All bands of a band-sharded judge on one GPU, one after another; the
     rank collective (sum of histograms, band-ordered gather of summaries) is
     done with torch ops -- no rank waits on another."""
@@ -328,9 +344,11 @@ def _run_bands(vol_t, halo_t, shape, pitch, codes, temporal, nbands):
     from paper_2310_09467_b200.device import BandJudge
     judges = [BandJudge(shape, pitch, codes, temporal, halo_t is not None, b, nbands)
               for b in range(nbands)]
+    views = [(_band_view(vol_t, halo_t, shape, pitch, nbands, b, 100 + b) if rows_only
+              else (vol_t, halo_t)) for b in range(nbands)]
     total = None
     for j in judges:
-        h, s = j.partial(vol_t, halo_t)
+        h, s = j.partial(*views[j.band])
         total = h.clone() if total is None else total + h
         judges[0].summaries[j.band].copy_(s)
     j0 = judges[0]
@@ -339,7 +357,7 @@ def _run_bands(vol_t, halo_t, shape, pitch, codes, temporal, nbands):
     streams = []
     for j in judges:
         j.sel.copy_(sel)
-        streams.append(j.emit(vol_t, halo_t).clone())
+        streams.append(j.emit(*views[j.band]).clone())
     torch.cuda.synchronize()
     return ent.cpu().numpy(), sel.cpu().numpy(), torch.cat(streams, dim=1).cpu().numpy()
 
@@ -348,7 +366,8 @@ def _run_bands(vol_t, halo_t, shape, pitch, codes, temporal, nbands):
     ((3, 96, 128), (15, 15), True, 2), ((3, 96, 128), (15, 15), True, 3),
     ((3, 96, 128), (15, 15), True, 8), ((2, 61, 75), (6, 5), False, 3),
     ((2, 40, 48), (17, 9), False, 5), ((1, 64, 64), (13, 13), False, 1)])
-def test_band_sharded_judge_equals_whole_frames(shape, pitch, halo, nbands):
+@pytest.mark.parametrize("rows_only", [False, True])
+def test_band_sharded_judge_equals_whole_frames(shape, pitch, halo, nbands, rows_only):
     """pcbz_judge_band_device x nbands + merge == pcbz_judge_device, bit for bit
     (entropies, modes), and the concatenated band streams == whole streams."""
     import torch
@@ -362,7 +381,7 @@ def test_band_sharded_judge_equals_whole_frames(shape, pitch, halo, nbands):
     codes = list(range(13)) + [0x80 | i for i in range(13)]
     whole = DeviceJudge(shape, pitch, codes, temporal=True)
     e0, s0, st0 = (x.cpu().numpy() for x in whole(frames, halo_t))
-    ent, sel, streams = _run_bands(frames, halo_t, shape, pitch, codes, True, nbands)
+    ent, sel, streams = _run_bands(frames, halo_t, shape, pitch, codes, True, nbands, rows_only)
     assert np.array_equal(ent, e0, equal_nan=True)
     assert np.array_equal(sel, s0)
     assert np.array_equal(streams, st0)
@@ -376,7 +395,7 @@ def test_band_sharded_large_frame_vs_oracle():
     img = generate_array(p)
     codes = [0, 5, 12]
     ent, sel, streams = _run_bands(torch.from_numpy(img).cuda(), None, img.shape, (13, 13), codes,
-                                   False, 4)
+                                   False, 4, rows_only=True)
     entries, best, _ = oracle.select_predictor(img[0], None, codes, 13, 13)
     for (c, want), got in zip(entries, ent[0]):
         assert_entropy(got, want)

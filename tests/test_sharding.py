@@ -185,3 +185,23 @@ def test_two_rank_band_sharded_judge_equals_oracle():
         assert np.array_equal(ent, want_ent, equal_nan=True)
         assert np.array_equal(sel, want_sel)
     assert np.array_equal(np.concatenate([r[3] for r in res], axis=1), want_streams)
+
+
+def test_band_rows_cover_neighbourhoods():
+    from paper_2310_09467_b200.shard import band_range, band_rows
+    assert band_rows(4096, 4096, 13, 4, 0) == [(0, 1024), (4082, 4096)]
+    assert band_rows(4096, 4096, 13, 4, 2) == [(2048 - 14, 3072)]
+    assert band_rows(10, 3, 2, 2, 0) == [(0, 5), (7, 10)]
+    for h, w, py, n in [(40, 32, 5, 3), (61, 75, 5, 7), (9, 7, 1, 4)]:
+        for b in range(n):
+            p0, p1 = band_range(h, w, n, b)
+            rows = set()
+            for r0, r1 in band_rows(h, w, py, n, b):
+                rows.update(range(r0, r1))
+            need = set()
+            for p in range(p0, p1):
+                y = p // w
+                need.update(range(max(0, y - py), y + 1))
+            if b == 0 and p1 > p0:
+                need.update(range(max(0, h - 1 - py), h))
+            assert need <= rows

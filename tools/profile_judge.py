@@ -24,6 +24,10 @@ from paper_2310_09467_b200.lfm_synth import generate_array  # noqa: E402
 vol = np.stack([generate_array(p)[0] for p in pick])
 frames = torch.from_numpy(vol).cuda()
 codes = [int(c) for c in os.environ.get("PCBZ_PROFILE_CODES", ",".join(map(str, range(13)))).split(",")]
+seg = int(os.environ.get("PCBZ_PROFILE_SEGMENTS", "0"))
+if seg:
+    from paper_2310_09467_b200 import _lib
+    _lib.load().pcbz_set_segment_override(seg)
 judge = DeviceJudge(vol.shape, (15, 15), codes, temporal=False)
 for _ in range(2):
     judge(frames)
