@@ -130,13 +130,15 @@ int validate_specs(const uint8_t *specs, int k) {
 
 // Work decomposition: segments per (frame, candidate) stream.  Items are
 // pulled dynamically by one CTA per SM; item costs differ by candidate (up to
-// ~1.8x, temporal phase predictors dearest), so the tail shrinks with the
-// item size, while every extra segment adds a histogram flush, a stitch and
-// the finalize pass.  Measured (profiles/r01_notes.md, tools/sweep_segments.py,
-// tools/trace_items.py): the fewest power-of-two segments giving >= 8 waves
-// of items win (C2 1300 pairs and C3: S = 1, no flush / finalize; C4 4096^2
-// x 195 pairs: S = 8; C1: S = 8); items below ~512K pixels lose to per-item
-// overhead.
+// ~1.8x, temporal phase predictors dearest; dispatched dearest first), and
+// every extra segment adds a histogram flush, a stitch and the finalize
+// pass.  Measured (profiles/r01_notes.md, tools/sweep_segments.py,
+// tools/trace_items.py):
+//  * small jobs (even the finest split is under two waves): fill one wave as
+//    exactly as possible (C1, 13 pairs of 2048^2: S = 11, 143 items);
+//  * otherwise the fewest power-of-two segments giving >= 8 waves (C2 1300
+//    pairs and C3: S = 1, no flush / finalize; C4 4096^2 x 195 pairs: S = 8).
+// Items stay >= kMinItemPixels, below which per-item overhead dominates.
 int choose_segments(int64_t npairs, int64_t npix, bool want_hist) {
   (void)want_hist;
   static const int64_t target_waves = [] {
@@ -147,6 +149,16 @@ int choose_segments(int64_t npairs, int64_t npix, bool want_hist) {
   const int64_t nsm = num_sms_cached();
   const int64_t s_min = std::max<int64_t>(1, (npix + kMaxSegPixels - 1) / kMaxSegPixels);
   const int64_t s_cap = std::max<int64_t>(s_min, std::min<int64_t>(4096, npix / kMinItemPixels));
+  if (npairs * s_cap < 2 * nsm) {
+    int64_t best = s_min;
+    double best_eff = -1.0;
+    for (int64_t s = s_min; s <= s_cap; ++s) {
+      const int64_t items = npairs * s;
+      const double eff = (double)items / (double)(((items + nsm - 1) / nsm) * nsm);
+      if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
+    }
+    return (int)best;
+  }
   int64_t s = 1;
   while (s < s_min) s <<= 1;
   while (npairs * s < target_waves * nsm && 2 * s <= s_cap) s <<= 1;

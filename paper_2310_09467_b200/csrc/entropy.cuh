@@ -109,12 +109,15 @@ __device__ __forceinline__ double np_term(double c, double total) {
 
 // `get(bin)` returns the bin count (integer; 0 = empty); all threads of the
 // block (kEntropyThreads) must call this.  `terms` may be null.
+// If occ_ready, the caller has already filled S.occ (bit j of word w = bin
+// 32w + j occupied) and synchronised.
 template <typename Get>
-__device__ double block_entropy(Get get, double total, NpScratch &S, const double *terms) {
+__device__ double block_entropy(Get get, double total, NpScratch &S, const double *terms,
+                                bool occ_ready = false) {
   const int t = threadIdx.x;
   // occupancy bitmap: one warp per 32-bin word (lane j reads bin 32w + j,
   // so the reads are bank-conflict free), a ballot makes the word
-  {
+  if (!occ_ready) {
     const int lane = t & 31;
     for (int w = t >> 5; w < kOccWords; w += kEntropyThreads / 32) {
       const bool occ = total > 0.0 && get(32 * w + lane) != 0;
@@ -168,12 +171,29 @@ __device__ double block_entropy(Get get, double total, NpScratch &S, const doubl
       bits = S.occ[++w];
     }
     for (uint32_t k = beg - idx; k > 0; --k) bits &= bits - 1;  // drop earlier terms
-    auto next_term = [&]() -> double {
+    auto next_bin = [&]() -> int {
       while (!bits) bits = S.occ[++w];
       const int bin = 32 * w + __ffs(bits) - 1;
       bits &= bits - 1;
-      const uint64_t c = get(bin);
-      return (terms && c < (uint64_t)kTermTable) ? __ldg(terms + c) : np_term((double)c, total);
+      return bin;
+    };
+    auto term_of = [&](uint64_t c) -> double {
+      if (!terms) return np_term((double)c, total);
+      const double v = __ldg(terms + (c < (uint64_t)kTermTable ? c : 0));
+      return c < (uint64_t)kTermTable ? v : np_term((double)c, total);
+    };
+    auto next_term = [&]() -> double { return term_of(get(next_bin())); };
+    // eight terms at a time: bin indices first (bitmap walk), then all eight
+    // count reads and table loads in flight together
+    auto next8 = [&](double (&v)[8]) {
+      int b[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) b[q] = next_bin();
+      uint64_t c[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) c[q] = get(b[q]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = term_of(c[q]);
     };
     double res;
     if (len < 8) {
@@ -181,12 +201,13 @@ __device__ double block_entropy(Get get, double total, NpScratch &S, const doubl
       for (uint32_t i = 0; i < len; ++i) res = __dadd_rn(res, next_term());
     } else {
       double r[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) r[q] = next_term();
+      next8(r);
       uint32_t i = 8;
       for (; i < len - (len % 8); i += 8) {
+        double v[8];
+        next8(v);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) r[q] = __dadd_rn(r[q], next_term());
+        for (int q = 0; q < 8; ++q) r[q] = __dadd_rn(r[q], v[q]);
       }
       res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                       __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));

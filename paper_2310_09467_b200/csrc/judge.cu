@@ -61,13 +61,17 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
   }
   __threadfence();
   __syncthreads();
-  // stage saturated u16 copies of the counts in shared memory: 16-byte loads,
-  // eight in flight per thread before any store (the loop is latency bound)
+  // stage saturated u16 copies of the counts in shared memory (16-byte loads,
+  // eight in flight per thread before any store: the loop is latency bound)
+  // and build the occupancy bitmap on the way: 4 bins per thread, 8 lanes
+  // per 32-bin word OR their nibbles together.  192 threads = 24 words per
+  // pass, so each word's eight lanes are in one warp.
   {
     const uint4 *G4 = reinterpret_cast<const uint4 *>(G);
     uint2 *c4 = reinterpret_cast<uint2 *>(c16);
     auto sat = [](uint32_t c) -> uint32_t { return c < 0xFFFFu ? c : 0xFFFFu; };
     constexpr int kUnroll = 8;
+    const int lane = threadIdx.x & 31;
     for (int b0 = threadIdx.x; b0 < 16384; b0 += kEntropyThreads * kUnroll) {
       uint4 v[kUnroll];
 #pragma unroll
@@ -80,6 +84,12 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
         const int b = b0 + u * kEntropyThreads;
         if (b < 16384)
           c4[b] = make_uint2(sat(v[u].x) | (sat(v[u].y) << 16), sat(v[u].z) | (sat(v[u].w) << 16));
+        uint32_t nib = (v[u].x != 0) | (v[u].y != 0) << 1 | (v[u].z != 0) << 2 | (v[u].w != 0) << 3;
+        nib <<= 4 * (lane & 7);
+        nib |= __shfl_xor_sync(0xffffffffu, nib, 1);
+        nib |= __shfl_xor_sync(0xffffffffu, nib, 2);
+        nib |= __shfl_xor_sync(0xffffffffu, nib, 4);
+        if ((lane & 7) == 0 && b < 16384) scr.occ[b >> 3] = nib;
       }
     }
   }
@@ -88,7 +98,7 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
     const uint32_t c = c16[bin];
     return c < 0xFFFFu ? c : __ldcg(G + bin);
   };
-  const double e = block_entropy(get, (double)(2 * P.npix - 1), scr, P.terms);
+  const double e = block_entropy(get, (double)(2 * P.npix - 1), scr, P.terms, true);
   if (threadIdx.x == 0) P.ent[pr.slot] = e;
 }
 

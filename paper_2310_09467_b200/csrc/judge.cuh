@@ -15,7 +15,7 @@ constexpr uint32_t kUnseen = 0x100;            // per-lane "key not seen yet" ma
 constexpr uint32_t kSpill = 0x8000;            // u16 bin spill threshold
 constexpr int kSpillCap = 512;                 // spill list entries per CTA
 constexpr int64_t kMaxSegPixels = 8000000;     // 2 events/pixel / kSpill < kSpillCap
-constexpr int64_t kMinItemPixels = 1 << 19;    // smaller work items lose to per-item overhead
+constexpr int64_t kMinItemPixels = 1 << 18;    // smaller work items lose to per-item overhead
 constexpr int kEntropyThreads = 192;           // all entropy reductions use this shape
 constexpr int kMaxFastPitch = 16;              // fast path: pitch_x <= 16 (template parameter)
 constexpr int kTermTable = 65536;              // precomputed entropy terms per call (entropy.cuh)
