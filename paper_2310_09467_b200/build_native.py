@@ -61,10 +61,15 @@ def _stale(target: Path, deps) -> bool:
 
 
 def build_library(force: bool = False, verbose: bool = False, jobs: int | None = None,
-                  defines: tuple = (), out_dir: Path | None = None, pitches=None) -> Path:
+                  defines: tuple = (), out_dir: Path | None = None, pitches=None,
+                  src_root: Path | None = None) -> Path:
     """Compile and link libpcbz_b200.so.  `defines` / `out_dir` build an
     experimental variant (e.g. ("PCBZ_SWIZZLE=0",)) into its own directory;
+    `src_root` builds from another tree holding paper_2310_09467_b200/csrc and
+    include/ (an A/B baseline exported from git, tools/build_variants.py);
     _lib.load() picks a variant up through the PCBZ_LIB environment variable."""
+    csrc = Path(src_root) / "paper_2310_09467_b200" / "csrc" if src_root else CSRC
+    inc = Path(src_root) / "include" if src_root else ROOT / "include"
     out = Path(out_dir) if out_dir else OUT_DIR
     lib = out / LIB.name
     if not force and not _stale(lib, _deps()):
@@ -75,8 +80,8 @@ def build_library(force: bool = False, verbose: bool = False, jobs: int | None =
 
     def compile_one(unit):
         src, extra, obj = unit
-        cmd = [nvcc, *NVCC_FLAGS, *dflags, *extra, "-I", str(ROOT / "include"), "-c",
-               str(CSRC / src), "-o", str(out / obj)]
+        cmd = [nvcc, *NVCC_FLAGS, *dflags, *extra, "-I", str(inc), "-c",
+               str(csrc / src), "-o", str(out / obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src} {extra}:\n{r.stdout}\n{r.stderr}")

@@ -136,7 +136,7 @@ struct ChainState {
 // 0x7FFF -> 0x8000.
 __device__ __forceinline__ uint32_t chain_event(const ChainState &cs, uint32_t key, uint32_t pred,
                                                 uint32_t &flag) {
-  const uint32_t a = cs.lbase + (key >> 1) * (4u * kJudgeThreads) + ((key & 1u) << 1);
+  const uint32_t a = cs.lbase + key * (2u * kJudgeThreads);
   uint32_t code;
   asm volatile("ld.shared.u16 %0, [%1];" : "=r"(code) : "r"(a));
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(lt_code(pred)));
@@ -366,7 +366,9 @@ __global__ void __launch_bounds__(256) emit_chunks_kernel(const EmitParams P) {
 //
 // dynamic shared memory:
 //   hist   kHistWords            packed u16 counters
-//   last   kLastWords * 192      last-pred tables, word (key>>1)*192 + lane
+//   last   kLastWords * 192      last-pred tables, u16 [key][lane] (a key's
+//                                 192 lanes share one 384-byte row: lanes
+//                                 2j, 2j+1 hit one word, 16 distinct banks)
 //   spill  kSpillCap             spilled bins
 // after the hot loop the last-pred region is reused for the spilled-bin
 // bitmap (words [0, 2048)), first/last per key ([2048, 2560)) and the
@@ -400,7 +402,7 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
   ChainState cs;
   cs.hist = hist_w;
   cs.hbase = (uint32_t)__cvta_generic_to_shared(hist_w);
-  cs.lbase = (uint32_t)__cvta_generic_to_shared(last_w + tid);
+  cs.lbase = (uint32_t)__cvta_generic_to_shared(reinterpret_cast<uint16_t *>(last_w) + tid);
   // first-pred scratch of this CTA, key-major: F[key][lane]
   const uint8_t *Fcta = P.fscratch + (size_t)blockIdx.x * kJudgeThreads * 256;
   cs.F = P.fscratch + (size_t)blockIdx.x * kJudgeThreads * 256 + tid;
@@ -416,7 +418,6 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
   };
   const int64_t w_total = cum_weight(kJudgeThreads);
   const int64_t w_lo = cum_weight(tid), w_hi = cum_weight(tid + 1);
-  uint32_t *Llane = last_w + tid;
 
   for (;;) {
     if (tid == 0) {
@@ -425,7 +426,8 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
     }
     uint4 *h4 = reinterpret_cast<uint4 *>(hist_w);
     for (int i = tid; i < (kHistWords + kDummyWords) / 4; i += kJudgeThreads) h4[i] = make_uint4(0, 0, 0, 0);
-    for (int w = 0; w < kLastWords; ++w) Llane[w * kJudgeThreads] = kUnseenCode | (kUnseenCode << 16);
+    for (int w = tid; w < kLastWords * kJudgeThreads; w += kJudgeThreads)
+      last_w[w] = kUnseenCode | (kUnseenCode << 16);
     __syncthreads();
     const int64_t item = s_item;
     if (item >= nitems) break;
@@ -472,12 +474,11 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
       const int warp = tid >> 5, lane = tid & 31;
       int kf0 = -1, kl0 = -1, kf1 = -1, kl1 = -1;  // keys k = lane and k = 32 + lane
       for (int v = warp, k = 0; v < 256; v += kJudgeThreads / 32, ++k) {
-        const uint32_t *col = last_w + (v >> 1) * kJudgeThreads;
-        const uint32_t sh = (v & 1) << 4;
+        const uint16_t *col = reinterpret_cast<const uint16_t *>(last_w) + v * kJudgeThreads;
         int carry = -1, first = -1;
         for (int b = 0; b < kJudgeThreads; b += 32) {
           const int j = b + lane;
-          const uint32_t code = (col[j] >> sh) & 0xFFFFu;
+          const uint32_t code = col[j];
           const bool seen = code != kUnseenCode;
           const int e = (int)(code >> 7);  // last pred of run j (if seen)
           const int f = Fcta[(size_t)v * kJudgeThreads + j];

@@ -147,13 +147,24 @@ __device__ __forceinline__ void chunk_events(const ChainState &cs, const uint32_
     key[2 * i + 1] = r[i] & 0xFFu;
     prd[2 * i + 1] = r[i] >> 8;
   }
+  // lt_code of both bytes of a residual at once: hi | lo << 16, one multiply
+  // and one mask for the pair (13 * 255 < 2^16, so the halves never carry)
+  uint32_t code[16];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t v2 = __byte_perm(r[i], 0, 0x4041);  // hi | lo << 16
+    const uint32_t cp = (v2 << 7) | ((v2 * kSwizzleMul) & 0x007F007Fu);
+    code[2 * i + 1] = cp & 0xFFFFu;               // lt_code(hi): pred of the lo event
+    if (i < 7) code[2 * i + 2] = cp >> 16;        // lt_code(lo): pred of the next hi event
+  }
+  code[0] = lt_code(prev_lo);
   prev_lo = r[7] & 0xFFu;
   uint32_t last[16];  // last-pred codes (lt_code), kUnseenCode for a first occurrence
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
-    const uint32_t la = cs.lbase + key[e] * 2u + (key[e] >> 1) * (4u * kJudgeThreads - 4u);
+    const uint32_t la = cs.lbase + key[e] * (2u * kJudgeThreads);  // u16 [key][lane]
     last[e] = lds_u16(la);
-    sts_u16(la, lt_code(prd[e]));
+    sts_u16(la, code[e]);
   }
   // the previous chunk's returned words arrived long ago; examining them
   // first frees their registers, so this chunk's atomics return straight

@@ -13,7 +13,25 @@ VARIANTS = {
     "half_lsb_noswz": ("PCBZ_HALF_MSB=0", "PCBZ_SWIZZLE=0"),
 }
 
+def build_from_git(rev: str, name: str):
+    """Baseline for an A/B run: the library as of git revision `rev`."""
+    import subprocess
+    import tarfile
+    import tempfile
+    tmp = Path(tempfile.mkdtemp(prefix="pcbz_ab_"))
+    data = subprocess.run(["git", "-C", str(ROOT), "archive", rev, "paper_2310_09467_b200/csrc",
+                           "include"], check=True, capture_output=True).stdout
+    import io
+    tarfile.open(fileobj=io.BytesIO(data)).extractall(tmp)
+    out = ROOT / "paper_2310_09467_b200" / "_native" / "variants" / name
+    print(name, build_native.build_library(force=True, out_dir=out, pitches={15}, src_root=tmp),
+          flush=True)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) == 4 and sys.argv[1] == "--git":   # --git REV NAME
+        build_from_git(sys.argv[2], sys.argv[3])
+        sys.exit(0)
     names = sys.argv[1:] or list(VARIANTS)
     for n in names:
         out = ROOT / "paper_2310_09467_b200" / "_native" / "variants" / n
