@@ -143,6 +143,86 @@ def write_container(width: int, height: int, pitch_x: int, pitch_y: int, block_s
     return b"".join(parts)
 
 
+class ContainerWriter:
+    """Incremental writer of the same bytes write_container produces, for
+    series too long to hold in memory.  Payloads are
+    appended as frames complete; the header (frame count, temporal flag) and
+    the per-frame records (compressed block sizes) are written at close().
+    With a known frame count and a seekable output, header and record space
+    is reserved up front and patched in place; otherwise payloads are spooled
+    to a temporary file and copied behind the header at close()."""
+
+    def __init__(self, out, width: int, height: int, pitch_x: int, pitch_y: int, block_size: int,
+                 nframes: int | None = None):
+        import tempfile
+        if min(width, height, pitch_x, pitch_y, block_size) < 1:
+            raise ValueError("non-positive container field")
+        self.out = out
+        self.dims = (width, height, pitch_x, pitch_y, block_size)
+        self.blocks_per_frame = BlockPlan.for_length(2 * width * height, block_size).block_count
+        self.nframes = nframes
+        self.records = []
+        self.temporal = False
+        seekable = getattr(out, "seekable", lambda: False)()
+        if nframes is not None and nframes >= 1 and seekable:
+            self.base = out.tell()
+            self.reserved = HEADER_SIZE + nframes * (_REC.size + 8 * self.blocks_per_frame)
+            out.write(b"\0" * self.reserved)
+            self.spool = None
+        else:
+            self.spool = tempfile.TemporaryFile()
+        self.closed = False
+
+    def add_frame(self, spec, payloads) -> None:
+        if self.closed:
+            raise ValueError("container writer is closed")
+        if not self.records and spec.temporal:
+            raise ValueError("frame 0 must not use a temporal predictor")
+        if self.nframes is not None and len(self.records) >= self.nframes:
+            raise ValueError(f"more than the announced {self.nframes} frames")
+        if len(payloads) != self.blocks_per_frame:
+            raise ValueError(f"frame has {len(payloads)} blocks, expected {self.blocks_per_frame}")
+        dst = self.spool if self.spool is not None else self.out
+        for p in payloads:
+            dst.write(p)
+        self.records.append((spec.to_byte(), tuple(len(p) for p in payloads)))
+        self.temporal |= bool(spec.temporal)
+
+    def _head_and_records(self) -> bytes:
+        w, h, px, py, bs = self.dims
+        parts = [_HEAD.pack(MAGIC, VERSION, FLAG_TEMPORAL if self.temporal else 0, BIT_DEPTH, 0,
+                            w, h, len(self.records), px, py, bs)]
+        for code, sizes in self.records:
+            parts.append(_REC.pack(code, len(sizes)))
+            parts.append(struct.pack(f"<{len(sizes)}Q", *sizes))
+        return b"".join(parts)
+
+    def close(self) -> int:
+        """Finish the container; returns its size in bytes."""
+        import shutil
+        if self.closed:
+            raise ValueError("container writer is closed")
+        if not self.records:
+            raise ValueError("container must hold at least one frame")
+        if self.nframes is not None and len(self.records) != self.nframes:
+            raise ValueError(f"{len(self.records)} frames written, {self.nframes} announced")
+        head = self._head_and_records()
+        payload_bytes = sum(sum(sz) for _, sz in self.records)
+        if self.spool is None:
+            assert len(head) == self.reserved
+            end = self.out.tell()
+            self.out.seek(self.base)
+            self.out.write(head)
+            self.out.seek(end)
+        else:
+            self.out.write(head)
+            self.spool.seek(0)
+            shutil.copyfileobj(self.spool, self.out, 16 << 20)
+            self.spool.close()
+        self.closed = True
+        return len(head) + payload_bytes
+
+
 def read_container(data):
     """Parse and validate (container.py:109-177); returns (header, records, payloads)."""
     buf = memoryview(data)

@@ -195,8 +195,16 @@ __device__ __forceinline__ void chunk_events(const ChainState &cs, const uint32_
 // One lane's run of `nch` chunks starting at pixel a (a % 8 == 0).  The next
 // chunk's rows are issued at the top of each iteration (pinned loads) and
 // consumed one iteration later.
+#ifndef PCBZ_LANE_INLINE
+#define PCBZ_LANE_INLINE 0
+#endif
+#if PCBZ_LANE_INLINE
+#define PCBZ_LANE_ATTR __forceinline__
+#else
+#define PCBZ_LANE_ATTR __noinline__
+#endif
 template <int PX, int ID, bool TEMP>
-__device__ __noinline__ void lane_fast(const uint16_t *__restrict__ src,
+__device__ PCBZ_LANE_ATTR void lane_fast(const uint16_t *__restrict__ src,
                                        const uint16_t *__restrict__ prv, int W, int py,
                                        int64_t npix, int64_t a, int64_t nch, const PredCfg cfg,
                                        const ChainState cs) {

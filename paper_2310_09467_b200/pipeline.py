@@ -160,6 +160,102 @@ def compress_stack(stack: FrameStack, opts: CompressOptions | None = None) -> by
     return compress_stack_detailed(stack, opts).data
 
 
+@dataclass
+class StreamResult:
+    frames: int
+    container_bytes: int
+    specs: list
+    select_seconds: float = 0.0
+    encode_wait_seconds: float = 0.0
+
+
+def compress_stream(frames, geometry: LensletGeometry, out, opts: CompressOptions | None = None,
+                    nframes: int | None = None, chunk_frames: int = GPU_CHUNK_FRAMES,
+                    max_inflight_chunks: int = 3, judge_fn=None) -> StreamResult:
+    """Bounded-memory compress_stack for long series:
+    `frames` is any iterable of 2-D uint16 arrays (or Frames) of one shape;
+    the container goes to the binary file `out` and is byte-identical to
+    compress_stack on the same frames (reference pipeline.py:76-113).
+    Chunks of `chunk_frames` frames are judged and emitted by one device call
+    (the previous chunk's last frame is the temporal halo); their bzip2
+    blocks are coded on `opts.workers` threads while the next chunks are
+    read and judged, with at most `max_inflight_chunks` chunks of streams
+    alive.  `judge_fn(chunk, halo, geo, codes, temporal) -> (ent, sel,
+    streams)` defaults to the device judge (tests inject the oracle)."""
+    from .codec import ContainerWriter
+    opts = opts or CompressOptions()
+    forced = opts.forced
+    codes = None if forced is not None else candidate_codes(opts)
+    if judge_fn is None:
+        def judge_fn(chunk, halo, geo, cands, temporal):
+            return judge_volume(chunk, geo, cands, temporal, halo=halo)
+    pool = ThreadPoolExecutor(max(1, opts.workers))
+    writer = None
+    specs = []
+    pending = []          # [(spec, [futures])] in frame order
+    halo = None
+    select_s = wait_s = 0.0
+    nseen = 0
+
+    def drain(keep_chunks: int):
+        nonlocal wait_s
+        while len(pending) > keep_chunks:
+            t0 = time.perf_counter()
+            for spec, futs in pending.pop(0):
+                writer.add_frame(spec, [f.result() for f in futs])
+            wait_s += time.perf_counter() - t0
+
+    def run_chunk(buf):
+        nonlocal halo, select_s
+        chunk = np.ascontiguousarray(np.stack(buf))
+        h = halo if opts.temporal else None
+        t0 = time.perf_counter()
+        if forced is None:
+            _, sel, streams = judge_fn(chunk, h, geometry, codes, opts.temporal)
+        else:
+            first = nseen - len(buf)
+            sel = np.array([forced.to_byte() if (first + i > 0 and opts.temporal) else forced.intra_id
+                            for i in range(len(buf))], np.uint8)
+            streams = emit_volume(chunk, geometry, sel, h)
+        select_s += time.perf_counter() - t0
+        halo = chunk[-1].copy()
+        entry = []
+        for i in range(len(buf)):
+            spec = PredictorSpec.from_byte(int(sel[i]))
+            specs.append(spec)
+            entry.append((spec, [pool.submit(bz2_block, blk)
+                                 for blk in split_blocks(streams[i], opts.block_size)]))
+        pending.append(entry)
+        drain(max_inflight_chunks - 1)
+
+    try:
+        buf = []
+        for fr in frames:
+            a = fr.samples if isinstance(fr, Frame) else np.asarray(fr)
+            if a.dtype != np.uint16 or a.ndim != 2:
+                raise ValueError("frames must be 2-D uint16 arrays")
+            if writer is None:
+                H, W = a.shape
+                writer = ContainerWriter(out, W, H, geometry.pitch_x, geometry.pitch_y,
+                                         opts.block_size, nframes)
+            elif a.shape != (H, W):
+                raise ValueError(f"frame {nseen} has shape {a.shape}, expected {(H, W)}")
+            buf.append(a)
+            nseen += 1
+            if len(buf) == chunk_frames:
+                run_chunk(buf)
+                buf = []
+        if buf:
+            run_chunk(buf)
+        if writer is None:
+            raise ValueError("container must hold at least one frame")
+        drain(0)
+        size = writer.close()
+    finally:
+        pool.shutdown(wait=True)
+    return StreamResult(nseen, size, specs, select_s, wait_s)
+
+
 def decompress_stack(data, workers: int = 1) -> FrameStack:
     """Reference pipeline.py:121-139: bzip2 on host threads, inverse
     prediction and temporal undelta on the device."""

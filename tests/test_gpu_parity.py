@@ -401,3 +401,23 @@ def test_band_sharded_large_frame_vs_oracle():
         assert_entropy(got, want)
     assert sel[0] == best
     assert streams[0].tobytes() == oracle.emit_stream(img[0], None, best, 13, 13)
+
+
+@pytest.mark.parametrize("forced", [None, PredictorSpec(True, 6)])
+def test_compress_stream_equals_compress_stack(forced):
+    """Streaming driver on the device judge (chunks of 8, halo across chunks)
+    == compress_stack == the oracle, byte for byte."""
+    import io
+    from paper_2310_09467_b200.pipeline import compress_stream
+    p = SynthParams(96, 80, 15, 15, mode="smooth_lenslet", noise_sigma=20.0, photon_scale=0.05,
+                    frames=19, drift=1.0, seed=12)
+    vol = generate_array(p)
+    geo = LensletGeometry(15, 15)
+    opts = CompressOptions(workers=4, forced=forced)
+    out = io.BytesIO()
+    res = compress_stream((f for f in vol), geo, out, opts, nframes=19, chunk_frames=8)
+    stack = FrameStack(tuple(Frame(f, geo) for f in vol))
+    assert out.getvalue() == compress_stack(stack, opts)
+    want, _ = oracle.compress_stack(vol, 15, 15, forced=None if forced is None else forced.to_byte())
+    assert sha(out.getvalue()) == sha(want)
+    assert res.frames == 19

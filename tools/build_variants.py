@@ -11,6 +11,8 @@ VARIANTS = {
     "half_lsb": ("PCBZ_HALF_MSB=0",),
     "half_msb": ("PCBZ_HALF_MSB=1",),
     "half_lsb_noswz": ("PCBZ_HALF_MSB=0", "PCBZ_SWIZZLE=0"),
+    "base": (),
+    "inline": ("PCBZ_LANE_INLINE=1",),
 }
 
 def build_from_git(rev: str, name: str):
