@@ -232,12 +232,12 @@ __device__ PCBZ_LANE_ATTR void lane_fast(const uint16_t *__restrict__ src,
     h.S1 = row(offs - 8, kTS && x0 >= 8 && y >= py);
     h.S2 = row(offs - 16, kTS && PX > 8 && x0 >= 16 && y >= py);
   }
-#ifndef PCBZ_PIPELINE
-#define PCBZ_PIPELINE 0
-#endif
-  if constexpr (!PCBZ_PIPELINE) {
-    // plain form: iteration c issues the rows of chunk c+1, then computes the
-    // residuals and events of chunk c
+  {
+    // iteration c issues the rows of chunk c+1, then computes the residuals
+    // and events of chunk c.  Measured alternatives, all slower on C2/C3
+    // (profiles/r01_notes.md): rows two chunks ahead, a software pipeline
+    // (residuals of c+1 beside the events of c), two chunks per iteration
+    // with ping-pong pending atomics, lane_fast inlined into the kernel.
     ChunkRows cur = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, y, x0);
     Pending pd;
 #pragma unroll
@@ -264,57 +264,6 @@ __device__ PCBZ_LANE_ATTR void lane_fast(const uint16_t *__restrict__ src,
     settle_pending(cs, pd);
     return;
   }
-  // Software pipeline: iteration c issues the rows of chunk c+2, computes the
-  // residuals of chunk c+1 and runs the events of chunk c -- two independent
-  // dependency chains the scheduler can interleave.
-  auto step = [&](int &yy, int &xx) {
-    xx += 8;
-    if (xx == W) { xx = 0; ++yy; }
-  };
-  auto advance = [&](const uint4 &X, const uint4 &T1, const uint4 &TS, bool row_start) {
-    if (row_start) {
-      h.X1 = h.X2 = h.T1 = h.S1 = h.S2 = make_uint4(0, 0, 0, 0);  // left neighbours are 0
-    } else {
-      h.X2 = h.X1; h.X1 = X; h.T1 = T1; h.S2 = h.S1; h.S1 = TS;
-    }
-  };
-  int y1 = y, x1 = x0;
-  step(y1, x1);  // chunk c+1
-  uint32_t r_cur[8];
-  ChunkRows raw_next;
-  {
-    const ChunkRows raw0 = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, y, x0);
-    raw_next = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, nch > 1 ? y1 : y, nch > 1 ? x1 : x0);
-    uint4 X, T1, TS;
-    source_rows<TEMP, kT1, kTS>(raw0, X, T1, TS);
-    chunk_residuals8<PX, ID>(X, T1, TS, h, r_cur);
-    advance(X, T1, TS, x1 == 0);
-  }
-  Pending pd;
-#pragma unroll
-  for (int e = 0; e < 16; ++e) { pd.old[e] = 0; pd.word[e] = ~0u; }
-  for (int64_t c = 0; c < nch; ++c) {
-    int y2 = y1, x2 = x1;
-    step(y2, x2);  // chunk c+2
-    const bool has2 = c + 2 < nch;
-    const ChunkRows raw2 = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, has2 ? y2 : y,
-                                                        has2 ? x2 : x0);
-    // residuals of chunk c+1 (past the run's end they are computed on valid,
-    // clamped rows and never used)
-    uint32_t r_next[8];
-    {
-      uint4 X, T1, TS;
-      source_rows<TEMP, kT1, kTS>(raw_next, X, T1, TS);
-      chunk_residuals8<PX, ID>(X, T1, TS, h, r_next);
-      advance(X, T1, TS, x2 == 0);
-    }
-    chunk_events(cs, r_cur, prev_lo, pd);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) r_cur[i] = r_next[i];
-    raw_next = raw2;
-    x1 = x2; y1 = y2;
-  }
-  settle_pending(cs, pd);
 }
 
 template <int PX, bool TEMP, int... IDs>
