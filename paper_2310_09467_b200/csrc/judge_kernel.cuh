@@ -366,9 +366,11 @@ __global__ void __launch_bounds__(256) emit_chunks_kernel(const EmitParams P) {
 //
 // dynamic shared memory:
 //   hist   kHistWords            packed u16 counters
-//   last   kLastWords * 192      last-pred tables, u16 [key][lane] (a key's
-//                                 192 lanes share one 384-byte row: lanes
-//                                 2j, 2j+1 hit one word, 16 distinct banks)
+//   last   kLastWords * 192      last-pred tables: u16 entries, one 384-byte
+//                                 row per key (lane_slot below); lane j of
+//                                 warps 2w and 2w+1 share a word, so a warp's
+//                                 32 lanes hit 32 distinct banks whatever
+//                                 their keys, and the address is one IMAD
 //   spill  kSpillCap             spilled bins
 // after the hot loop the last-pred region is reused for the spilled-bin
 // bitmap (words [0, 2048)), first/last per key ([2048, 2560)) and the
@@ -384,6 +386,12 @@ __device__ __forceinline__ uint32_t smid() {
   uint32_t s;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
   return s;
+}
+
+// u16 slot of lane t within a key's row of the last-pred tables: word
+// 32 * (warp / 2) + (t % 32), half warp % 2
+__device__ __forceinline__ uint32_t lane_slot(uint32_t t) {
+  return 2u * (t & 31u) + 64u * (t >> 6) + ((t >> 5) & 1u);
 }
 
 template <int PX>
@@ -402,7 +410,7 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
   ChainState cs;
   cs.hist = hist_w;
   cs.hbase = (uint32_t)__cvta_generic_to_shared(hist_w);
-  cs.lbase = (uint32_t)__cvta_generic_to_shared(reinterpret_cast<uint16_t *>(last_w) + tid);
+  cs.lbase = (uint32_t)__cvta_generic_to_shared(reinterpret_cast<uint16_t *>(last_w) + lane_slot(tid));
   // first-pred scratch of this CTA, key-major: F[key][lane]
   const uint8_t *Fcta = P.fscratch + (size_t)blockIdx.x * kJudgeThreads * 256;
   cs.F = P.fscratch + (size_t)blockIdx.x * kJudgeThreads * 256 + tid;
@@ -475,10 +483,11 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
       int kf0 = -1, kl0 = -1, kf1 = -1, kl1 = -1;  // keys k = lane and k = 32 + lane
       for (int v = warp, k = 0; v < 256; v += kJudgeThreads / 32, ++k) {
         const uint16_t *col = reinterpret_cast<const uint16_t *>(last_w) + v * kJudgeThreads;
+        // col[lane_slot(j)] = entry of lane j
         int carry = -1, first = -1;
         for (int b = 0; b < kJudgeThreads; b += 32) {
           const int j = b + lane;
-          const uint32_t code = col[j];
+          const uint32_t code = col[lane_slot(j)];
           const bool seen = code != kUnseenCode;
           const int e = (int)(code >> 7);  // last pred of run j (if seen)
           const int f = Fcta[(size_t)v * kJudgeThreads + j];
