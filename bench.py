@@ -378,6 +378,7 @@ def run_gpu(args, wl: Workload):
                  for f in range(nloc)) * (2 * H * W)
     ev_rate = events / (hist_ms * 1e-3)
     roof = profile_json("smem_roof.json")
+    lsu_pct = tf.get("l1tex_lsu_data_pipe_pct_of_peak") if (tf and wl.name == "c2") else None
     res = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -394,7 +395,10 @@ def run_gpu(args, wl: Workload):
             "achieved": ev_rate, "unit": "pair increments/s",
             "peak": roof["atoms_random_lane_ops_per_s"] if roof else None,
             "frac": ev_rate / roof["atoms_random_lane_ops_per_s"] if roof else None,
-            "peak_source": "profiles/smem_roof.json (microbenchmark, random 32-bit words)" if roof else None},
+            "peak_source": "profiles/smem_roof.json (microbenchmark, random 32-bit words)" if roof else None,
+            "smem_data_pipe_pct_of_peak_ncu": lsu_pct,
+            "smem_data_pipe_source": ("profiles/latest_hist_traffic.json (ncu --set full of this kernel in this "
+                                      "command)") if lsu_pct is not None else None},
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": raw_bytes_local,
                 "d2h_bytes_per_step": stream_h.nbytes + ent_h.nbytes + sel_h.nbytes,
                 "api": "paper_2310_09467_b200.pipeline.judge_volume (pcbz_judge_host)",
