@@ -10,6 +10,7 @@ function of (stack, options) and identical to the reference's.
 """
 from __future__ import annotations
 
+import bz2
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
@@ -17,8 +18,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .codec import (DEFAULT_BLOCK_SIZE, BlockPlan, CompressedBlocks, CorruptContainerError,
-                    bz2_block, decompress_blocks, read_container, split_blocks, write_container)
+from .codec import (DEFAULT_BLOCK_SIZE, BlockDecodeError, BlockPlan, CompressedBlocks,
+                    CorruptContainerError, bz2_block, read_container, split_blocks, write_container)
 from .core import Frame, FrameStack, LensletGeometry, PredictorSpec, unpack_symbols
 from .criterion import EntropyReport, default_candidates
 
@@ -262,11 +263,33 @@ def decompress_stack(data, workers: int = 1) -> FrameStack:
     header, records, payloads = read_container(data)
     H, W = header.height, header.width
     res = np.empty((header.frame_count, H, W), np.uint16)
-    for i, rec in enumerate(records):
-        blocks = CompressedBlocks(BlockPlan(header.block_size, len(rec.block_sizes)),
-                                  tuple(bytes(p) for p in payloads[i]))
+    # every (frame, block) payload of the container on one pool (the
+    # reference decodes frame by frame, pipeline.py:127-133, which leaves all
+    # but block_count threads idle); errors are reported for the first bad
+    # frame in frame order, as the sequential loop would
+    jobs = [(j, bytes(p)) for i in range(len(records)) for j, p in enumerate(payloads[i])]
+
+    def decode(job):
+        j, payload = job
         try:
-            res[i] = unpack_symbols(decompress_blocks(blocks, workers), W, H)
+            return bz2.decompress(payload), None
+        except (OSError, EOFError, ValueError) as exc:   # codec.decompress_blocks' mapping
+            return None, BlockDecodeError(j, str(exc))
+
+    if workers > 1 and len(jobs) > 1:
+        with ThreadPoolExecutor(workers) as pool:
+            decoded = list(pool.map(decode, jobs))
+    else:
+        decoded = [decode(j) for j in jobs]
+    k = 0
+    for i, rec in enumerate(records):
+        parts = decoded[k:k + len(payloads[i])]
+        k += len(payloads[i])
+        for _, exc in parts:    # undecodable payload: BlockDecodeError, unwrapped (blocks.py:87-92)
+            if exc is not None:
+                raise exc
+        try:
+            res[i] = unpack_symbols(b"".join(p for p, _ in parts), W, H)
         except ValueError as exc:
             raise CorruptContainerError(f"frame {i}: {exc}") from exc
     sel = np.array([r.spec.to_byte() for r in records], np.uint8)
