@@ -167,6 +167,27 @@ PCBZ_API int pcbz_emit_band_device(const uint16_t *d_frames, const uint16_t *d_h
                           int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *d_sel,
                           int band, int nbands, uint8_t *d_stream_out, void *stream);
 
+/* bzip2 back end on the GPU: the reference codes every PCBZ block with
+ * bz2.compress(chunk, 9) on host threads (blocks.py:73-81, libbzip2 1.0.8).
+ * These code njobs independent inputs, byte-exact with that call.
+ *   in / d_in         the inputs back to back; in_off[njobs + 1] (host array)
+ *                     gives job j = [in_off[j], in_off[j+1])
+ *   out / d_out       receives job j's bzip2 stream at out_start[j],
+ *                     out_len[j] bytes (4-byte aligned starts); capacity
+ *                     out_cap >= pcbz_bzip2_bound(in_off, njobs)
+ *   host_needed[j]    1: job j holds an exactly periodic block, whose
+ *                     rotation ties libbzip2 breaks by implementation-defined
+ *                     quicksort order -- the caller codes it with libbzip2
+ *                     (out_len[j] = 0)
+ * Synchronous.  A batch is limited to < 2^31 bytes after RLE1. */
+PCBZ_API size_t pcbz_bzip2_bound(const int64_t *in_off, int njobs);
+PCBZ_API int pcbz_bzip2_host(const uint8_t *in, const int64_t *in_off, int njobs, uint8_t *out,
+                    size_t out_cap, int64_t *out_start, int64_t *out_len, uint8_t *host_needed);
+PCBZ_API int pcbz_bzip2_device(const uint8_t *d_in, const int64_t *in_off, int njobs, uint8_t *d_out,
+                      size_t out_cap, int64_t *out_start, int64_t *out_len, uint8_t *host_needed,
+                      void *stream);
+PCBZ_API const char *pcbz_bzip2_last_error(void);
+
 /* Testing hook: force the number of segments each (frame, candidate) stream
  * is split into (0 = automatic).  Outputs must not depend on it. */
 PCBZ_API int pcbz_set_segment_override(int segments);

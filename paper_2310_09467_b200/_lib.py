@@ -59,6 +59,10 @@ SIGNATURES = {
                                          _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp]),
     "pcbz_emit_band_device": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp,
                                        _c_int, _c_int, _vp, _vp]),
+    "pcbz_bzip2_bound": (_c_size, [_vp, _c_int]),
+    "pcbz_bzip2_host": (_c_int, [_vp, _vp, _c_int, _vp, _c_size, _vp, _vp, _vp]),
+    "pcbz_bzip2_device": (_c_int, [_vp, _vp, _c_int, _vp, _c_size, _vp, _vp, _vp, _vp]),
+    "pcbz_bzip2_last_error": (ctypes.c_char_p, []),
     "pcbz_set_segment_override": (_c_int, [_c_int]),
     "pcbz_set_profiling": (_c_int, [_c_int]),
     "pcbz_set_item_trace": (_c_int, [_c_int]),

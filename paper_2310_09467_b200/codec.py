@@ -80,6 +80,49 @@ def bz2_block(chunk) -> bytes:
     return bz2.compress(chunk, BZ2_LEVEL)
 
 
+#: input bytes per pcbz_bzip2_host call (the device coder takes < 2^31 bytes after RLE1)
+DEVICE_BZ2_BATCH = 1 << 30
+
+
+def bz2_blocks_device(chunks) -> list:
+    """bz2.compress(chunk, 9) of every chunk, coded on the GPU by
+    csrc/bzip2.cu (pcbz_bzip2_host), byte-exact with libbzip2 1.0.8.  A chunk
+    holding an exactly periodic block -- whose rotation ties libbzip2 breaks
+    in an implementation-defined order -- is coded by the host libbzip2."""
+    import numpy as np
+
+    from . import _lib
+    lib = _lib.load()
+    chunks = [memoryview(c).cast("B") for c in chunks]
+    out_all, i = [], 0
+    while i < len(chunks):
+        j, size = i, 0
+        while j < len(chunks) and (j == i or size + len(chunks[j]) <= DEVICE_BZ2_BATCH):
+            size += len(chunks[j])
+            j += 1
+        batch = chunks[i:j]
+        off = np.zeros(len(batch) + 1, np.int64)
+        off[1:] = np.cumsum([len(c) for c in batch])
+        buf = np.empty(max(int(off[-1]), 1), np.uint8)
+        for k, c in enumerate(batch):
+            buf[off[k]:off[k + 1]] = np.frombuffer(c, np.uint8)
+        cap = lib.pcbz_bzip2_bound(off.ctypes.data, len(batch))
+        out = np.empty(max(cap, 1), np.uint8)
+        start = np.zeros(len(batch), np.int64)
+        length = np.zeros(len(batch), np.int64)
+        host = np.zeros(len(batch), np.uint8)
+        rc = lib.pcbz_bzip2_host(buf.ctypes.data, off.ctypes.data, len(batch), out.ctypes.data, cap,
+                                 start.ctypes.data, length.ctypes.data, host.ctypes.data)
+        if rc:
+            msg = lib.pcbz_bzip2_last_error().decode(errors="replace")
+            raise (ValueError if rc == _lib.PCBZ_E_INVALID else RuntimeError)(msg)
+        for k, c in enumerate(batch):
+            out_all.append(bz2.compress(c, BZ2_LEVEL) if host[k]
+                           else out[start[k]:start[k] + length[k]].tobytes())
+        i = j
+    return out_all
+
+
 def compress_blocks(stream, block_size: int = DEFAULT_BLOCK_SIZE, workers: int = 1) -> CompressedBlocks:
     """blocks.py:73-81: every block is an independent level-9 bzip2 stream."""
     chunks = split_blocks(stream, block_size)

@@ -1,0 +1,923 @@
+// bzip2.cu -- libbzip2 1.0.8 level-9 block coder on the GPU, byte-exact with
+// bz2.compress(chunk, 9): the back end the reference runs on host threads
+// (pkg/src/pcbz/blocks.py:73-81 -> stdlib bz2 -> libbz2 1.0.8, SURVEY §8(f)
+// rank 4).  The algorithm is restated in oracle/bzip2_ref.py (pinned against
+// libbz2 by tests/test_bzip2_ref.py); stages follow it.
+//
+// Many independent inputs ("jobs", one per PCBZ block) are coded together:
+//   A  rle1_kernel       one thread per job: bzlib.c's RLE1 state machine,
+//                        block split at nblockMAX, block CRC, symbol map
+//   B  prefix doubling   cyclic-rotation sort of every block at once: CUB
+//                        radix sorts of (group, partner rank) keys over the
+//                        shrinking set of unresolved groups
+//   C  mtf_kernel        one thread per block: BWT column, MTF, RUNA/RUNB
+//   D  tables_kernel     one CTA per block: initial tables, four refinement
+//                        passes (parallel over 50-symbol groups), huffman.c
+//                        code lengths, selector MTF, bit counts
+//   E  emit_kernel       one CTA per block: header fields, then every code at
+//                        its scanned bit offset (atomicOr into the job's
+//                        big-endian word stream); frame_kernel adds 'BZh9'
+//                        and the end-of-stream marker + combined CRC
+// A block whose rotations tie (an exactly periodic block) flags its job for
+// the host libbz2: libbz2 orders equal rotations by its quicksort
+// refinements, which are not restated.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pcbz_b200.h"
+
+namespace pcbz {
+namespace bz {
+
+constexpr int kBlockMax = 899981;          // 100000 * 9 - 19 (bzlib.c nblockMAX)
+constexpr int kMaxAlpha = 258;
+constexpr int kMaxGroups = 6;
+constexpr int kGroupSize = 50;
+constexpr int kMaxCodeLen = 17;
+constexpr int kTableThreads = 256;
+constexpr int kEmitThreads = 256;
+constexpr int kEmitItems = 8;
+
+struct Job {
+  int64_t in_off, in_len;
+  int64_t rle_off;        // RLE1 output region
+  int32_t block0;         // first block slot
+  int32_t nblocks;        // filled by stage A
+};
+
+struct Block {
+  int64_t rle_off;        // absolute offset of the block's bytes in the RLE buffer
+  int32_t n;              // block bytes
+  int32_t job;
+  uint32_t crc;
+  uint32_t in_use[8];
+  uint32_t base;          // first global element index (stage B)
+  int32_t orig, tie;
+  int64_t mtf_off;        // into mtfv (room for n + 1 values)
+  int64_t sel_off;        // into selectors (room for (n + 1 + 49) / 50)
+  int32_t n_mtf, n_groups, n_sel, n_in_use;
+  int64_t hdr_bits, data_bits;
+  int64_t bit_off;        // absolute bit position in the output word stream
+};
+
+__device__ __forceinline__ uint32_t crc_entry(uint32_t i) {
+  uint32_t c = i << 24;
+  for (int k = 0; k < 8; ++k) c = (c & 0x80000000u) ? (c << 1) ^ 0x04C11DB7u : (c << 1);
+  return c;
+}
+
+// ---------------------------------------------------------------------------
+// A: RLE1 + block split (bzlib.c ADD_CHAR_TO_BLOCK, add_pair_to_block,
+// copy_input_until_stop, handle_compress as driven by bz2.compress)
+// ---------------------------------------------------------------------------
+
+__global__ void rle1_kernel(const uint8_t *__restrict__ in, Job *jobs, int njobs,
+                            uint8_t *__restrict__ rle, Block *blocks) {
+  __shared__ uint32_t tab[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = crc_entry(i);
+  __syncthreads();
+  const int jid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (jid >= njobs) return;
+  Job &J = jobs[jid];
+  const uint8_t *src = in + J.in_off;
+  uint8_t *dst = rle + J.rle_off;
+  int64_t pos = 0, bstart = 0;
+  int nb = 0;
+  uint32_t crc = 0xFFFFFFFFu;
+  uint32_t used[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  uint32_t ch = 256, run = 0;
+  auto crc_up = [&](uint32_t c) { crc = (crc << 8) ^ tab[(crc >> 24) ^ c]; };
+  auto mark = [&](uint32_t c) { used[c >> 5] |= 1u << (c & 31); };
+  auto close_block = [&]() {
+    Block &B = blocks[J.block0 + nb];
+    B.rle_off = J.rle_off + bstart;
+    B.n = (int32_t)(pos - bstart);
+    B.job = jid;
+    B.crc = ~crc;
+    for (int k = 0; k < 8; ++k) { B.in_use[k] = used[k]; used[k] = 0; }
+    B.tie = 0;
+    ++nb;
+    bstart = pos;
+    crc = 0xFFFFFFFFu;
+  };
+  auto add_pair = [&]() {
+    for (uint32_t i = 0; i < run; ++i) crc_up(ch);
+    mark(ch);
+    if (run <= 3) {
+      for (uint32_t i = 0; i < run; ++i) dst[pos++] = (uint8_t)ch;
+    } else {
+      mark(run - 4);
+      for (int i = 0; i < 4; ++i) dst[pos++] = (uint8_t)ch;
+      dst[pos++] = (uint8_t)(run - 4);
+    }
+  };
+  for (int64_t k = 0; k < J.in_len; ++k) {
+    const uint32_t c = __ldg(src + k);
+    if (pos - bstart >= kBlockMax) close_block();
+    if (c != ch && run == 1) {
+      crc_up(ch);
+      mark(ch);
+      dst[pos++] = (uint8_t)ch;
+      ch = c;
+    } else if (c != ch || run == 255) {
+      if (ch < 256) add_pair();
+      ch = c;
+      run = 1;
+    } else {
+      ++run;
+    }
+  }
+  if (pos - bstart >= kBlockMax) close_block();
+  if (ch < 256) add_pair();
+  if (pos > bstart) close_block();
+  J.nblocks = nb;
+}
+
+// ---------------------------------------------------------------------------
+// B: cyclic rotation sort by prefix doubling
+// ---------------------------------------------------------------------------
+
+__global__ void fill_block_of_kernel(const Block *blocks, const int *ids, uint32_t *block_of) {
+  const Block &B = blocks[ids[blockIdx.x]];
+  for (int i = threadIdx.x; i < B.n; i += blockDim.x) block_of[B.base + i] = (uint32_t)ids[blockIdx.x];
+}
+
+__global__ void init_keys_kernel(const Block *blocks, const uint32_t *block_of, const uint8_t *rle,
+                                 uint32_t N, uint64_t *keys, uint32_t *vals) {
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < N; g += gridDim.x * blockDim.x) {
+    const uint32_t b = block_of[g];
+    const Block &B = blocks[b];
+    const uint32_t i = g - B.base, n = (uint32_t)B.n;
+    const uint8_t *d = rle + B.rle_off;
+    uint32_t k = 0;
+    for (int t = 0; t < 4; ++t) k = (k << 8) | d[(i + t) % n];
+    keys[g] = ((uint64_t)b << 32) | k;
+    vals[g] = g;
+  }
+}
+
+__global__ void heads_kernel(const uint64_t *keys, uint32_t m, uint8_t *hd) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x)
+    hd[k] = (k == 0 || keys[k] != keys[k - 1]) ? 1 : 0;
+}
+
+// gs[k] = (hd[k] ? pos(k) : 0), pos = U[k] (or k for the first round)
+__global__ void head_pos_kernel(const uint8_t *hd, const uint32_t *U, uint32_t m, uint32_t *gs) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x)
+    gs[k] = hd[k] ? (U ? U[k] : k) : 0u;
+}
+
+struct MaxOp {
+  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
+};
+
+// after a sort of m elements (sorted vals, their slots U[k] or k): write the
+// suffix array, the new ranks and the unresolved flags; groups of blocks
+// whose compared prefix (plen) already covers the whole block are ties
+__global__ void settle_kernel(const uint32_t *vals, const uint32_t *U, uint32_t m, const uint8_t *hd,
+                              const uint32_t *gs, uint32_t *sa, uint32_t *rank, const uint32_t *block_of,
+                              Block *blocks, uint64_t plen, uint8_t *unres) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) {
+    const uint32_t g = vals[k];
+    const uint32_t slot = U ? U[k] : k;
+    sa[slot] = g;
+    rank[g] = gs[k];
+    const bool open = !hd[k] || (k + 1 < m && !hd[k + 1]);
+    uint8_t u = 0;
+    if (open) {
+      const uint32_t b = block_of[g];
+      if (plen >= (uint64_t)blocks[b].n) blocks[b].tie = 1;  // equal full rotations
+      else u = 1;
+    }
+    unres[k] = u;
+  }
+}
+
+__global__ void pair_keys_kernel(const uint32_t *U, uint32_t m, const uint32_t *sa, const uint32_t *rank,
+                                 const uint32_t *block_of, const Block *blocks, uint64_t h,
+                                 uint64_t *keys, uint32_t *vals) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) {
+    const uint32_t g = sa[U[k]];
+    const Block &B = blocks[block_of[g]];
+    const uint32_t n = (uint32_t)B.n;
+    const uint32_t p = B.base + (uint32_t)(((uint64_t)(g - B.base) + h) % n);
+    keys[k] = ((uint64_t)rank[g] << 32) | rank[p];
+    vals[k] = g;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// C: BWT column, MTF and zero-run coding (compress.c generateMTFValues)
+// ---------------------------------------------------------------------------
+
+__global__ void mtf_kernel(Block *blocks, const int *ids, int nb, const uint32_t *sa,
+                           const uint8_t *rle, uint16_t *mtfv, uint32_t *freq_out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nb) return;
+  Block &B = blocks[ids[t]];
+  if (B.tie) return;
+  uint8_t u2s[256], yy[256];
+  int nin = 0;
+  for (int c = 0; c < 256; ++c)
+    if (B.in_use[c >> 5] & (1u << (c & 31))) u2s[c] = (uint8_t)nin++;
+  const int eob = nin + 1;
+  uint32_t freq[kMaxAlpha];
+  for (int i = 0; i < kMaxAlpha; ++i) freq[i] = 0;
+  for (int i = 0; i < nin; ++i) yy[i] = (uint8_t)i;
+  const uint8_t *d = rle + B.rle_off;
+  uint16_t *out = mtfv + B.mtf_off;
+  const uint32_t n = (uint32_t)B.n;
+  int64_t wr = 0;
+  uint32_t zpend = 0;
+  auto flush_zeros = [&]() {
+    zpend--;
+    for (;;) {
+      const uint16_t v = (zpend & 1) ? 1 : 0;  // RUNB : RUNA
+      out[wr++] = v;
+      freq[v]++;
+      if (zpend < 2) break;
+      zpend = (zpend - 2) / 2;
+    }
+    zpend = 0;
+  };
+  int orig = 0;
+  for (uint32_t j = 0; j < n; ++j) {
+    const uint32_t i = sa[B.base + j] - B.base;
+    if (i == 0) orig = (int)j;
+    const uint8_t ll = u2s[d[i == 0 ? n - 1 : i - 1]];
+    if (yy[0] == ll) {
+      zpend++;
+      continue;
+    }
+    if (zpend > 0) flush_zeros();
+    uint8_t tmp = yy[1];
+    yy[1] = yy[0];
+    int k = 1;
+    while (ll != tmp) {
+      ++k;
+      const uint8_t t2 = tmp;
+      tmp = yy[k];
+      yy[k] = t2;
+    }
+    yy[0] = tmp;
+    out[wr++] = (uint16_t)(k + 1);  // position k in the MTF list -> symbol k + 1
+    freq[k + 1]++;
+  }
+  if (zpend > 0) flush_zeros();
+  out[wr++] = (uint16_t)eob;
+  freq[eob]++;
+  B.n_mtf = (int32_t)wr;
+  B.n_in_use = nin;
+  B.orig = orig;
+  uint32_t *fo = freq_out + (size_t)ids[t] * kMaxAlpha;
+  for (int i = 0; i < kMaxAlpha; ++i) fo[i] = freq[i];
+}
+
+// ---------------------------------------------------------------------------
+// D: coding tables (compress.c sendMTFValues, huffman.c)
+// ---------------------------------------------------------------------------
+
+// BZ2_hbMakeCodeLengths, heap operations and tie-breaks as in huffman.c
+__device__ void make_code_lengths(uint8_t *len, const uint32_t *freq, int alpha, int max_len) {
+  int32_t heap[kMaxAlpha + 2];
+  int32_t weight[kMaxAlpha * 2];
+  int32_t parent[kMaxAlpha * 2];
+  for (int i = 0; i < alpha; ++i) weight[i + 1] = (int32_t)((freq[i] == 0 ? 1u : freq[i]) << 8);
+  for (;;) {
+    int n_nodes = alpha, n_heap = 0;
+    heap[0] = 0;
+    weight[0] = 0;
+    parent[0] = -2;
+    auto upheap = [&](int z) {
+      const int tmp = heap[z];
+      while (weight[tmp] < weight[heap[z >> 1]]) {
+        heap[z] = heap[z >> 1];
+        z >>= 1;
+      }
+      heap[z] = tmp;
+    };
+    auto downheap = [&](int z) {
+      const int tmp = heap[z];
+      for (;;) {
+        int y = z << 1;
+        if (y > n_heap) break;
+        if (y < n_heap && weight[heap[y + 1]] < weight[heap[y]]) y++;
+        if (weight[tmp] < weight[heap[y]]) break;
+        heap[z] = heap[y];
+        z = y;
+      }
+      heap[z] = tmp;
+    };
+    for (int i = 1; i <= alpha; ++i) {
+      parent[i] = -1;
+      heap[++n_heap] = i;
+      upheap(n_heap);
+    }
+    while (n_heap > 1) {
+      const int n1 = heap[1];
+      heap[1] = heap[n_heap--];
+      downheap(1);
+      const int n2 = heap[1];
+      heap[1] = heap[n_heap--];
+      downheap(1);
+      ++n_nodes;
+      parent[n1] = parent[n2] = n_nodes;
+      const int32_t w1 = weight[n1], w2 = weight[n2];
+      const int32_t d1 = w1 & 0xFF, d2 = w2 & 0xFF;
+      weight[n_nodes] = (int32_t)(((uint32_t)w1 & 0xFFFFFF00u) + ((uint32_t)w2 & 0xFFFFFF00u)) |
+                        (1 + (d1 > d2 ? d1 : d2));
+      parent[n_nodes] = -1;
+      heap[++n_heap] = n_nodes;
+      upheap(n_heap);
+    }
+    bool too_long = false;
+    for (int i = 1; i <= alpha; ++i) {
+      int j = 0, k = i;
+      while (parent[k] >= 0) {
+        k = parent[k];
+        ++j;
+      }
+      len[i - 1] = (uint8_t)j;
+      too_long |= j > max_len;
+    }
+    if (!too_long) return;
+    for (int i = 1; i <= alpha; ++i) {
+      const int j = weight[i] >> 8;
+      weight[i] = (1 + j / 2) << 8;
+    }
+  }
+}
+
+struct TablesOut {
+  uint8_t len[kMaxGroups][kMaxAlpha];
+  uint32_t code[kMaxGroups][kMaxAlpha];
+};
+
+__global__ void __launch_bounds__(kTableThreads) tables_kernel(Block *blocks, const int *ids,
+                                                               const uint16_t *mtfv,
+                                                               const uint32_t *freq_in,
+                                                               uint8_t *selectors, uint8_t *sel_mtf,
+                                                               TablesOut *tables) {
+  Block &B = blocks[ids[blockIdx.x]];
+  if (B.tie) return;
+  __shared__ uint8_t len[kMaxGroups][kMaxAlpha];
+  __shared__ uint32_t rfreq[kMaxGroups][kMaxAlpha];
+  __shared__ uint32_t freq[kMaxAlpha];
+  __shared__ unsigned long long data_bits;
+  const int tid = threadIdx.x;
+  const int alpha = B.n_in_use + 2;
+  const int n_mtf = B.n_mtf;
+  const int n_groups = n_mtf < 200 ? 2 : n_mtf < 600 ? 3 : n_mtf < 1200 ? 4 : n_mtf < 2400 ? 5 : 6;
+  const int n_sel = (n_mtf + kGroupSize - 1) / kGroupSize;
+  const uint16_t *mv = mtfv + B.mtf_off;
+  uint8_t *sel = selectors + B.sel_off;
+  for (int i = tid; i < kMaxAlpha; i += blockDim.x) freq[i] = freq_in[(size_t)ids[blockIdx.x] * kMaxAlpha + i];
+  __syncthreads();
+  if (tid == 0) {  // initial partition of the symbol range into n_groups tables
+    int n_part = n_groups, rem_f = n_mtf, gs = 0;
+    while (n_part > 0) {
+      const int t_freq = rem_f / n_part;
+      int ge = gs - 1, a_freq = 0;
+      while (a_freq < t_freq && ge < alpha - 1) a_freq += (int)freq[++ge];
+      if (ge > gs && n_part != n_groups && n_part != 1 && ((n_groups - n_part) % 2 == 1))
+        a_freq -= (int)freq[ge--];
+      for (int v = 0; v < alpha; ++v) len[n_part - 1][v] = (v >= gs && v <= ge) ? 0 : 15;
+      n_part--;
+      gs = ge + 1;
+      rem_f -= a_freq;
+    }
+  }
+  __syncthreads();
+  for (int iter = 0; iter < 4; ++iter) {
+    for (int i = tid; i < kMaxGroups * kMaxAlpha; i += blockDim.x) (&rfreq[0][0])[i] = 0;
+    __syncthreads();
+    for (int g = tid; g < n_sel; g += blockDim.x) {
+      const int gs = g * kGroupSize, ge = min(gs + kGroupSize, n_mtf);
+      uint32_t cost[kMaxGroups] = {0, 0, 0, 0, 0, 0};
+      for (int i = gs; i < ge; ++i) {
+        const int v = mv[i];
+#pragma unroll
+        for (int t = 0; t < kMaxGroups; ++t)
+          if (t < n_groups) cost[t] += len[t][v];
+      }
+      int bt = 0;
+      uint32_t bc = cost[0];
+      for (int t = 1; t < n_groups; ++t)
+        if (cost[t] < bc) { bc = cost[t]; bt = t; }
+      sel[g] = (uint8_t)bt;
+      for (int i = gs; i < ge; ++i) atomicAdd(&rfreq[bt][mv[i]], 1u);
+    }
+    __syncthreads();
+    if (tid < n_groups) make_code_lengths(len[tid], rfreq[tid], alpha, kMaxCodeLen);
+    __syncthreads();
+  }
+  TablesOut &T = tables[ids[blockIdx.x]];
+  if (tid < n_groups) {  // BZ2_hbAssignCodes
+    int mn = 32, mx = 0;
+    for (int i = 0; i < alpha; ++i) {
+      mn = min(mn, (int)len[tid][i]);
+      mx = max(mx, (int)len[tid][i]);
+    }
+    uint32_t vec = 0;
+    for (int n = mn; n <= mx; ++n) {
+      for (int i = 0; i < alpha; ++i)
+        if (len[tid][i] == n) T.code[tid][i] = vec++;
+      vec <<= 1;
+    }
+    for (int i = 0; i < alpha; ++i) T.len[tid][i] = len[tid][i];
+  }
+  if (tid == 0) data_bits = 0;
+  __syncthreads();
+  unsigned long long mine = 0;
+  for (int i = tid; i < n_mtf; i += blockDim.x) mine += len[sel[i / kGroupSize]][mv[i]];
+  atomicAdd(&data_bits, mine);
+  if (tid == 0) {
+    // selector MTF and the header bit count (compress.c sendMTFValues)
+    uint8_t pos[kMaxGroups];
+    for (int i = 0; i < n_groups; ++i) pos[i] = (uint8_t)i;
+    int64_t sel_bits = 0;
+    uint8_t *sm = sel_mtf + B.sel_off;
+    for (int i = 0; i < n_sel; ++i) {
+      const uint8_t s = sel[i];
+      int j = 0;
+      uint8_t tmp = pos[0];
+      while (s != tmp) {
+        ++j;
+        const uint8_t t2 = tmp;
+        tmp = pos[j];
+        pos[j] = t2;
+      }
+      pos[0] = tmp;
+      sm[i] = (uint8_t)j;
+      sel_bits += j + 1;
+    }
+    int used16 = 0;
+    for (int i = 0; i < 16; ++i) used16 += ((B.in_use[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu) ? 1 : 0;
+    int64_t tab_bits = 0;
+    for (int t = 0; t < n_groups; ++t) {
+      int curr = len[t][0];
+      tab_bits += 5;
+      for (int i = 0; i < alpha; ++i) {
+        const int l = len[t][i];
+        tab_bits += 2 * (int64_t)abs(l - curr) + 1;
+        curr = l;
+      }
+    }
+    B.n_groups = n_groups;
+    B.n_sel = n_sel;
+    B.hdr_bits = 48 + 32 + 1 + 24 + 16 + 16 * used16 + 3 + 15 + sel_bits + tab_bits;
+  }
+  __syncthreads();
+  if (tid == 0) B.data_bits = (int64_t)data_bits;
+}
+
+// ---------------------------------------------------------------------------
+// E: bit emission (big-endian bit order of bzlib.c bsW)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void put_bits(uint32_t *w, uint64_t bit, uint32_t v, int n) {
+  if (n == 0) return;
+  const uint64_t wi = bit >> 5;
+  const int off = (int)(bit & 31);
+  if (off + n <= 32) {
+    atomicOr(w + wi, v << (32 - off - n));
+  } else {
+    const int hi = 32 - off, lo = n - hi;
+    atomicOr(w + wi, v >> lo);
+    atomicOr(w + wi + 1, v << (32 - lo));
+  }
+}
+
+__global__ void __launch_bounds__(kEmitThreads) emit_kernel(const Block *blocks, const int *ids,
+                                                             const uint16_t *mtfv,
+                                                             const uint8_t *selectors,
+                                                             const uint8_t *sel_mtf,
+                                                             const TablesOut *tables, uint32_t *out) {
+  const Block &B = blocks[ids[blockIdx.x]];
+  if (B.tie) return;
+  const TablesOut &T = tables[ids[blockIdx.x]];
+  const int tid = threadIdx.x;
+  const int alpha = B.n_in_use + 2;
+  if (tid == 0) {
+    uint64_t p = B.bit_off;
+    auto put = [&](int n, uint32_t v) { put_bits(out, p, v, n); p += n; };
+    put(24, 0x314159u);
+    put(24, 0x265359u);
+    put(32, B.crc);
+    put(1, 0);
+    put(24, (uint32_t)B.orig);
+    uint32_t used16 = 0;
+    for (int i = 0; i < 16; ++i)
+      if ((B.in_use[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu) used16 |= 1u << (15 - i);
+    put(16, used16);
+    for (int i = 0; i < 16; ++i) {
+      const uint32_t h = (B.in_use[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
+      if (h) put(16, __brev(h) >> 16);  // bit for symbol 16i+j first
+    }
+    put(3, (uint32_t)B.n_groups);
+    put(15, (uint32_t)B.n_sel);
+    const uint8_t *sm = sel_mtf + B.sel_off;
+    for (int i = 0; i < B.n_sel; ++i) {
+      int j = sm[i] + 1;  // j ones then a zero
+      while (j > 0) {
+        const int k = j > 31 ? 31 : j;
+        j -= k;
+        put(k, j > 0 ? (1u << k) - 1u : ((1u << k) - 2u));
+      }
+    }
+    for (int t = 0; t < B.n_groups; ++t) {
+      int curr = T.len[t][0];
+      put(5, (uint32_t)curr);
+      for (int i = 0; i < alpha; ++i) {
+        const int l = T.len[t][i];
+        while (curr < l) { put(2, 2); ++curr; }
+        while (curr > l) { put(2, 3); --curr; }
+        put(1, 0);
+      }
+    }
+  }
+  // data: codes at scanned offsets
+  typedef cub::BlockScan<unsigned long long, kEmitThreads> Scan;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ unsigned long long s_base;
+  if (tid == 0) s_base = (unsigned long long)(B.bit_off + B.hdr_bits);
+  __syncthreads();
+  const uint16_t *mv = mtfv + B.mtf_off;
+  const uint8_t *sel = selectors + B.sel_off;
+  const int n_mtf = B.n_mtf;
+  for (int tile = 0; tile < n_mtf; tile += kEmitThreads * kEmitItems) {
+    const int i0 = tile + tid * kEmitItems;
+    uint8_t l[kEmitItems];
+    uint32_t c[kEmitItems];
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int q = 0; q < kEmitItems; ++q) {
+      const int i = i0 + q;
+      if (i < n_mtf) {
+        const int t = sel[i / kGroupSize];
+        const int v = mv[i];
+        l[q] = T.len[t][v];
+        c[q] = T.code[t][v];
+      } else {
+        l[q] = 0;
+        c[q] = 0;
+      }
+      sum += l[q];
+    }
+    unsigned long long excl, total;
+    Scan(scan_tmp).ExclusiveSum(sum, excl, total);
+    uint64_t p = s_base + excl;
+#pragma unroll
+    for (int q = 0; q < kEmitItems; ++q) {
+      put_bits(out, p, c[q], l[q]);
+      p += l[q];
+    }
+    __syncthreads();
+    if (tid == 0) s_base += total;
+    __syncthreads();
+  }
+}
+
+struct JobFrame {
+  uint64_t bit0;      // absolute bit position of the job's stream
+  uint64_t end_bit;   // position of the end-of-stream marker
+  uint32_t combined;
+};
+
+__global__ void frame_kernel(const JobFrame *frames, const int *jids, int n, uint32_t *out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const JobFrame &F = frames[jids[t]];
+  put_bits(out, F.bit0, 0x425A6839u, 32);  // "BZh9"
+  put_bits(out, F.end_bit, 0x177245u, 24);
+  put_bits(out, F.end_bit + 24, 0x385090u, 24);
+  put_bits(out, F.end_bit + 48, F.combined, 32);
+}
+
+__global__ void byteswap_kernel(uint32_t *w, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    w[i] = __byte_perm(w[i], 0, 0x0123);
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+
+thread_local std::string g_bz_err;
+
+int bz_fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_bz_err = buf;
+  return code;
+}
+
+#define BZ_TRY(x)                                                                             \
+  do {                                                                                        \
+    cudaError_t e_ = (x);                                                                     \
+    if (e_ != cudaSuccess)                                                                    \
+      return bz_fail(PCBZ_E_CUDA, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, \
+                     __LINE__);                                                               \
+  } while (0)
+
+struct Scratch {  // grow-only device buffers, one set per host thread
+  struct Buf {
+    void *p = nullptr;
+    size_t cap = 0;
+  };
+  Buf b[32];
+  template <typename T>
+  int get(int slot, size_t count, T **out) {
+    Buf &x = b[slot];
+    const size_t need = std::max<size_t>(count * sizeof(T), 256);
+    if (need > x.cap) {
+      if (x.p) cudaFree(x.p);
+      x.p = nullptr;
+      x.cap = 0;
+      BZ_TRY(cudaMalloc(&x.p, need));
+      x.cap = need;
+    }
+    *out = static_cast<T *>(x.p);
+    return PCBZ_OK;
+  }
+};
+thread_local Scratch g_scr;
+
+int grid_of(int64_t n, int threads = 256) {
+  int64_t g = (n + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
+}
+
+__global__ void iota_kernel(uint32_t *a, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
+}
+
+// Rotation sort of every block (stage B): sa[base + j] = start of the j-th
+// smallest rotation of the block; blocks[b].tie set for periodic blocks.
+int sort_rotations(Block *d_blocks, const int *d_ids, int nb, int nslots, const uint8_t *d_rle,
+                   uint32_t N, uint32_t *sa, cudaStream_t st) {
+  uint32_t *block_of, *rank, *vals_a, *vals_b, *U, *U2, *gs;
+  uint64_t *keys_a, *keys_b;
+  uint8_t *hd, *unres;
+  int *d_nsel;
+  int rc;
+  if ((rc = g_scr.get(4, N, &block_of)) || (rc = g_scr.get(6, N, &rank)) || (rc = g_scr.get(7, N, &vals_a)) ||
+      (rc = g_scr.get(8, N, &vals_b)) || (rc = g_scr.get(9, N, &U)) || (rc = g_scr.get(10, N, &U2)) ||
+      (rc = g_scr.get(11, N, &gs)) || (rc = g_scr.get(12, N, &keys_a)) || (rc = g_scr.get(13, N, &keys_b)) ||
+      (rc = g_scr.get(14, N, &hd)) || (rc = g_scr.get(15, N, &unres)) || (rc = g_scr.get(16, 1, &d_nsel)))
+    return rc;
+  size_t t_sort = 0, t_scan = 0, t_sel = 0;
+  BZ_TRY(cub::DeviceRadixSort::SortPairs(nullptr, t_sort, keys_a, keys_b, vals_a, vals_b, N, 0, 64, st));
+  BZ_TRY(cub::DeviceScan::InclusiveScan(nullptr, t_scan, gs, gs, MaxOp(), N, st));
+  BZ_TRY(cub::DeviceSelect::Flagged(nullptr, t_sel, U, unres, U2, d_nsel, N, st));
+  const size_t t_all = std::max({t_sort, t_scan, t_sel});
+  uint8_t *d_tmp;
+  if ((rc = g_scr.get(17, t_all, &d_tmp))) return rc;
+  int bits_b = 1;
+  while ((1 << bits_b) < nslots) ++bits_b;
+  int bits_r = 1;
+  while (((uint64_t)1 << bits_r) <= (uint64_t)N) ++bits_r;
+  fill_block_of_kernel<<<nb, 256, 0, st>>>(d_blocks, d_ids, block_of);
+  init_keys_kernel<<<grid_of(N), 256, 0, st>>>(d_blocks, block_of, d_rle, N, keys_a, vals_a);
+  BZ_TRY(cudaGetLastError());
+  size_t tb = t_all;
+  BZ_TRY(cub::DeviceRadixSort::SortPairs(d_tmp, tb, keys_a, keys_b, vals_a, vals_b, N, 0, 32 + bits_b, st));
+  heads_kernel<<<grid_of(N), 256, 0, st>>>(keys_b, N, hd);
+  head_pos_kernel<<<grid_of(N), 256, 0, st>>>(hd, nullptr, N, gs);
+  tb = t_all;
+  BZ_TRY(cub::DeviceScan::InclusiveScan(d_tmp, tb, gs, gs, MaxOp(), N, st));
+  settle_kernel<<<grid_of(N), 256, 0, st>>>(vals_b, nullptr, N, hd, gs, sa, rank, block_of, d_blocks, 4, unres);
+  iota_kernel<<<grid_of(N), 256, 0, st>>>(vals_a, N);
+  tb = t_all;
+  BZ_TRY(cub::DeviceSelect::Flagged(d_tmp, tb, vals_a, unres, U, d_nsel, N, st));
+  int h_nsel = 0;
+  BZ_TRY(cudaMemcpyAsync(&h_nsel, d_nsel, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BZ_TRY(cudaStreamSynchronize(st));
+  uint32_t m = (uint32_t)h_nsel;
+  for (uint64_t h = 4; m > 0; h *= 2) {
+    pair_keys_kernel<<<grid_of(m), 256, 0, st>>>(U, m, sa, rank, block_of, d_blocks, h, keys_a, vals_a);
+    tb = t_all;
+    BZ_TRY(cub::DeviceRadixSort::SortPairs(d_tmp, tb, keys_a, keys_b, vals_a, vals_b, m, 0, 32 + bits_r, st));
+    heads_kernel<<<grid_of(m), 256, 0, st>>>(keys_b, m, hd);
+    head_pos_kernel<<<grid_of(m), 256, 0, st>>>(hd, U, m, gs);
+    tb = t_all;
+    BZ_TRY(cub::DeviceScan::InclusiveScan(d_tmp, tb, gs, gs, MaxOp(), m, st));
+    settle_kernel<<<grid_of(m), 256, 0, st>>>(vals_b, U, m, hd, gs, sa, rank, block_of, d_blocks, 2 * h, unres);
+    tb = t_all;
+    BZ_TRY(cub::DeviceSelect::Flagged(d_tmp, tb, U, unres, U2, d_nsel, m, st));
+    BZ_TRY(cudaMemcpyAsync(&h_nsel, d_nsel, sizeof(int), cudaMemcpyDeviceToHost, st));
+    BZ_TRY(cudaStreamSynchronize(st));
+    m = (uint32_t)h_nsel;
+    std::swap(U, U2);
+  }
+  return PCBZ_OK;
+}
+
+size_t job_bound(int64_t len) { return (size_t)((len + len / 100 + 1024 + 3) & ~(int64_t)3); }
+
+// Code jobs held in device memory (in_off: host array of njobs + 1 offsets
+// into d_in).  Job j's bytes land at d_out + out_start[j] (4-byte aligned),
+// out_len[j] bytes; host_needed[j] = 1 marks a job left to the host libbz2
+// (a periodic block), with out_len[j] = 0.  Synchronises `st`.
+int compress_jobs(const uint8_t *d_in, const int64_t *in_off, int njobs, uint8_t *d_out, size_t out_cap,
+                  int64_t *out_start, int64_t *out_len, uint8_t *host_needed, cudaStream_t st) {
+  if (njobs <= 0) return PCBZ_OK;
+  for (int j = 0; j < njobs; ++j)
+    if (in_off[j + 1] < in_off[j]) return bz_fail(PCBZ_E_INVALID, "job offsets must be non-decreasing");
+  // ---- A: RLE1 + block split ---------------------------------------------------
+  std::vector<Job> jobs(njobs);
+  int64_t rle_total = 0;
+  int nslots = 0;
+  for (int j = 0; j < njobs; ++j) {
+    Job &J = jobs[j];
+    J.in_off = in_off[j];
+    J.in_len = in_off[j + 1] - in_off[j];
+    J.rle_off = rle_total;
+    const int64_t cap = J.in_len + J.in_len / 4 + 64;
+    rle_total += (cap + 15) & ~(int64_t)15;
+    J.block0 = nslots;
+    nslots += (int)(cap / kBlockMax) + 2;
+    J.nblocks = 0;
+  }
+  if (rle_total >= ((int64_t)1 << 31)) return bz_fail(PCBZ_E_INVALID, "bzip2 batch too large: split the jobs");
+  Job *d_jobs;
+  Block *d_blocks;
+  uint8_t *d_rle;
+  int rc;
+  if ((rc = g_scr.get(0, njobs, &d_jobs)) || (rc = g_scr.get(1, nslots, &d_blocks)) ||
+      (rc = g_scr.get(2, (size_t)rle_total, &d_rle)))
+    return rc;
+  BZ_TRY(cudaMemcpyAsync(d_jobs, jobs.data(), njobs * sizeof(Job), cudaMemcpyHostToDevice, st));
+  rle1_kernel<<<(njobs + 63) / 64, 64, 0, st>>>(d_in, d_jobs, njobs, d_rle, d_blocks);
+  BZ_TRY(cudaGetLastError());
+  std::vector<Block> blocks(nslots);
+  BZ_TRY(cudaMemcpyAsync(jobs.data(), d_jobs, njobs * sizeof(Job), cudaMemcpyDeviceToHost, st));
+  BZ_TRY(cudaMemcpyAsync(blocks.data(), d_blocks, nslots * sizeof(Block), cudaMemcpyDeviceToHost, st));
+  BZ_TRY(cudaStreamSynchronize(st));
+  std::vector<int> ids;
+  int64_t N = 0, mtf_total = 0, sel_total = 0;
+  for (int j = 0; j < njobs; ++j)
+    for (int k = 0; k < jobs[j].nblocks; ++k) {
+      const int b = jobs[j].block0 + k;
+      Block &B = blocks[b];
+      B.base = (uint32_t)N;
+      B.mtf_off = mtf_total;
+      B.sel_off = sel_total;
+      N += B.n;
+      mtf_total += B.n + 1;
+      sel_total += (B.n + 1 + kGroupSize - 1) / kGroupSize;
+      ids.push_back(b);
+    }
+  const int nb = (int)ids.size();
+  if (N >= ((int64_t)1 << 31)) return bz_fail(PCBZ_E_INVALID, "bzip2 batch too large: split the jobs");
+  int *d_ids;
+  uint16_t *mtfv;
+  uint32_t *freq, *sa;
+  uint8_t *selectors, *sel_mtf;
+  TablesOut *tables;
+  if ((rc = g_scr.get(3, std::max(nb, 1), &d_ids)) || (rc = g_scr.get(5, std::max<int64_t>(N, 1), &sa)) ||
+      (rc = g_scr.get(18, std::max<int64_t>(mtf_total, 1), &mtfv)) ||
+      (rc = g_scr.get(19, (size_t)nslots * kMaxAlpha, &freq)) ||
+      (rc = g_scr.get(20, std::max<int64_t>(sel_total, 1), &selectors)) ||
+      (rc = g_scr.get(21, std::max<int64_t>(sel_total, 1), &sel_mtf)) ||
+      (rc = g_scr.get(22, (size_t)nslots, &tables)))
+    return rc;
+  if (nb > 0) {
+    BZ_TRY(cudaMemcpyAsync(d_ids, ids.data(), nb * sizeof(int), cudaMemcpyHostToDevice, st));
+    BZ_TRY(cudaMemcpyAsync(d_blocks, blocks.data(), nslots * sizeof(Block), cudaMemcpyHostToDevice, st));
+    // ---- B, C, D ---------------------------------------------------------------
+    if ((rc = sort_rotations(d_blocks, d_ids, nb, nslots, d_rle, (uint32_t)N, sa, st))) return rc;
+    mtf_kernel<<<(nb + 63) / 64, 64, 0, st>>>(d_blocks, d_ids, nb, sa, d_rle, mtfv, freq);
+    tables_kernel<<<nb, kTableThreads, 0, st>>>(d_blocks, d_ids, mtfv, freq, selectors, sel_mtf, tables);
+    BZ_TRY(cudaGetLastError());
+    BZ_TRY(cudaMemcpyAsync(blocks.data(), d_blocks, nslots * sizeof(Block), cudaMemcpyDeviceToHost, st));
+    BZ_TRY(cudaStreamSynchronize(st));
+  }
+  // ---- E: output layout, emission, framing --------------------------------------
+  std::vector<JobFrame> frames(njobs);
+  std::vector<int> coded;
+  int64_t word = 0;
+  for (int j = 0; j < njobs; ++j) {
+    bool tie = false;
+    for (int k = 0; k < jobs[j].nblocks; ++k) tie |= blocks[jobs[j].block0 + k].tie != 0;
+    host_needed[j] = tie ? 1 : 0;
+    out_start[j] = word * 4;
+    out_len[j] = 0;
+    if (tie) continue;
+    const uint64_t bit0 = (uint64_t)word * 32;
+    uint64_t p = bit0 + 32;
+    uint32_t combined = 0;
+    for (int k = 0; k < jobs[j].nblocks; ++k) {
+      Block &B = blocks[jobs[j].block0 + k];
+      B.bit_off = (int64_t)p;
+      p += (uint64_t)(B.hdr_bits + B.data_bits);
+      combined = ((combined << 1) | (combined >> 31)) ^ B.crc;
+    }
+    frames[j] = JobFrame{bit0, p, combined};
+    const uint64_t end = p + 80;
+    out_len[j] = (int64_t)((end - bit0 + 7) / 8);
+    word += (int64_t)((end - bit0 + 31) / 32);
+    coded.push_back(j);
+  }
+  if ((size_t)word * 4 > out_cap) return bz_fail(PCBZ_E_INVALID, "bzip2 output buffer too small");
+  JobFrame *d_frames;
+  int *d_coded;
+  if ((rc = g_scr.get(23, njobs, &d_frames)) || (rc = g_scr.get(24, std::max<size_t>(coded.size(), 1), &d_coded)))
+    return rc;
+  BZ_TRY(cudaMemcpyAsync(d_frames, frames.data(), njobs * sizeof(JobFrame), cudaMemcpyHostToDevice, st));
+  if (!coded.empty())
+    BZ_TRY(cudaMemcpyAsync(d_coded, coded.data(), coded.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  uint32_t *out_w = reinterpret_cast<uint32_t *>(d_out);
+  if (word > 0) BZ_TRY(cudaMemsetAsync(out_w, 0, (size_t)word * 4, st));
+  if (nb > 0) {
+    BZ_TRY(cudaMemcpyAsync(d_blocks, blocks.data(), nslots * sizeof(Block), cudaMemcpyHostToDevice, st));
+    emit_kernel<<<nb, kEmitThreads, 0, st>>>(d_blocks, d_ids, mtfv, selectors, sel_mtf, tables, out_w);
+  }
+  if (!coded.empty())
+    frame_kernel<<<((int)coded.size() + 127) / 128, 128, 0, st>>>(d_frames, d_coded, (int)coded.size(), out_w);
+  if (word > 0) byteswap_kernel<<<grid_of(word), 256, 0, st>>>(out_w, word);
+  BZ_TRY(cudaGetLastError());
+  BZ_TRY(cudaStreamSynchronize(st));
+  return PCBZ_OK;
+}
+
+}  // namespace bz
+}  // namespace pcbz
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+
+namespace {
+thread_local cudaStream_t g_bz_stream = nullptr;
+struct HostBufs { pcbz::bz::Scratch::Buf in, out; };
+thread_local HostBufs g_bz_host;
+int grow(pcbz::bz::Scratch::Buf &b, size_t n) {
+  if (n <= b.cap) return PCBZ_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  cudaError_t e = cudaMalloc(&b.p, std::max<size_t>(n, 256));
+  if (e != cudaSuccess) return pcbz::bz::bz_fail(PCBZ_E_CUDA, "cudaMalloc: %s", cudaGetErrorString(e));
+  b.cap = std::max<size_t>(n, 256);
+  return PCBZ_OK;
+}
+}  // namespace
+
+extern "C" {
+
+const char *pcbz_bzip2_last_error(void) { return pcbz::bz::g_bz_err.c_str(); }
+
+size_t pcbz_bzip2_bound(const int64_t *in_off, int njobs) {
+  size_t b = 0;
+  for (int j = 0; j < njobs; ++j) b += pcbz::bz::job_bound(in_off[j + 1] - in_off[j]);
+  return b;
+}
+
+int pcbz_bzip2_device(const uint8_t *d_in, const int64_t *in_off, int njobs, uint8_t *d_out, size_t out_cap,
+                      int64_t *out_start, int64_t *out_len, uint8_t *host_needed, void *stream) {
+  return pcbz::bz::compress_jobs(d_in, in_off, njobs, d_out, out_cap, out_start, out_len, host_needed,
+                                 static_cast<cudaStream_t>(stream));
+}
+
+int pcbz_bzip2_host(const uint8_t *in, const int64_t *in_off, int njobs, uint8_t *out, size_t out_cap,
+                    int64_t *out_start, int64_t *out_len, uint8_t *host_needed) {
+  if (njobs <= 0) return PCBZ_OK;
+  if (!g_bz_stream) {
+    cudaError_t e = cudaStreamCreateWithFlags(&g_bz_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return pcbz::bz::bz_fail(PCBZ_E_NODEVICE, "no CUDA device: %s", cudaGetErrorString(e));
+  }
+  const int64_t total = in_off[njobs] - in_off[0];
+  int rc;
+  const size_t bound = pcbz_bzip2_bound(in_off, njobs);
+  if ((rc = grow(g_bz_host.in, (size_t)std::max<int64_t>(total, 1))) || (rc = grow(g_bz_host.out, bound)))
+    return rc;
+  std::vector<int64_t> rel(njobs + 1);
+  for (int j = 0; j <= njobs; ++j) rel[j] = in_off[j] - in_off[0];
+  cudaStream_t st = g_bz_stream;
+  if (total > 0 &&
+      cudaMemcpyAsync(g_bz_host.in.p, in + in_off[0], (size_t)total, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return pcbz::bz::bz_fail(PCBZ_E_CUDA, "H2D copy failed");
+  rc = pcbz::bz::compress_jobs(static_cast<const uint8_t *>(g_bz_host.in.p), rel.data(), njobs,
+                               static_cast<uint8_t *>(g_bz_host.out.p), bound, out_start, out_len,
+                               host_needed, st);
+  if (rc) return rc;
+  int64_t used = 0;
+  for (int j = 0; j < njobs; ++j) used = std::max(used, out_start[j] + out_len[j]);
+  if ((size_t)used > out_cap) return pcbz::bz::bz_fail(PCBZ_E_INVALID, "output buffer too small");
+  if (used > 0 && cudaMemcpy(out, g_bz_host.out.p, (size_t)used, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return pcbz::bz::bz_fail(PCBZ_E_CUDA, "D2H copy failed");
+  return PCBZ_OK;
+}
+
+}  // extern "C"
