@@ -5,8 +5,10 @@
 // libbz2 by tests/test_bzip2_ref.py); stages follow it.
 //
 // Many independent inputs ("jobs", one per PCBZ block) are coded together:
-//   A  rle1_kernel       one thread per job: bzlib.c's RLE1 state machine,
-//                        block split at nblockMAX, block CRC, symbol map
+//   A  RLE1              runs -> 255-byte chunk events -> output offsets
+//                        (scan), libbz2's greedy block split (binary search
+//                        per job), bytes, block CRCs (GF(2)-linear, chunked),
+//                        used-symbol maps
 //   B  prefix doubling   cyclic-rotation sort of every block at once: CUB
 //                        radix sorts of (group, partner rank) keys over the
 //                        shrinking set of unresolved groups
@@ -64,6 +66,7 @@ struct Block {
   int32_t n_mtf, n_groups, n_sel, n_in_use;
   int64_t hdr_bits, data_bits;
   int64_t bit_off;        // absolute bit position in the output word stream
+  uint32_t in_begin, in_end;   // the job input bytes this block codes (stage A)
 };
 
 __device__ __forceinline__ uint32_t crc_entry(uint32_t i) {
@@ -77,66 +80,193 @@ __device__ __forceinline__ uint32_t crc_entry(uint32_t i) {
 // copy_input_until_stop, handle_compress as driven by bz2.compress)
 // ---------------------------------------------------------------------------
 
-__global__ void rle1_kernel(const uint8_t *__restrict__ in, Job *jobs, int njobs,
-                            uint8_t *__restrict__ rle, Block *blocks) {
+// Stage A in parallel (oracle/bzip2_ref.py rle1_blocks is the sequential
+// restatement):
+//   runs       maximal runs of one byte value (job starts force a run start)
+//   events     a run of L bytes is added as floor(L/255) chunks of 255 (5
+//              output bytes: 4 x ch + 251) and a remainder r (r <= 3: r bytes,
+//              else 5) -- bzlib.c flushes a run at 255 and at its end
+//   blocks     greedy over events: a block closes after the first event that
+//              brings it to >= nblockMAX bytes (the check before every input
+//              char), so a block may end inside a long run
+//   CRC        linear over GF(2): each 4 KB chunk's CRC from a zero register,
+//              shifted by the bytes after it in the block (32x32 bit-matrix
+//              powers of "append a zero byte"), XORed together with the
+//              shifted initial register
+
+__constant__ uint32_t c_zero_shift[32][32];   // [k][bit]: image of bit after 2^k zero bytes
+
+__device__ __forceinline__ uint32_t gf2_apply(int k, uint32_t v) {
+  uint32_t r = 0;
+#pragma unroll 4
+  for (int b = 0; b < 32; ++b)
+    if (v & (1u << b)) r ^= c_zero_shift[k][b];
+  return r;
+}
+
+__device__ uint32_t crc_shift(uint32_t v, uint64_t nbytes) {
+  for (int k = 0; nbytes; ++k, nbytes >>= 1)
+    if (nbytes & 1) v = gf2_apply(k, v);
+  return v;
+}
+
+__device__ __forceinline__ uint32_t run_out_bytes(uint32_t L) {
+  const uint32_t rem = L % 255;
+  return 5 * (L / 255) + (rem <= 3 ? rem : 5);
+}
+
+__global__ void run_flags_kernel(const uint8_t *in, int64_t total, uint8_t *flags) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = (i == 0 || in[i] != in[i - 1]) ? 1 : 0;
+}
+
+__global__ void job_start_flags_kernel(const int64_t *in_off, int njobs, uint8_t *flags) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < njobs && in_off[j] < in_off[j + 1]) flags[in_off[j]] = 1;
+}
+
+__global__ void iota64_kernel(uint32_t *a, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = (uint32_t)i;
+}
+
+__global__ void run_sizes_kernel(const uint32_t *rs, uint32_t R, uint32_t total, uint32_t *osz) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+    const uint32_t e = r + 1 < R ? rs[r + 1] : total;
+    osz[r] = run_out_bytes(e - rs[r]);
+  }
+}
+
+// one thread per job: block split by binary search over the runs' output
+// offsets (ocum: exclusive scan of the run sizes, R + 1 entries)
+__global__ void split_kernel(const int64_t *in_off, int njobs, const uint32_t *rs, uint32_t R,
+                             uint32_t total, const uint32_t *ocum, Job *jobs, Block *blocks) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= njobs) return;
+  Job &J = jobs[j];
+  J.nblocks = 0;
+  if (in_off[j] == in_off[j + 1]) return;
+  auto lower = [&](uint32_t x) {  // first run with rs >= x
+    uint32_t lo = 0, hi = R;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (rs[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  const uint32_t r0 = lower((uint32_t)in_off[j]), r1 = lower((uint32_t)in_off[j + 1]);
+  auto run_end = [&](uint32_t r) { return r + 1 < R ? rs[r + 1] : total; };
+  uint32_t start = ocum[r0];
+  const uint32_t end = ocum[r1];
+  uint32_t in_start = rs[r0];
+  uint32_t r = r0;
+  int nb = 0;
+  while (start < end) {
+    uint32_t bend, in_end;
+    if (end - start < (uint32_t)kBlockMax) {
+      bend = end;
+      in_end = (uint32_t)in_off[j + 1];
+    } else {
+      // first run rr >= r whose end brings the block to >= kBlockMax
+      uint32_t lo = r, hi = r1 - 1;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (ocum[mid + 1] - start >= (uint32_t)kBlockMax) hi = mid; else lo = mid + 1;
+      }
+      const uint32_t rr = lo;
+      const int64_t c0 = (int64_t)ocum[rr] - (int64_t)start;   // may be < 0 mid-run
+      const uint32_t L = run_end(rr) - rs[rr];
+      const int64_t nfull = L / 255;
+      const int64_t e = (kBlockMax - c0 + 4) / 5;                // chunk events needed
+      if (nfull > 0 && e <= nfull) {
+        bend = ocum[rr] + (uint32_t)(5 * e);
+        in_end = rs[rr] + (uint32_t)(255 * e);
+        r = rr;
+      } else {
+        bend = ocum[rr + 1];
+        in_end = run_end(rr);
+        r = rr + 1;
+      }
+    }
+    Block &B = blocks[J.block0 + nb];
+    B.rle_off = start;
+    B.n = (int32_t)(bend - start);
+    B.job = j;
+    B.tie = 0;
+    B.in_begin = in_start;
+    B.in_end = in_end;
+    ++nb;
+    start = bend;
+    in_start = in_end;
+  }
+  J.nblocks = nb;
+}
+
+__global__ void run_write_kernel(const uint8_t *in, const uint32_t *rs, uint32_t R, uint32_t total,
+                                 const uint32_t *ocum, uint8_t *rle) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+    const uint32_t b = rs[r], L = (r + 1 < R ? rs[r + 1] : total) - b;
+    const uint8_t ch = in[b];
+    uint8_t *o = rle + ocum[r];
+    for (uint32_t k = 0; k < L / 255; ++k) {
+      o[0] = o[1] = o[2] = o[3] = ch;
+      o[4] = 251;
+      o += 5;
+    }
+    const uint32_t rem = L % 255;
+    if (rem <= 3) {
+      for (uint32_t k = 0; k < rem; ++k) o[k] = ch;
+    } else {
+      o[0] = o[1] = o[2] = o[3] = ch;
+      o[4] = (uint8_t)(rem - 4);
+    }
+  }
+}
+
+constexpr int kCrcChunk = 4096;
+
+// grid: (chunk, block) pairs; acc[b] ^= shifted CRC of one input chunk
+__global__ void crc_chunks_kernel(const uint8_t *in, const Block *blocks, const int *ids,
+                                  const uint32_t *chunk0, int nb, uint32_t *acc) {
   __shared__ uint32_t tab[256];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = crc_entry(i);
   __syncthreads();
-  const int jid = blockIdx.x * blockDim.x + threadIdx.x;
-  if (jid >= njobs) return;
-  Job &J = jobs[jid];
-  const uint8_t *src = in + J.in_off;
-  uint8_t *dst = rle + J.rle_off;
-  int64_t pos = 0, bstart = 0;
-  int nb = 0;
-  uint32_t crc = 0xFFFFFFFFu;
-  uint32_t used[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  uint32_t ch = 256, run = 0;
-  auto crc_up = [&](uint32_t c) { crc = (crc << 8) ^ tab[(crc >> 24) ^ c]; };
-  auto mark = [&](uint32_t c) { used[c >> 5] |= 1u << (c & 31); };
-  auto close_block = [&]() {
-    Block &B = blocks[J.block0 + nb];
-    B.rle_off = J.rle_off + bstart;
-    B.n = (int32_t)(pos - bstart);
-    B.job = jid;
-    B.crc = ~crc;
-    for (int k = 0; k < 8; ++k) { B.in_use[k] = used[k]; used[k] = 0; }
-    B.tie = 0;
-    ++nb;
-    bstart = pos;
-    crc = 0xFFFFFFFFu;
-  };
-  auto add_pair = [&]() {
-    for (uint32_t i = 0; i < run; ++i) crc_up(ch);
-    mark(ch);
-    if (run <= 3) {
-      for (uint32_t i = 0; i < run; ++i) dst[pos++] = (uint8_t)ch;
-    } else {
-      mark(run - 4);
-      for (int i = 0; i < 4; ++i) dst[pos++] = (uint8_t)ch;
-      dst[pos++] = (uint8_t)(run - 4);
-    }
-  };
-  for (int64_t k = 0; k < J.in_len; ++k) {
-    const uint32_t c = __ldg(src + k);
-    if (pos - bstart >= kBlockMax) close_block();
-    if (c != ch && run == 1) {
-      crc_up(ch);
-      mark(ch);
-      dst[pos++] = (uint8_t)ch;
-      ch = c;
-    } else if (c != ch || run == 255) {
-      if (ch < 256) add_pair();
-      ch = c;
-      run = 1;
-    } else {
-      ++run;
-    }
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  // block of chunk c: last t with chunk0[t] <= c
+  int lo = 0, hi = nb;  // chunk0 has nb + 1 entries
+  if (c >= chunk0[nb]) return;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (chunk0[mid] <= c) lo = mid; else hi = mid;
   }
-  if (pos - bstart >= kBlockMax) close_block();
-  if (ch < 256) add_pair();
-  if (pos > bstart) close_block();
-  J.nblocks = nb;
+  const Block &B = blocks[ids[lo]];
+  const uint32_t ib = B.in_begin, ie = B.in_end;
+  const uint32_t a = ib + (c - chunk0[lo]) * kCrcChunk;
+  const uint32_t e = min(ie, a + kCrcChunk);
+  uint32_t crc = 0;
+  for (uint32_t i = a; i < e; ++i) crc = (crc << 8) ^ tab[(crc >> 24) ^ in[i]];
+  crc = crc_shift(crc, ie - e);
+  if (c == chunk0[lo]) crc ^= crc_shift(0xFFFFFFFFu, ie - ib);   // the initial register
+  atomicXor(&acc[lo], crc);
+}
+
+// one CTA per block: final CRC and the used-byte map of its RLE1 bytes
+__global__ void block_meta_kernel(const uint8_t *rle, Block *blocks, const int *ids, const uint32_t *acc) {
+  __shared__ uint8_t seen[256];
+  Block &B = blocks[ids[blockIdx.x]];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) seen[i] = 0;
+  __syncthreads();
+  const uint8_t *d = rle + B.rle_off;
+  for (int i = threadIdx.x; i < B.n; i += blockDim.x) seen[d[i]] = 1;
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    uint32_t w = 0;
+    for (int b = 0; b < 32; ++b) w |= (uint32_t)seen[32 * threadIdx.x + b] << b;
+    B.in_use[threadIdx.x] = w;
+  }
+  if (threadIdx.x == 0) B.crc = ~acc[blockIdx.x];
 }
 
 // ---------------------------------------------------------------------------
@@ -215,68 +345,245 @@ __global__ void pair_keys_kernel(const uint32_t *U, uint32_t m, const uint32_t *
 // ---------------------------------------------------------------------------
 // C: BWT column, MTF and zero-run coding (compress.c generateMTFValues)
 // ---------------------------------------------------------------------------
+//
+// One warp per block.  The 256-entry MTF list lives in registers: lane l
+// holds positions 8l..8l+7 as the bytes of a 64-bit word.  A symbol is found
+// with two SIMD byte compares and a ballot; moving it to the front shifts
+// every lane below it by one byte (the carry byte comes from the lane below
+// through a shuffle).  BWT characters are gathered 32 at a time.
 
-__global__ void mtf_kernel(Block *blocks, const int *ids, int nb, const uint32_t *sa,
-                           const uint8_t *rle, uint16_t *mtfv, uint32_t *freq_out) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nb) return;
-  Block &B = blocks[ids[t]];
-  if (B.tie) return;
-  uint8_t u2s[256], yy[256];
-  int nin = 0;
-  for (int c = 0; c < 256; ++c)
-    if (B.in_use[c >> 5] & (1u << (c & 31))) u2s[c] = (uint8_t)nin++;
-  const int eob = nin + 1;
-  uint32_t freq[kMaxAlpha];
-  for (int i = 0; i < kMaxAlpha; ++i) freq[i] = 0;
-  for (int i = 0; i < nin; ++i) yy[i] = (uint8_t)i;
-  const uint8_t *d = rle + B.rle_off;
-  uint16_t *out = mtfv + B.mtf_off;
-  const uint32_t n = (uint32_t)B.n;
-  int64_t wr = 0;
-  uint32_t zpend = 0;
-  auto flush_zeros = [&]() {
-    zpend--;
-    for (;;) {
-      const uint16_t v = (zpend & 1) ? 1 : 0;  // RUNB : RUNA
-      out[wr++] = v;
-      freq[v]++;
-      if (zpend < 2) break;
-      zpend = (zpend - 2) / 2;
-    }
-    zpend = 0;
-  };
-  int orig = 0;
-  for (uint32_t j = 0; j < n; ++j) {
-    const uint32_t i = sa[B.base + j] - B.base;
-    if (i == 0) orig = (int)j;
-    const uint8_t ll = u2s[d[i == 0 ? n - 1 : i - 1]];
-    if (yy[0] == ll) {
-      zpend++;
-      continue;
-    }
-    if (zpend > 0) flush_zeros();
-    uint8_t tmp = yy[1];
-    yy[1] = yy[0];
-    int k = 1;
-    while (ll != tmp) {
-      ++k;
-      const uint8_t t2 = tmp;
-      tmp = yy[k];
-      yy[k] = t2;
-    }
-    yy[0] = tmp;
-    out[wr++] = (uint16_t)(k + 1);  // position k in the MTF list -> symbol k + 1
-    freq[k + 1]++;
+constexpr int kMtfWarps = 4;
+
+__device__ __forceinline__ uint32_t byte_match(uint64_t w, uint32_t s) {
+  // mask of bytes of w equal to s (bit k set for byte k)
+  const uint32_t lo = __vcmpeq4((uint32_t)w, s * 0x01010101u);
+  const uint32_t hi = __vcmpeq4((uint32_t)(w >> 32), s * 0x01010101u);
+  const uint64_t m = ((uint64_t)hi << 32) | lo;        // 0xFF per matching byte
+  return (uint32_t)(__popcll(m & 0x0101010101010101ull) ? (__ffsll(m) - 1) / 8 + 1 : 0);
+}
+
+// Segment-parallel form: the MTF list at any position is "symbols by most
+// recent occurrence, then the never-seen ones in symbol order", so each
+// segment of kMtfSeg symbols starts from a list built out of the last
+// occurrences before it (a prefix max over the block's segments) and runs
+// on its own warp, emitting ranks.  Zero-run coding is then vectorised: a
+// nonzero rank knows the zero run before it from a max-scan of nonzero
+// positions, its output count (bijective base-2 digits + 1) is scanned into
+// offsets, and every position writes its own symbols.
+
+constexpr int kMtfSeg = 8192;
+
+__device__ __forceinline__ int find_seg(const uint32_t *seg0, int nb, uint32_t s) {
+  int lo = 0, hi = nb;  // seg0 has nb + 1 entries; last t with seg0[t] <= s
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (seg0[mid] <= s) lo = mid; else hi = mid;
   }
-  if (zpend > 0) flush_zeros();
-  out[wr++] = (uint16_t)eob;
-  freq[eob]++;
-  B.n_mtf = (int32_t)wr;
-  B.n_in_use = nin;
-  B.orig = orig;
-  uint32_t *fo = freq_out + (size_t)ids[t] * kMaxAlpha;
-  for (int i = 0; i < kMaxAlpha; ++i) fo[i] = freq[i];
+  return lo;
+}
+
+__device__ __forceinline__ void symbol_map(const Block &B, uint8_t *u2s, int lane, int &nin) {
+  nin = 0;
+  for (int base = 0; base < 256; base += 32) {
+    const int c = base + lane;
+    const bool used = (B.in_use[c >> 5] >> (c & 31)) & 1u;
+    const uint32_t m = __ballot_sync(0xffffffffu, used);
+    if (used) u2s[c] = (uint8_t)(nin + __popc(m & ((1u << lane) - 1u)));
+    nin += __popc(m);
+  }
+  __syncwarp();
+}
+
+// C1: BWT column as symbols (makeMaps_e numbering), last occurrence of every
+// symbol per segment, origPtr
+__global__ void __launch_bounds__(32 * kMtfWarps) mtf_gather_kernel(Block *blocks, const int *ids, int nb,
+                                                                     const uint32_t *seg0, const uint32_t *sa,
+                                                                     const uint8_t *rle, uint8_t *symseq,
+                                                                     int32_t *lastpos) {
+  __shared__ uint8_t s_u2s[kMtfWarps][256];
+  __shared__ int32_t s_last[kMtfWarps][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t sg = blockIdx.x * kMtfWarps + warp;
+  if (sg >= seg0[nb]) return;
+  const int t = find_seg(seg0, nb, sg);
+  Block &B = blocks[ids[t]];
+  const uint32_t k = sg - seg0[t];
+  uint8_t *u2s = s_u2s[warp];
+  int32_t *last = s_last[warp];
+  int nin;
+  symbol_map(B, u2s, lane, nin);
+  if (k == 0 && lane == 0) B.n_in_use = nin;
+  for (int x = lane; x < 256; x += 32) last[x] = -1;
+  __syncwarp();
+  const uint32_t n = (uint32_t)B.n;
+  const uint32_t j0 = k * kMtfSeg, j1 = min(n, j0 + kMtfSeg);
+  const uint8_t *d = rle + B.rle_off;
+  for (uint32_t j = j0 + lane; j < j1; j += 32) {
+    const uint32_t i = sa[B.base + j] - B.base;
+    if (i == 0) B.orig = (int32_t)j;
+    const uint8_t sym = u2s[d[i == 0 ? n - 1 : i - 1]];
+    symseq[B.base + j] = sym;
+    atomicMax(&last[sym], (int32_t)j);
+  }
+  __syncwarp();
+  for (int x = lane; x < 256; x += 32) lastpos[(size_t)sg * 256 + x] = last[x];
+}
+
+// C2: last occurrence before each segment (one CTA of 256 per block)
+__global__ void mtf_prefix_kernel(const uint32_t *seg0, int32_t *lastpos) {
+  const int x = threadIdx.x;
+  int32_t run = -1;
+  for (uint32_t sg = seg0[blockIdx.x]; sg < seg0[blockIdx.x + 1]; ++sg) {
+    const int32_t v = lastpos[(size_t)sg * 256 + x];
+    lastpos[(size_t)sg * 256 + x] = run;   // now: last occurrence BEFORE the segment
+    run = max(run, v);
+  }
+}
+
+// C3: MTF ranks of one segment (warp), list in registers
+__global__ void __launch_bounds__(32 * kMtfWarps) mtf_rank_kernel(const Block *blocks, const int *ids, int nb,
+                                                                   const uint32_t *seg0, const uint8_t *symseq,
+                                                                   const int32_t *before, uint8_t *ranks) {
+  __shared__ int32_t s_bef[kMtfWarps][256];
+  __shared__ uint8_t s_at[kMtfWarps][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t sg = blockIdx.x * kMtfWarps + warp;
+  if (sg >= seg0[nb]) return;
+  const int t = find_seg(seg0, nb, sg);
+  const Block &B = blocks[ids[t]];
+  const uint32_t k = sg - seg0[t];
+  int32_t *bef = s_bef[warp];
+  uint8_t *at = s_at[warp];
+  int seen_mine = 0;
+  for (int x = lane; x < 256; x += 32) {
+    bef[x] = before[(size_t)sg * 256 + x];
+    seen_mine += bef[x] >= 0;
+  }
+  int nseen = seen_mine;
+  for (int o = 16; o > 0; o >>= 1) nseen += __shfl_xor_sync(0xffffffffu, nseen, o);
+  __syncwarp();
+  for (int x = lane; x < 256; x += 32) {  // initial list position of symbol x
+    const int32_t bx = bef[x];
+    int pos = 0;
+    if (bx >= 0) {
+      for (int y = 0; y < 256; ++y) pos += bef[y] > bx;
+    } else {
+      pos = nseen;
+      for (int y = 0; y < x; ++y) pos += bef[y] < 0;
+    }
+    at[pos] = (uint8_t)x;
+  }
+  __syncwarp();
+  uint64_t lst = 0;
+  for (int q = 0; q < 8; ++q) lst |= (uint64_t)at[8 * lane + q] << (8 * q);
+  const uint32_t n = (uint32_t)B.n;
+  const uint32_t j0 = k * kMtfSeg, j1 = min(n, j0 + kMtfSeg);
+  for (uint32_t jb = j0; jb < j1; jb += 32) {
+    const uint32_t j = jb + lane;
+    const uint32_t sym = j < j1 ? symseq[B.base + j] : 0u;
+    const int cnt = (int)min(32u, j1 - jb);
+    uint32_t myrank = 0;
+    for (int q = 0; q < cnt; ++q) {
+      const uint32_t s = __shfl_sync(0xffffffffu, sym, q);
+      const uint32_t k1 = byte_match(lst, s);
+      const uint32_t ball = __ballot_sync(0xffffffffu, k1 != 0);
+      const int pl = __ffs(ball) - 1;
+      const int pk = (int)__shfl_sync(0xffffffffu, k1, pl) - 1;
+      const uint32_t top = (uint32_t)(lst >> 56);
+      uint32_t carry = __shfl_up_sync(0xffffffffu, top, 1);
+      if (lane == 0) carry = s;
+      if (lane < pl) {
+        lst = (lst << 8) | carry;
+      } else if (lane == pl) {
+        const uint64_t keep = pk == 7 ? 0ull : (~0ull << (8 * (pk + 1)));
+        lst = (((lst << 8) | carry) & ~keep) | (lst & keep);
+      }
+      if (lane == q) myrank = (uint32_t)(8 * pl + pk);
+    }
+    if (j < j1) ranks[B.base + j] = (uint8_t)myrank;
+  }
+}
+
+__device__ __forceinline__ uint32_t run_digits(uint32_t L) { return L ? 31u - __clz(L + 1u) : 0u; }
+
+// C4: zero-run coding
+__global__ void nz_pos_kernel(const uint8_t *ranks, uint32_t N, uint32_t *P) {
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < N; g += gridDim.x * blockDim.x)
+    P[g] = ranks[g] ? g + 1 : 0u;
+}
+
+__device__ __forceinline__ uint32_t zeros_before(const uint32_t *P, uint32_t g, uint32_t base) {
+  // zero ranks strictly between the previous nonzero rank of the block (or
+  // its start) and g
+  const uint32_t pp = g > base ? P[g - 1] : 0u;
+  const int64_t prev = pp > base ? (int64_t)pp - 1 : (int64_t)base - 1;
+  return (uint32_t)((int64_t)g - prev - 1);
+}
+
+__global__ void run_count_kernel(const uint8_t *ranks, const uint32_t *P, const uint32_t *block_of,
+                                 const Block *blocks, uint32_t N, uint32_t *cnt) {
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g <= N; g += gridDim.x * blockDim.x) {
+    if (g == N) { cnt[g] = 0; continue; }
+    if (!ranks[g]) { cnt[g] = 0; continue; }
+    const uint32_t base = blocks[block_of[g]].base;
+    cnt[g] = run_digits(zeros_before(P, g, base)) + 1;
+  }
+}
+
+__device__ __forceinline__ uint16_t *put_run(uint16_t *o, uint32_t L) {
+  if (!L) return o;
+  uint32_t z = L - 1;
+  for (;;) {
+    *o++ = (z & 1) ? 1 : 0;  // RUNB : RUNA
+    if (z < 2) break;
+    z = (z - 2) / 2;
+  }
+  return o;
+}
+
+__global__ void run_write_mtf_kernel(const uint8_t *ranks, const uint32_t *P, const uint32_t *off,
+                                     const uint32_t *block_of, const Block *blocks, uint32_t N,
+                                     uint16_t *mtfv) {
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < N; g += gridDim.x * blockDim.x) {
+    const uint32_t r = ranks[g];
+    if (!r) continue;
+    const Block &B = blocks[block_of[g]];
+    uint16_t *o = mtfv + B.mtf_off + (off[g] - off[B.base]);
+    o = put_run(o, zeros_before(P, g, B.base));
+    *o = (uint16_t)(r + 1);
+  }
+}
+
+// tail (zero run before EOB, EOB) and symbol frequencies: one CTA per block
+__global__ void mtf_tail_freq_kernel(Block *blocks, const int *ids, const uint32_t *P, const uint32_t *off,
+                                     uint16_t *mtfv, uint32_t *freq_out) {
+  __shared__ uint32_t hist[8][kMaxAlpha];
+  __shared__ int32_t s_nmtf;
+  Block &B = blocks[ids[blockIdx.x]];
+  if (B.tie) return;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 8 * kMaxAlpha; i += blockDim.x) (&hist[0][0])[i] = 0;
+  if (threadIdx.x == 0) {
+    const uint32_t last = B.base + (uint32_t)B.n - 1;
+    const uint32_t pp = P[last];
+    const int64_t prev = pp > B.base ? (int64_t)pp - 1 : (int64_t)B.base - 1;
+    const uint32_t L = (uint32_t)((int64_t)last - prev);
+    const uint32_t w = off[B.base + B.n] - off[B.base];
+    uint16_t *o = put_run(mtfv + B.mtf_off + w, L);
+    *o = (uint16_t)(B.n_in_use + 1);     // EOB
+    s_nmtf = (int32_t)(o + 1 - (mtfv + B.mtf_off));
+  }
+  __syncthreads();
+  const int n_mtf = s_nmtf;
+  const uint16_t *mv = mtfv + B.mtf_off;
+  for (int i = threadIdx.x; i < n_mtf; i += blockDim.x) atomicAdd(&hist[warp][mv[i]], 1u);
+  __syncthreads();
+  for (int v = threadIdx.x; v < kMaxAlpha; v += blockDim.x) {
+    uint32_t c = 0;
+    for (int w = 0; w < 8; ++w) c += hist[w][v];
+    freq_out[(size_t)ids[blockIdx.x] * kMaxAlpha + v] = c;
+  }
+  if (threadIdx.x == 0) B.n_mtf = n_mtf;
 }
 
 // ---------------------------------------------------------------------------
@@ -635,7 +942,7 @@ struct Scratch {  // grow-only device buffers, one set per host thread
     void *p = nullptr;
     size_t cap = 0;
   };
-  Buf b[32];
+  Buf b[40];
   template <typename T>
   int get(int slot, size_t count, T **out) {
     Buf &x = b[slot];
@@ -723,6 +1030,35 @@ int sort_rotations(Block *d_blocks, const int *d_ids, int nb, int nslots, const 
   return PCBZ_OK;
 }
 
+// c_zero_shift[k] = matrix of "append 2^k zero bytes" to the CRC register
+int upload_zero_shift(cudaStream_t st) {
+  static bool done = false;
+  if (done) return PCBZ_OK;
+  uint32_t tab[256];
+  for (uint32_t i = 0; i < 256; ++i) {
+    uint32_t c = i << 24;
+    for (int k = 0; k < 8; ++k) c = (c & 0x80000000u) ? (c << 1) ^ 0x04C11DB7u : (c << 1);
+    tab[i] = c;
+  }
+  static uint32_t P[32][32];
+  for (int b = 0; b < 32; ++b) {
+    const uint32_t v = 1u << b;
+    P[0][b] = (v << 8) ^ tab[v >> 24];
+  }
+  auto apply = [](const uint32_t *M, uint32_t v) {
+    uint32_t r = 0;
+    for (int b = 0; b < 32; ++b)
+      if (v & (1u << b)) r ^= M[b];
+    return r;
+  };
+  for (int k = 1; k < 32; ++k)
+    for (int b = 0; b < 32; ++b) P[k][b] = apply(P[k - 1], apply(P[k - 1], 1u << b));
+  BZ_TRY(cudaMemcpyToSymbolAsync(c_zero_shift, P, sizeof P, 0, cudaMemcpyHostToDevice, st));
+  BZ_TRY(cudaStreamSynchronize(st));
+  done = true;
+  return PCBZ_OK;
+}
+
 size_t job_bound(int64_t len) { return (size_t)((len + len / 100 + 1024 + 3) & ~(int64_t)3); }
 
 // Code jobs held in device memory (in_off: host array of njobs + 1 offsets
@@ -734,36 +1070,73 @@ int compress_jobs(const uint8_t *d_in, const int64_t *in_off, int njobs, uint8_t
   if (njobs <= 0) return PCBZ_OK;
   for (int j = 0; j < njobs; ++j)
     if (in_off[j + 1] < in_off[j]) return bz_fail(PCBZ_E_INVALID, "job offsets must be non-decreasing");
+  if (int rc0 = upload_zero_shift(st)) return rc0;
   // ---- A: RLE1 + block split ---------------------------------------------------
+  const int64_t base_off = in_off[0];
+  const int64_t total = in_off[njobs] - base_off;
+  if (total >= ((int64_t)1 << 31)) return bz_fail(PCBZ_E_INVALID, "bzip2 batch too large: split the jobs");
+  d_in += base_off;
+  std::vector<int64_t> rel(njobs + 1);
+  for (int j = 0; j <= njobs; ++j) rel[j] = in_off[j] - base_off;
   std::vector<Job> jobs(njobs);
-  int64_t rle_total = 0;
   int nslots = 0;
   for (int j = 0; j < njobs; ++j) {
     Job &J = jobs[j];
-    J.in_off = in_off[j];
-    J.in_len = in_off[j + 1] - in_off[j];
-    J.rle_off = rle_total;
-    const int64_t cap = J.in_len + J.in_len / 4 + 64;
-    rle_total += (cap + 15) & ~(int64_t)15;
+    J.in_off = rel[j];
+    J.in_len = rel[j + 1] - rel[j];
+    J.rle_off = 0;
     J.block0 = nslots;
-    nslots += (int)(cap / kBlockMax) + 2;
+    nslots += (int)((J.in_len + J.in_len / 4 + 64) / kBlockMax) + 2;
     J.nblocks = 0;
   }
-  if (rle_total >= ((int64_t)1 << 31)) return bz_fail(PCBZ_E_INVALID, "bzip2 batch too large: split the jobs");
+  nslots = std::max(nslots, 1);
   Job *d_jobs;
   Block *d_blocks;
-  uint8_t *d_rle;
+  uint8_t *d_rle, *d_flags;
+  int64_t *d_rel;
+  uint32_t *d_rs, *d_iota, *d_osz, *d_acc, *d_chunk0;
+  int *d_cnt;
   int rc;
+  const int64_t T = std::max<int64_t>(total, 1);
   if ((rc = g_scr.get(0, njobs, &d_jobs)) || (rc = g_scr.get(1, nslots, &d_blocks)) ||
-      (rc = g_scr.get(2, (size_t)rle_total, &d_rle)))
+      (rc = g_scr.get(2, (size_t)(T + T / 4 + 64), &d_rle)) || (rc = g_scr.get(25, T, &d_flags)) ||
+      (rc = g_scr.get(26, njobs + 1, &d_rel)) || (rc = g_scr.get(27, T + 1, &d_rs)) ||
+      (rc = g_scr.get(28, T + 1, &d_iota)) || (rc = g_scr.get(29, T + 1, &d_osz)) ||
+      (rc = g_scr.get(30, 1, &d_cnt)))
     return rc;
   BZ_TRY(cudaMemcpyAsync(d_jobs, jobs.data(), njobs * sizeof(Job), cudaMemcpyHostToDevice, st));
-  rle1_kernel<<<(njobs + 63) / 64, 64, 0, st>>>(d_in, d_jobs, njobs, d_rle, d_blocks);
-  BZ_TRY(cudaGetLastError());
+  BZ_TRY(cudaMemcpyAsync(d_rel, rel.data(), (njobs + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  uint32_t R = 0;
+  if (total > 0) {
+    run_flags_kernel<<<grid_of(total), 256, 0, st>>>(d_in, total, d_flags);
+    job_start_flags_kernel<<<(njobs + 127) / 128, 128, 0, st>>>(d_rel, njobs, d_flags);
+    iota64_kernel<<<grid_of(total), 256, 0, st>>>(d_iota, total);
+    size_t tb = 0;
+    BZ_TRY(cub::DeviceSelect::Flagged(nullptr, tb, d_iota, d_flags, d_rs, d_cnt, (int)total, st));
+    uint8_t *d_tmp;
+    if ((rc = g_scr.get(17, tb, &d_tmp))) return rc;
+    BZ_TRY(cub::DeviceSelect::Flagged(d_tmp, tb, d_iota, d_flags, d_rs, d_cnt, (int)total, st));
+    int h_cnt = 0;
+    BZ_TRY(cudaMemcpyAsync(&h_cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+    BZ_TRY(cudaStreamSynchronize(st));
+    R = (uint32_t)h_cnt;
+    run_sizes_kernel<<<grid_of(R), 256, 0, st>>>(d_rs, R, (uint32_t)total, d_osz);
+    BZ_TRY(cudaMemsetAsync(d_osz + R, 0, sizeof(uint32_t), st));
+    tb = 0;
+    BZ_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, d_osz, d_iota, R + 1, st));
+    if ((rc = g_scr.get(17, tb, &d_tmp))) return rc;
+    BZ_TRY(cub::DeviceScan::ExclusiveSum(d_tmp, tb, d_osz, d_iota, R + 1, st));   // d_iota := ocum
+    split_kernel<<<(njobs + 127) / 128, 128, 0, st>>>(d_rel, njobs, d_rs, R, (uint32_t)total, d_iota, d_jobs,
+                                                      d_blocks);
+    run_write_kernel<<<grid_of(R), 256, 0, st>>>(d_in, d_rs, R, (uint32_t)total, d_iota, d_rle);
+    BZ_TRY(cudaGetLastError());
+  }
   std::vector<Block> blocks(nslots);
   BZ_TRY(cudaMemcpyAsync(jobs.data(), d_jobs, njobs * sizeof(Job), cudaMemcpyDeviceToHost, st));
   BZ_TRY(cudaMemcpyAsync(blocks.data(), d_blocks, nslots * sizeof(Block), cudaMemcpyDeviceToHost, st));
   BZ_TRY(cudaStreamSynchronize(st));
+  if (total == 0)
+    for (int j = 0; j < njobs; ++j) jobs[j].nblocks = 0;
   std::vector<int> ids;
   int64_t N = 0, mtf_total = 0, sel_total = 0;
   for (int j = 0; j < njobs; ++j)
@@ -795,9 +1168,52 @@ int compress_jobs(const uint8_t *d_in, const int64_t *in_off, int njobs, uint8_t
   if (nb > 0) {
     BZ_TRY(cudaMemcpyAsync(d_ids, ids.data(), nb * sizeof(int), cudaMemcpyHostToDevice, st));
     BZ_TRY(cudaMemcpyAsync(d_blocks, blocks.data(), nslots * sizeof(Block), cudaMemcpyHostToDevice, st));
+    // block CRCs (chunked) and used-symbol maps
+    std::vector<uint32_t> chunk0(nb + 1, 0);
+    for (int t = 0; t < nb; ++t) {
+      const Block &B = blocks[ids[t]];
+      chunk0[t + 1] = chunk0[t] + (B.in_end - B.in_begin + kCrcChunk - 1) / kCrcChunk;
+    }
+    if ((rc = g_scr.get(31, nb + 1, &d_chunk0)) || (rc = g_scr.get(32, nb, &d_acc))) return rc;
+    BZ_TRY(cudaMemcpyAsync(d_chunk0, chunk0.data(), (nb + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    BZ_TRY(cudaMemsetAsync(d_acc, 0, nb * sizeof(uint32_t), st));
+    crc_chunks_kernel<<<(chunk0[nb] + 127) / 128, 128, 0, st>>>(d_in, d_blocks, d_ids, d_chunk0, nb, d_acc);
+    block_meta_kernel<<<nb, 256, 0, st>>>(d_rle, d_blocks, d_ids, d_acc);
+    BZ_TRY(cudaGetLastError());
     // ---- B, C, D ---------------------------------------------------------------
     if ((rc = sort_rotations(d_blocks, d_ids, nb, nslots, d_rle, (uint32_t)N, sa, st))) return rc;
-    mtf_kernel<<<(nb + 63) / 64, 64, 0, st>>>(d_blocks, d_ids, nb, sa, d_rle, mtfv, freq);
+    // ---- C: MTF + zero-run coding --------------------------------------------
+    {
+      std::vector<uint32_t> seg0(nb + 1, 0);
+      for (int t = 0; t < nb; ++t) seg0[t + 1] = seg0[t] + (uint32_t)((blocks[ids[t]].n + kMtfSeg - 1) / kMtfSeg);
+      const uint32_t nseg = seg0[nb];
+      uint32_t *d_seg0, *P, *cnt, *block_of;
+      uint8_t *symseq, *ranks;
+      int32_t *lastpos;
+      if ((rc = g_scr.get(33, nb + 1, &d_seg0)) || (rc = g_scr.get(34, N, &symseq)) ||
+          (rc = g_scr.get(35, N, &ranks)) || (rc = g_scr.get(36, (size_t)nseg * 256, &lastpos)) ||
+          (rc = g_scr.get(37, N, &P)) || (rc = g_scr.get(38, N + 1, &cnt)) || (rc = g_scr.get(4, N, &block_of)))
+        return rc;
+      BZ_TRY(cudaMemcpyAsync(d_seg0, seg0.data(), (nb + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+      const int gw = (int)((nseg + kMtfWarps - 1) / kMtfWarps);
+      mtf_gather_kernel<<<gw, 32 * kMtfWarps, 0, st>>>(d_blocks, d_ids, nb, d_seg0, sa, d_rle, symseq, lastpos);
+      mtf_prefix_kernel<<<nb, 256, 0, st>>>(d_seg0, lastpos);
+      mtf_rank_kernel<<<gw, 32 * kMtfWarps, 0, st>>>(d_blocks, d_ids, nb, d_seg0, symseq, lastpos, ranks);
+      nz_pos_kernel<<<grid_of(N), 256, 0, st>>>(ranks, (uint32_t)N, P);
+      size_t tb = 0;
+      uint8_t *d_tmp;
+      BZ_TRY(cub::DeviceScan::InclusiveScan(nullptr, tb, P, P, MaxOp(), (uint32_t)N, st));
+      if ((rc = g_scr.get(17, tb, &d_tmp))) return rc;
+      BZ_TRY(cub::DeviceScan::InclusiveScan(d_tmp, tb, P, P, MaxOp(), (uint32_t)N, st));
+      run_count_kernel<<<grid_of(N + 1), 256, 0, st>>>(ranks, P, block_of, d_blocks, (uint32_t)N, cnt);
+      tb = 0;
+      BZ_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, cnt, (uint32_t)N + 1, st));
+      if ((rc = g_scr.get(17, tb, &d_tmp))) return rc;
+      BZ_TRY(cub::DeviceScan::ExclusiveSum(d_tmp, tb, cnt, cnt, (uint32_t)N + 1, st));
+      run_write_mtf_kernel<<<grid_of(N), 256, 0, st>>>(ranks, P, cnt, block_of, d_blocks, (uint32_t)N, mtfv);
+      mtf_tail_freq_kernel<<<nb, 256, 0, st>>>(d_blocks, d_ids, P, cnt, mtfv, freq);
+      BZ_TRY(cudaGetLastError());
+    }
     tables_kernel<<<nb, kTableThreads, 0, st>>>(d_blocks, d_ids, mtfv, freq, selectors, sel_mtf, tables);
     BZ_TRY(cudaGetLastError());
     BZ_TRY(cudaMemcpyAsync(blocks.data(), d_blocks, nslots * sizeof(Block), cudaMemcpyDeviceToHost, st));
