@@ -188,6 +188,22 @@ PCBZ_API int pcbz_bzip2_device(const uint8_t *d_in, const int64_t *in_off, int n
                       void *stream);
 PCBZ_API const char *pcbz_bzip2_last_error(void);
 
+/* The reference's per-frame compress loop up to the container
+ * (pipeline.py:85-108 + blocks.py:73-81) on the device: judge (or, with
+ * sel_in != NULL, the given predictor bytes -- CompressOptions.forced),
+ * emission and bzip2 of every (frame, block) pair, block = block_size bytes
+ * of the frame's stream; only ent_out / sel_out and the payloads return.
+ * Payload (f, b) is out[out_start[i] .. + out_len[i]), i = f * nb + b,
+ * nb = ceil(2*h*w / block_size); raw_flag[i] = 1 marks an exactly periodic
+ * block returned RAW for the caller's libbzip2 (see pcbz_bzip2_host).
+ * out_cap >= pcbz_compress_bound(nframes, h, w, block_size). */
+PCBZ_API size_t pcbz_compress_bound(int64_t nframes, int64_t h, int64_t w, int64_t block_size);
+PCBZ_API int pcbz_compress_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t nframes,
+                       int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *specs, int k,
+                       int temporal, const uint8_t *sel_in, int64_t block_size, double *ent_out,
+                       uint8_t *sel_out, uint8_t *out, size_t out_cap, int64_t *out_start,
+                       int64_t *out_len, uint8_t *raw_flag);
+
 /* Testing hook: force the number of segments each (frame, candidate) stream
  * is split into (0 = automatic).  Outputs must not depend on it. */
 PCBZ_API int pcbz_set_segment_override(int segments);

@@ -63,6 +63,9 @@ SIGNATURES = {
     "pcbz_bzip2_host": (_c_int, [_vp, _vp, _c_int, _vp, _c_size, _vp, _vp, _vp]),
     "pcbz_bzip2_device": (_c_int, [_vp, _vp, _c_int, _vp, _c_size, _vp, _vp, _vp, _vp]),
     "pcbz_bzip2_last_error": (ctypes.c_char_p, []),
+    "pcbz_compress_bound": (_c_size, [_c_i64, _c_i64, _c_i64, _c_i64]),
+    "pcbz_compress_host": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _c_int,
+                                    _c_int, _vp, _c_i64, _vp, _vp, _vp, _c_size, _vp, _vp, _vp]),
     "pcbz_set_segment_override": (_c_int, [_c_int]),
     "pcbz_set_profiling": (_c_int, [_c_int]),
     "pcbz_set_item_trace": (_c_int, [_c_int]),

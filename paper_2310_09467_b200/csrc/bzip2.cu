@@ -1061,6 +1061,8 @@ int upload_zero_shift(cudaStream_t st) {
 
 size_t job_bound(int64_t len) { return (size_t)((len + len / 100 + 1024 + 3) & ~(int64_t)3); }
 
+const char *last_error() { return g_bz_err.c_str(); }
+
 // Code jobs held in device memory (in_off: host array of njobs + 1 offsets
 // into d_in).  Job j's bytes land at d_out + out_start[j] (4-byte aligned),
 // out_len[j] bytes; host_needed[j] = 1 marks a job left to the host libbz2

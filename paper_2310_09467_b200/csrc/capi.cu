@@ -904,3 +904,119 @@ int64_t pcbz_item_trace(uint64_t *out, int64_t max_items, int *segments) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// judge + emission + bzip2 on the device: pipeline.py:85-108 end to end, only
+// the compressed payloads come back
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+size_t pcbz_compress_bound(int64_t nframes, int64_t h, int64_t w, int64_t block_size) {
+  if (nframes < 1 || h < 1 || w < 1 || block_size < 1) return 0;
+  const int64_t sb = 2 * h * w, nb = (sb + block_size - 1) / block_size;
+  size_t b = 0;
+  for (int64_t k = 0; k < nb; ++k) b += bz::job_bound(std::min(block_size, sb - k * block_size));
+  return b * (size_t)nframes;
+}
+
+int pcbz_compress_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t nframes, int64_t h,
+                       int64_t w, int64_t px, int64_t py, const uint8_t *specs, int k, int temporal,
+                       const uint8_t *sel_in, int64_t block_size, double *ent_out, uint8_t *sel_out,
+                       uint8_t *out, size_t out_cap, int64_t *out_start, int64_t *out_len,
+                       uint8_t *raw_flag) {
+  int rc = validate_geometry(h, w, px, py);
+  if (rc) return rc;
+  if (nframes < 1) return fail(PCBZ_E_INVALID, "at least one frame is required");
+  if (block_size < 1) return fail(PCBZ_E_INVALID, "block_size must be >= 1, got %lld", (long long)block_size);
+  if (sel_in && (rc = check_sel(sel_in, nframes, halo_prev != nullptr))) return rc;
+  HostCtx &c = g_ctx;
+  if ((rc = c.init())) return rc;
+  const int64_t npix = h * w, sb = 2 * npix;
+  const int64_t nbf = (sb + block_size - 1) / block_size;     // blocks per frame
+  if (out_cap < pcbz_compress_bound(nframes, h, w, block_size))
+    return fail(PCBZ_E_INVALID, "output buffer smaller than pcbz_compress_bound");
+  // frames per device round: streams of at most 1 GiB (bzip2 batch limit)
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nframes, ((int64_t)1 << 30) / sb));
+  cudaStream_t st = c.stream;
+  if (halo_prev) {
+    if ((rc = c.prev.ensure((size_t)npix * 2))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c.prev.p, halo_prev, (size_t)npix * 2, cudaMemcpyHostToDevice, st));
+  }
+  size_t used = 0;
+  std::vector<int64_t> in_off, o_start, o_len;
+  std::vector<uint8_t> host_need;
+  for (int64_t a = 0; a < nframes; a += chunk) {
+    const int64_t n = std::min(chunk, nframes - a);
+    const size_t fb = (size_t)n * npix * 2;
+    // the previous frame of this chunk's first frame: halo, or frame a-1
+    // (kept in c.prev from the previous round)
+    const bool have_prev = a > 0 ? true : halo_prev != nullptr;
+    if ((rc = c.frames.ensure(fb)) || (rc = c.stream_out.ensure((size_t)n * sb)) ||
+        (rc = c.ent.ensure((size_t)n * std::max(k, 1) * 8)) || (rc = c.sel.ensure((size_t)n)) ||
+        (rc = c.out.ensure(pcbz_compress_bound(n, h, w, block_size))))
+      return rc;
+    CUDA_TRY(cudaMemcpyAsync(c.frames.p, frames + (size_t)a * npix, fb, cudaMemcpyHostToDevice, st));
+    const uint16_t *d_prev = have_prev ? c.prev.as<uint16_t>() : nullptr;
+    if (sel_in) {
+      CUDA_TRY(cudaMemcpyAsync(c.sel.p, sel_in + a, (size_t)n, cudaMemcpyHostToDevice, st));
+      EmitParams ep{c.frames.as<uint16_t>(), d_prev, n, npix, (int)h, (int)w, (int)px, (int)py,
+                    c.sel.as<uint8_t>(), c.stream_out.as<uint8_t>(), 0, npix};
+      CUDA_TRY(launch_emit_any(ep, st));
+    } else {
+      Plan pl;
+      rc = make_plan(n, h, w, px, py, specs, k, a > 0 ? temporal != 0 : halo_prev != nullptr, temporal, false, pl);
+      if (rc) return rc;
+      if ((rc = c.ws.ensure(pl.ws_bytes))) return rc;
+      rc = run_plan(pl, c.frames.as<uint16_t>(), (a > 0 && temporal) || (a == 0 && halo_prev) ? d_prev : nullptr,
+                    c.ent.as<double>(), c.sel.as<uint8_t>(), c.stream_out.as<uint8_t>(), nullptr, c.ws.p, st);
+      if (rc) return rc;
+      CUDA_TRY(cudaMemcpyAsync(ent_out + a * k, c.ent.p, (size_t)n * k * 8, cudaMemcpyDeviceToHost, st));
+      rc = check_err_flag(pl, c.ws.p, st);
+      if (rc) return rc;
+    }
+    CUDA_TRY(cudaMemcpyAsync(sel_out + a, c.sel.p, (size_t)n, cudaMemcpyDeviceToHost, st));
+    // the last frame of this round is the next round's previous frame
+    if ((rc = c.prev.ensure((size_t)npix * 2))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c.prev.p, c.frames.as<uint16_t>() + (size_t)(n - 1) * npix, (size_t)npix * 2,
+                             cudaMemcpyDeviceToDevice, st));
+    // bzip2 of every (frame, block) of the round
+    const int nj = (int)(n * nbf);
+    in_off.assign(nj + 1, 0);
+    for (int64_t f = 0; f < n; ++f)
+      for (int64_t b = 0; b < nbf; ++b) in_off[f * nbf + b] = f * sb + std::min(b * block_size, sb);
+    in_off[nj] = n * sb;
+    o_start.assign(nj, 0);
+    o_len.assign(nj, 0);
+    host_need.assign(nj, 0);
+    const size_t cap = pcbz_compress_bound(n, h, w, block_size);
+    rc = bz::compress_jobs(c.stream_out.as<uint8_t>(), in_off.data(), nj, c.out.as<uint8_t>(), cap,
+                           o_start.data(), o_len.data(), host_need.data(), st);
+    if (rc) return fail(rc, "%s", bz::last_error());
+    size_t coded = 0;
+    for (int j = 0; j < nj; ++j) coded = std::max(coded, (size_t)(o_start[j] + o_len[j]));
+    if (used + coded > out_cap) return fail(PCBZ_E_INVALID, "output buffer too small");
+    if (coded) CUDA_TRY(cudaMemcpy(out + used, c.out.p, coded, cudaMemcpyDeviceToHost));
+    for (int j = 0; j < nj; ++j) {
+      const size_t g = (size_t)(a * nbf + j);
+      raw_flag[g] = host_need[j];
+      if (host_need[j]) {  // periodic block: hand the raw bytes to the caller's libbzip2
+        const size_t len = (size_t)(in_off[j + 1] - in_off[j]);
+        out_start[g] = (int64_t)(used + coded);
+        out_len[g] = (int64_t)len;
+        if (used + coded + len > out_cap) return fail(PCBZ_E_INVALID, "output buffer too small");
+        if (len)
+          CUDA_TRY(cudaMemcpy(out + used + coded, c.stream_out.as<uint8_t>() + in_off[j], len, cudaMemcpyDeviceToHost));
+        coded += len;
+      } else {
+        out_start[g] = (int64_t)used + o_start[j];
+        out_len[g] = o_len[j];
+      }
+    }
+    used += (coded + 3) & ~(size_t)3;
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return PCBZ_OK;
+}
+
+}  // extern "C"

@@ -107,4 +107,11 @@ cudaError_t launch_reconstruct(const uint16_t *res, const uint16_t *halo, int64_
                                uint16_t *out, cudaStream_t st);
 cudaError_t judge_configure();  // one-time smem attribute setup
 
+namespace bz {  // bzip2.cu
+int compress_jobs(const uint8_t *d_in, const int64_t *in_off, int njobs, uint8_t *d_out, size_t out_cap,
+                  int64_t *out_start, int64_t *out_len, uint8_t *host_needed, cudaStream_t st);
+size_t job_bound(int64_t len);
+const char *last_error();
+}  // namespace bz
+
 }  // namespace pcbz

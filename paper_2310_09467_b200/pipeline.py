@@ -36,8 +36,13 @@ class CompressOptions:
     block_size: int = DEFAULT_BLOCK_SIZE
     workers: int = 1
     temporal: bool = True
+    #: "device": bzip2 on the GPU next to the judge (csrc/bzip2.cu, the same
+    #: bytes as libbzip2); "host": bz2.compress on `workers` threads
+    coder: str = "device"
 
     def __post_init__(self):
+        if self.coder not in ("device", "host"):
+            raise ValueError(f"coder must be 'device' or 'host', got {self.coder!r}")
         if self.workers < 1:
             raise ValueError(f"workers must be >= 1, got {self.workers}")
         if self.block_size < 1:
@@ -89,6 +94,41 @@ def judge_volume(vol: np.ndarray, geo: LensletGeometry, codes: list, temporal: b
     return ent, sel, stream
 
 
+def encode_volume(vol: np.ndarray, geo: LensletGeometry, codes, temporal: bool,
+                  halo: np.ndarray | None = None, forced_sel: np.ndarray | None = None,
+                  block_size: int = DEFAULT_BLOCK_SIZE):
+    """Judge (or the forced modes), emission and bzip2 of every (frame, block)
+    on the device (pcbz_compress_host): (ent [F, k] or None, sel [F],
+    payloads [F] of tuples of bzip2 streams).  Blocks the device leaves to
+    libbzip2 (exactly periodic ones) come back raw and are coded here."""
+    F, H, W = vol.shape
+    lib = _lib.load()
+    nb = -(-2 * H * W // block_size)
+    cap = lib.pcbz_compress_bound(F, H, W, block_size)
+    out = np.empty(max(cap, 1), np.uint8)
+    start = np.zeros(F * nb, np.int64)
+    length = np.zeros(F * nb, np.int64)
+    raw = np.zeros(F * nb, np.uint8)
+    spec = None if codes is None else np.array(codes, np.uint8)
+    ent = None if forced_sel is not None else np.empty((F, spec.size), np.float64)
+    sel = np.empty(F, np.uint8)
+    fs = None if forced_sel is None else np.ascontiguousarray(forced_sel, np.uint8)
+    _lib.check(lib.pcbz_compress_host(
+        _lib.ptr(vol), _lib.ptr(halo), F, H, W, geo.pitch_x, geo.pitch_y, _lib.ptr(spec),
+        0 if spec is None else spec.size, 1 if temporal else 0, _lib.ptr(fs), block_size,
+        _lib.ptr(ent), _lib.ptr(sel), out.ctypes.data, cap, start.ctypes.data, length.ctypes.data,
+        raw.ctypes.data))
+    payloads = []
+    for f in range(F):
+        blocks = []
+        for b in range(nb):
+            i = f * nb + b
+            piece = out[start[i]:start[i] + length[i]]
+            blocks.append(bz2_block(piece) if raw[i] else piece.tobytes())
+        payloads.append(tuple(blocks))
+    return ent, sel, payloads
+
+
 def emit_volume(vol: np.ndarray, geo: LensletGeometry, sel: np.ndarray,
                 halo: np.ndarray | None = None) -> np.ndarray:
     F, H, W = vol.shape
@@ -120,6 +160,27 @@ def compress_stack_detailed(stack: FrameStack, opts: CompressOptions | None = No
     specs, reports = [], []
     payloads = [None] * F
     select_s = encode_s = 0.0
+    if opts.coder == "device":
+        coded = {}
+        for a in range(0, F, GPU_CHUNK_FRAMES):
+            b = min(F, a + GPU_CHUNK_FRAMES)
+            halo = vol[a - 1] if (a > 0 and opts.temporal) else None
+            t0 = time.perf_counter()
+            fsel = None
+            if forced is not None:
+                fsel = np.array([forced.to_byte() if (a + i > 0 and opts.temporal) else forced.intra_id
+                                 for i in range(b - a)], np.uint8)
+            ent, sel, pl = encode_volume(np.ascontiguousarray(vol[a:b]), geo, codes, opts.temporal, halo,
+                                         fsel, opts.block_size)
+            encode_s += time.perf_counter() - t0
+            reports += _reports(ent, codes) if forced is None else [None] * (b - a)
+            specs += [PredictorSpec.from_byte(int(c)) for c in sel]
+            for i in range(b - a):
+                coded[a + i] = pl[i]
+        payloads = [CompressedBlocks(BlockPlan(opts.block_size, len(coded[fi])), coded[fi]) for fi in range(F)]
+        data = write_container(stack.width, stack.height, geo.pitch_x, geo.pitch_y, opts.block_size,
+                               list(zip(specs, payloads)))
+        return CompressResult(data, specs, reports, select_s, encode_s)
     pool = ThreadPoolExecutor(max(1, opts.workers))
     futures = []
     try:
@@ -161,6 +222,16 @@ def compress_stack(stack: FrameStack, opts: CompressOptions | None = None) -> by
     return compress_stack_detailed(stack, opts).data
 
 
+class _done:
+    """An already-available result with the Future.result() interface."""
+
+    def __init__(self, value):
+        self.value = value
+
+    def result(self):
+        return self.value
+
+
 @dataclass
 class StreamResult:
     frames: int
@@ -187,6 +258,7 @@ def compress_stream(frames, geometry: LensletGeometry, out, opts: CompressOption
     opts = opts or CompressOptions()
     forced = opts.forced
     codes = None if forced is not None else candidate_codes(opts)
+    injected = judge_fn
     if judge_fn is None:
         def judge_fn(chunk, halo, geo, cands, temporal):
             return judge_volume(chunk, geo, cands, temporal, halo=halo)
@@ -206,11 +278,29 @@ def compress_stream(frames, geometry: LensletGeometry, out, opts: CompressOption
                 writer.add_frame(spec, [f.result() for f in futs])
             wait_s += time.perf_counter() - t0
 
+    device_coder = opts.coder == "device" and injected is None
+
     def run_chunk(buf):
         nonlocal halo, select_s
         chunk = np.ascontiguousarray(np.stack(buf))
         h = halo if opts.temporal else None
         t0 = time.perf_counter()
+        if device_coder:
+            first = nseen - len(buf)
+            fsel = None if forced is None else np.array(
+                [forced.to_byte() if (first + i > 0 and opts.temporal) else forced.intra_id
+                 for i in range(len(buf))], np.uint8)
+            _, sel, pl = encode_volume(chunk, geometry, codes, opts.temporal, h, fsel, opts.block_size)
+            select_s += time.perf_counter() - t0
+            halo = chunk[-1].copy()
+            entry = []
+            for i in range(len(buf)):
+                spec = PredictorSpec.from_byte(int(sel[i]))
+                specs.append(spec)
+                entry.append((spec, [_done(p) for p in pl[i]]))
+            pending.append(entry)
+            drain(max_inflight_chunks - 1)
+            return
         if forced is None:
             _, sel, streams = judge_fn(chunk, h, geometry, codes, opts.temporal)
         else:

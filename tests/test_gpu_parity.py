@@ -444,3 +444,21 @@ def test_workspace_bound_without_halo(F, H, W, codes):
         for c, want in entries:
             assert_entropy(ent[f, sorted(codes).index(c)], want)
         prev = vol[f]
+
+
+@pytest.mark.parametrize("forced", [None, PredictorSpec(True, 3)])
+def test_device_and_host_coders_identical(forced):
+    """CompressOptions.coder: bzip2 on the device (judge + emission + bzip2 in
+    one call, pcbz_compress_host) and on host threads give the same
+    container, equal to the oracle's."""
+    p = SynthParams(256, 200, 15, 15, mode="smooth_lenslet", noise_sigma=20.0, photon_scale=0.05,
+                    frames=5, drift=1.0, seed=9)
+    vol = generate_array(p)
+    geo = LensletGeometry(15, 15)
+    stack = FrameStack(tuple(Frame(f, geo) for f in vol))
+    dev = compress_stack(stack, CompressOptions(forced=forced, block_size=30000, coder="device"))
+    host = compress_stack(stack, CompressOptions(forced=forced, block_size=30000, coder="host", workers=4))
+    assert dev == host
+    want, _ = oracle.compress_stack(vol, 15, 15, forced=None if forced is None else forced.to_byte(),
+                                    block_size=30000)
+    assert sha(dev) == sha(want)
