@@ -248,6 +248,33 @@ def run_reference(args, wl: Workload):
     return 0
 
 
+def pipeline_e2e(wl: Workload, host: np.ndarray) -> dict:
+    """Informational: the whole compressor on this rank's frames --
+    compress_stack (device judge + emission + bzip2, container) and
+    decompress_stack -- wall-clock once after a warm-up, lossless checked."""
+    from paper_2310_09467_b200 import (CompressOptions, Frame, FrameStack, LensletGeometry,
+                                       all_intra_specs, compress_stack_detailed, decompress_stack)
+    from paper_2310_09467_b200.pipeline import GPU_CHUNK_FRAMES
+    geo = LensletGeometry(wl.pitch, wl.pitch)
+    stack = FrameStack(tuple(Frame(f, geo) for f in host))
+    cores = os.cpu_count() or 1
+    opts = CompressOptions(workers=cores, temporal=wl.temporal,
+                           candidates=None if wl.temporal else tuple(all_intra_specs()))
+    compress_stack_detailed(FrameStack(stack.frames[:GPU_CHUNK_FRAMES]), opts)
+    t0 = time.perf_counter()
+    data = compress_stack_detailed(stack, opts).data
+    t_c = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    back = decompress_stack(data, workers=cores)
+    t_d = time.perf_counter() - t0
+    raw = host.nbytes
+    return {"compress_GBps": raw / t_c / 1e9, "decompress_GBps": raw / t_d / 1e9,
+            "compression_ratio": raw / len(data), "lossless": bool(np.array_equal(back.to_array(), host)),
+            "what": "compress_stack (device judge + emission + bzip2 on the GPU, container) and "
+                    f"decompress_stack (bzip2 decode on {cores} host threads, inverse prediction on the "
+                    "GPU), wall clock, informational (not the metric)"}
+
+
 def run_gpu(args, wl: Workload):
     import torch
     import torch.distributed as dist
@@ -406,6 +433,8 @@ def run_gpu(args, wl: Workload):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    if not args.no_pipeline:
+        res["pipeline_e2e"] = pipeline_e2e(wl, host)
     if not args.no_cpu_baseline:
         nf = min(nloc, int(os.environ.get("PCBZ_CPU_SAMPLE_FRAMES", "100")))
         v, dt, nfr = cpu_reference_sample(wl, host[:nf], cores)
@@ -544,6 +573,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true", help="skip the informational pipeline_e2e")
     ap.add_argument("--shard", choices=["frames", "bands"], default="frames",
                     help="N>1: frame shards / replicas (default) or within-frame bands (c1, c4)")
     args = ap.parse_args()
