@@ -434,18 +434,42 @@ int pcbz_judge_device(const uint16_t *d_frames, const uint16_t *d_halo_prev, int
                   d_workspace, static_cast<cudaStream_t>(stream));
 }
 
-// Frames per pipeline chunk of pcbz_judge_host: uploads of chunk i+1,
-// the judge of chunk i and downloads of chunk i-1 overlap on three streams.
-int64_t host_chunk_frames(int64_t nframes) {
-  static const int64_t forced = [] {
-    const char *e = getenv("PCBZ_HOST_CHUNK");
-    return (int64_t)(e ? atoll(e) : 0);
-  }();
-  if (forced > 0) return std::min(forced, nframes);
-  if (nframes < 16) return nframes;  // too few frames to pay for a pipeline
-  // ~10 chunks of >= 8 frames: measured best on C2 (chunk 4/6/8/10/13 frames:
-  // 25.4/32.6/35.8/36.6/35.2 GB/s e2e, profiles/r01_notes.md)
-  return std::max<int64_t>(8, (nframes + 9) / 10);
+// Frame counts of the pipeline chunks of pcbz_judge_host: uploads of chunk
+// i+1, the judge of chunk i and downloads of chunk i-1 overlap on three
+// streams, so the first upload and the last download are exposed.  Base
+// chunks of ~n/10 frames (>= 8) measured best on C2 (4/6/8/10/13 frames:
+// 25.4/32.6/35.8/36.6/35.2 GB/s e2e, profiles/r01_notes.md).  Optional
+// ramps (PCBZ_HOST_RAMP / PCBZ_HOST_RAMP_DOWN: doubling from that many frames
+// at the start / halving to it at the end) shorten the exposed ends;
+// PCBZ_HOST_CHUNK forces the base size.
+std::vector<int64_t> host_chunks(int64_t nframes) {
+  auto env = [](const char *name) -> int64_t {
+    const char *e = getenv(name);
+    return e ? atoll(e) : 0;
+  };
+  static const int64_t forced = env("PCBZ_HOST_CHUNK");
+  static const int64_t ramp = env("PCBZ_HOST_RAMP");            // first chunk size of the ramp-up
+  static const int64_t ramp_down = env("PCBZ_HOST_RAMP_DOWN");  // last chunk size of the ramp-down
+  if (nframes < 16 && forced <= 0) return {nframes};  // too few frames to pay for a pipeline
+  const int64_t base = forced > 0 ? std::min(forced, nframes) : std::max<int64_t>(8, (nframes + 9) / 10);
+  std::vector<int64_t> head, tail, out;
+  int64_t left = nframes;
+  for (int64_t c = ramp; c > 0 && c < base && left >= 4 * c; c *= 2) {
+    head.push_back(c);
+    left -= c;
+  }
+  for (int64_t c = ramp_down; c > 0 && c < base && left >= 4 * c; c *= 2) {
+    tail.push_back(c);
+    left -= c;
+  }
+  out = head;
+  while (left > 0) {
+    const int64_t c = std::min(base, left);
+    out.push_back(c);
+    left -= c;
+  }
+  out.insert(out.end(), tail.rbegin(), tail.rend());
+  return out;
 }
 
 int pcbz_judge_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t nframes, int64_t h,
@@ -459,20 +483,29 @@ int pcbz_judge_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t n
   if (rc) return rc;
   const int64_t npix = h * w;
   const size_t fbytes = (size_t)nframes * npix * 2;
-  const int64_t chunk = host_chunk_frames(nframes);
-  const int64_t nchunks = (nframes + chunk - 1) / chunk;
+  const std::vector<int64_t> sizes = host_chunks(nframes);
+  const int64_t nchunks = (int64_t)sizes.size();
+  std::vector<int64_t> starts(nchunks + 1, 0);
+  for (int64_t i = 0; i < nchunks; ++i) starts[i + 1] = starts[i] + sizes[i];
   // Chunks alternate between two compute streams (one workspace each), so the
   // last, partly filled wave of chunk i overlaps the start of chunk i+1; the
   // segment count is planned for the whole call's pairs accordingly.
-  auto chunk_plan = [&](int64_t a, Plan &pl) {
-    const int64_t n = std::min(chunk, nframes - a);
+  // The last `tail` chunks choose their segment count for their own pairs
+  // (shorter items, so the final judge -- and the download behind it --
+  // finishes sooner); the others plan for the whole call (PCBZ_HOST_TAIL).
+  static const int64_t tail = [] {
+    const char *e = getenv("PCBZ_HOST_TAIL");
+    return (int64_t)(e ? atoll(e) : 0);
+  }();
+  auto chunk_plan = [&](int64_t i, Plan &pl) {
+    const int64_t a = starts[i], n = sizes[i];
     return make_plan(n, h, w, px, py, specs, k, a > 0 ? temporal != 0 : halo_prev != nullptr,
-                     temporal, false, pl, 1, 0, full.jp.npairs);
+                     temporal, false, pl, 1, 0, i >= nchunks - tail ? 0 : full.jp.npairs);
   };
   size_t ws_bytes = 0;
-  for (int64_t a = 0; a < nframes; a += chunk) {
+  for (int64_t i = 0; i < nchunks; ++i) {
     Plan pl;
-    if ((rc = chunk_plan(a, pl))) return rc;
+    if ((rc = chunk_plan(i, pl))) return rc;
     ws_bytes = std::max(ws_bytes, pl.ws_bytes);
   }
   ws_bytes = align_up(ws_bytes);
@@ -498,25 +531,36 @@ int pcbz_judge_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t n
   if (halo_prev)
     CUDA_TRY(cudaMemcpyAsync(c.prev.p, halo_prev, (size_t)npix * 2, cudaMemcpyHostToDevice, c.s_in));
   const uint16_t *d_frames = c.frames.as<uint16_t>();
+  // PCBZ_HOST_TRACE=1: per-chunk timeline (upload end, judge end, download
+  // end, ms after the call's first upload) on stderr, for tuning the chunks
+  static const bool trace = getenv("PCBZ_HOST_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  if (trace) {
+    tev.resize(3 * nchunks + 1);
+    for (auto &e : tev) CUDA_TRY(cudaEventCreate(&e));
+    CUDA_TRY(cudaEventRecord(tev[3 * nchunks], c.s_in));
+  }
   for (int64_t i = 0; i < nchunks; ++i) {
-    const int64_t a = i * chunk, n = std::min(chunk, nframes - a);
+    const int64_t a = starts[i], n = sizes[i];
     const size_t off = (size_t)a * npix;
     cudaStream_t st = comp[i & 1];
     char *ws = c.ws.as<char>() + (i & 1) * ws_bytes;
     CUDA_TRY(cudaMemcpyAsync(c.frames.as<uint16_t>() + off, frames + off, (size_t)n * npix * 2,
                              cudaMemcpyHostToDevice, c.s_in));
     CUDA_TRY(cudaEventRecord(ev[2 * i], c.s_in));
+    if (trace) CUDA_TRY(cudaEventRecord(tev[3 * i], c.s_in));
     CUDA_TRY(cudaStreamWaitEvent(st, ev[2 * i], 0));
     // the previous frame of chunk i's first frame: the halo (chunk 0) or frame
     // a-1, uploaded earlier on the same (in-order) copy stream
     const uint16_t *d_halo = a > 0 ? (temporal ? d_frames + off - npix : nullptr)
                                    : (halo_prev ? c.prev.as<uint16_t>() : nullptr);
     Plan pl;
-    if ((rc = chunk_plan(a, pl))) return rc;
+    if ((rc = chunk_plan(i, pl))) return rc;
     rc = run_plan(pl, d_frames + off, d_halo, c.ent.as<double>() + a * k, c.sel.as<uint8_t>() + a,
                   stream_out ? c.stream_out.as<uint8_t>() + 2 * off : nullptr, nullptr, ws, st, d_err);
     if (rc) return rc;
     CUDA_TRY(cudaEventRecord(ev[2 * i + 1], st));
+    if (trace) CUDA_TRY(cudaEventRecord(tev[3 * i + 1], st));
     CUDA_TRY(cudaStreamWaitEvent(c.s_out, ev[2 * i + 1], 0));
     CUDA_TRY(cudaMemcpyAsync(ent_out + a * k, c.ent.as<double>() + a * k, (size_t)n * k * 8,
                              cudaMemcpyDeviceToHost, c.s_out));
@@ -525,9 +569,19 @@ int pcbz_judge_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t n
     if (stream_out)
       CUDA_TRY(cudaMemcpyAsync(stream_out + 2 * off, c.stream_out.as<uint8_t>() + 2 * off,
                                (size_t)n * npix * 2, cudaMemcpyDeviceToHost, c.s_out));
+    if (trace) CUDA_TRY(cudaEventRecord(tev[3 * i + 2], c.s_out));
   }
   int flag = 0;
   CUDA_TRY(cudaStreamSynchronize(c.s_out));  // every chunk's judge precedes its D2H
+  if (trace) {
+    for (int64_t i = 0; i < nchunks; ++i) {
+      float t[3];
+      for (int j = 0; j < 3; ++j) CUDA_TRY(cudaEventElapsedTime(&t[j], tev[3 * nchunks], tev[3 * i + j]));
+      fprintf(stderr, "pcbz_judge_host chunk %lld (%lld frames): up %.3f judged %.3f down %.3f ms\n",
+              (long long)i, (long long)sizes[i], t[0], t[1], t[2]);
+    }
+    for (auto &e : tev) cudaEventDestroy(e);
+  }
   CUDA_TRY(cudaMemcpy(&flag, d_err, 4, cudaMemcpyDeviceToHost));
   for (auto &e : ev) cudaEventDestroy(e);
   if (flag) return fail(PCBZ_E_INTERNAL, "judge kernel reported internal error %d", flag);
