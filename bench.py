@@ -254,13 +254,12 @@ def pipeline_e2e(wl: Workload, host: np.ndarray) -> dict:
     decompress_stack -- wall-clock once after a warm-up, lossless checked."""
     from paper_2310_09467_b200 import (CompressOptions, Frame, FrameStack, LensletGeometry,
                                        all_intra_specs, compress_stack_detailed, decompress_stack)
-    from paper_2310_09467_b200.pipeline import GPU_CHUNK_FRAMES
     geo = LensletGeometry(wl.pitch, wl.pitch)
     stack = FrameStack(tuple(Frame(f, geo) for f in host))
     cores = os.cpu_count() or 1
     opts = CompressOptions(workers=cores, temporal=wl.temporal,
                            candidates=None if wl.temporal else tuple(all_intra_specs()))
-    compress_stack_detailed(FrameStack(stack.frames[:GPU_CHUNK_FRAMES]), opts)
+    compress_stack_detailed(stack, opts)   # warm-up at full size: device buffers sized once
     t0 = time.perf_counter()
     data = compress_stack_detailed(stack, opts).data
     t_c = time.perf_counter() - t0

@@ -43,6 +43,17 @@ extern "C" {
 #endif
 
 PCBZ_API const char *pcbz_version(void);
+
+/* Host memory helpers for the whole-compressor path (no reference
+ * counterpart: they replace the Python-side bytes copies of
+ * pipeline.py:99-113 / container.py:84-106 with page-locked transfers and a
+ * multithreaded join).  pcbz_host_alloc returns page-locked memory (NULL on
+ * failure); pcbz_gather concatenates n pieces into dst with up to `threads`
+ * host threads. */
+PCBZ_API void *pcbz_host_alloc(size_t bytes);
+PCBZ_API int pcbz_host_free(void *p);
+PCBZ_API int pcbz_gather(uint8_t *dst, const uint8_t *const *src, const int64_t *len, int64_t n,
+                         int threads);
 PCBZ_API const char *pcbz_last_error(void);
 /* Number of visible CUDA devices of compute capability 10.x (0 if none). */
 PCBZ_API int pcbz_device_count(void);
@@ -203,6 +214,14 @@ PCBZ_API int pcbz_compress_host(const uint16_t *frames, const uint16_t *halo_pre
                        int temporal, const uint8_t *sel_in, int64_t block_size, double *ent_out,
                        uint8_t *sel_out, uint8_t *out, size_t out_cap, int64_t *out_start,
                        int64_t *out_len, uint8_t *raw_flag);
+/* The same with one pointer per frame (each h*w uint16, C-contiguous), so a
+ * caller holding separate frame arrays (pcbz.FrameStack) needs no stacked
+ * copy of the volume. */
+PCBZ_API int pcbz_compress_frames_host(const uint16_t *const *frames, const uint16_t *halo_prev,
+                       int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py,
+                       const uint8_t *specs, int k, int temporal, const uint8_t *sel_in,
+                       int64_t block_size, double *ent_out, uint8_t *sel_out, uint8_t *out,
+                       size_t out_cap, int64_t *out_start, int64_t *out_len, uint8_t *raw_flag);
 
 /* Testing hook: force the number of segments each (frame, candidate) stream
  * is split into (0 = automatic).  Outputs must not depend on it. */

@@ -66,6 +66,12 @@ SIGNATURES = {
     "pcbz_compress_bound": (_c_size, [_c_i64, _c_i64, _c_i64, _c_i64]),
     "pcbz_compress_host": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _c_int,
                                     _c_int, _vp, _c_i64, _vp, _vp, _vp, _c_size, _vp, _vp, _vp]),
+    "pcbz_compress_frames_host": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp,
+                                           _c_int, _c_int, _vp, _c_i64, _vp, _vp, _vp, _c_size, _vp,
+                                           _vp, _vp]),
+    "pcbz_host_alloc": (_vp, [_c_size]),
+    "pcbz_host_free": (_c_int, [_vp]),
+    "pcbz_gather": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int]),
     "pcbz_set_segment_override": (_c_int, [_c_int]),
     "pcbz_set_profiling": (_c_int, [_c_int]),
     "pcbz_set_item_trace": (_c_int, [_c_int]),
@@ -121,3 +127,66 @@ def version() -> str:
 
 def device_count() -> int:
     return int(load().pcbz_device_count())
+
+
+# ---- host memory helpers (whole-compressor path) ------------------------------
+
+class _PinnedCache(threading.local):
+    """Grow-only page-locked buffer per thread (pcbz_host_alloc): device->host
+    payload copies land in it at PCIe speed.  Valid until the same thread
+    asks for a larger one."""
+
+    def __init__(self):
+        self.addr, self.size = None, 0
+
+    def get(self, nbytes: int) -> np.ndarray:
+        if nbytes > self.size:
+            lib = load()
+            if self.addr:
+                lib.pcbz_host_free(self.addr)
+                self.addr, self.size = None, 0
+            size = max(int(nbytes), 1 << 20)
+            addr = lib.pcbz_host_alloc(size)
+            if not addr:
+                check(PCBZ_E_CUDA)
+            self.addr, self.size = addr, size
+        return np.ctypeslib.as_array((ctypes.c_uint8 * self.size).from_address(self.addr))[:nbytes]
+
+
+_pinned = _PinnedCache()
+
+
+def pinned_buffer(nbytes: int) -> np.ndarray:
+    """This thread's cached page-locked uint8 buffer of at least nbytes."""
+    return _pinned.get(nbytes)
+
+
+_PyBytes_FromStringAndSize = ctypes.pythonapi.PyBytes_FromStringAndSize
+_PyBytes_FromStringAndSize.restype = ctypes.py_object
+_PyBytes_FromStringAndSize.argtypes = [ctypes.c_void_p, ctypes.c_ssize_t]
+_PyBytes_AsString = ctypes.pythonapi.PyBytes_AsString
+_PyBytes_AsString.restype = ctypes.c_void_p
+_PyBytes_AsString.argtypes = [ctypes.py_object]
+
+
+def _address(part) -> int:
+    if isinstance(part, bytes):
+        return _PyBytes_AsString(part)
+    return np.frombuffer(part, np.uint8).ctypes.data
+
+
+def join(parts, threads: int | None = None) -> bytes:
+    """b"".join(parts) for bytes-like parts, the copy done by pcbz_gather on
+    up to `threads` host threads into a fresh bytes object (filled before it
+    is shared, the CPython PyBytes_FromStringAndSize(NULL, n) idiom)."""
+    import os
+    parts = [p for p in parts if len(p)]
+    total = sum(len(p) for p in parts)
+    out = _PyBytes_FromStringAndSize(None, total)
+    n = len(parts)
+    if n:
+        srcs = (ctypes.c_void_p * n)(*[_address(p) for p in parts])
+        lens = np.array([len(p) for p in parts], np.int64)
+        check(load().pcbz_gather(_PyBytes_AsString(out), srcs, lens.ctypes.data, n,
+                                 threads or (os.cpu_count() or 1)))
+    return out

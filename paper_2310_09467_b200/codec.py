@@ -166,9 +166,10 @@ class FrameRecord:
 
 
 def write_container(width: int, height: int, pitch_x: int, pitch_y: int, block_size: int,
-                    frames: Sequence) -> bytes:
+                    frames: Sequence, joiner=None) -> bytes:
     """Header, per-frame records, then payloads in frame/block order
-    (container.py:84-106, FORMAT.md)."""
+    (container.py:84-106, FORMAT.md).  `joiner` replaces b"".join (the
+    device path passes the native multithreaded join, _lib.join)."""
     frames = list(frames)
     if not frames:
         raise ValueError("container must hold at least one frame")
@@ -183,7 +184,7 @@ def write_container(width: int, height: int, pitch_x: int, pitch_y: int, block_s
         parts.append(struct.pack(f"<{len(sizes)}Q", *sizes))
     for _, blocks in frames:
         parts.extend(blocks.payloads)
-    return b"".join(parts)
+    return joiner(parts) if joiner else b"".join(parts)
 
 
 class ContainerWriter:

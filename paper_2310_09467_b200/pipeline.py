@@ -11,6 +11,7 @@ function of (stack, options) and identical to the reference's.
 from __future__ import annotations
 
 import bz2
+import ctypes
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
@@ -94,18 +95,33 @@ def judge_volume(vol: np.ndarray, geo: LensletGeometry, codes: list, temporal: b
     return ent, sel, stream
 
 
-def encode_volume(vol: np.ndarray, geo: LensletGeometry, codes, temporal: bool,
+def encode_volume(vol, geo: LensletGeometry, codes, temporal: bool,
                   halo: np.ndarray | None = None, forced_sel: np.ndarray | None = None,
-                  block_size: int = DEFAULT_BLOCK_SIZE):
+                  block_size: int = DEFAULT_BLOCK_SIZE, views: bool = False):
     """Judge (or the forced modes), emission and bzip2 of every (frame, block)
-    on the device (pcbz_compress_host): (ent [F, k] or None, sel [F],
-    payloads [F] of tuples of bzip2 streams).  Blocks the device leaves to
-    libbzip2 (exactly periodic ones) come back raw and are coded here."""
-    F, H, W = vol.shape
+    on the device (pcbz_compress_host / pcbz_compress_frames_host): (ent [F, k]
+    or None, sel [F], payloads [F] of tuples of bzip2 streams).  `vol` is a
+    [F, H, W] volume or a sequence of [H, W] frames (passed by pointer, never
+    stacked).  Blocks the device leaves to libbzip2 (exactly periodic ones)
+    come back raw and are coded here.  views=True returns the payloads as
+    memoryviews into one output buffer (no per-block copy; the container
+    writer joins them)."""
+    frames = None
+    if isinstance(vol, np.ndarray) and vol.ndim == 3:
+        F, H, W = vol.shape
+        vol = np.ascontiguousarray(vol)
+    else:
+        frames = [np.ascontiguousarray(f, dtype=np.uint16) for f in vol]
+        F = len(frames)
+        H, W = frames[0].shape
+        if any(f.shape != (H, W) for f in frames):
+            raise ValueError("all frames must have the same shape")
     lib = _lib.load()
     nb = -(-2 * H * W // block_size)
     cap = lib.pcbz_compress_bound(F, H, W, block_size)
-    out = np.empty(max(cap, 1), np.uint8)
+    # views: payloads land in this thread's page-locked buffer (valid until
+    # its next views call); otherwise a fresh array the payloads are copied from
+    out = _lib.pinned_buffer(max(cap, 1)) if views else np.empty(max(cap, 1), np.uint8)
     start = np.zeros(F * nb, np.int64)
     length = np.zeros(F * nb, np.int64)
     raw = np.zeros(F * nb, np.uint8)
@@ -113,18 +129,26 @@ def encode_volume(vol: np.ndarray, geo: LensletGeometry, codes, temporal: bool,
     ent = None if forced_sel is not None else np.empty((F, spec.size), np.float64)
     sel = np.empty(F, np.uint8)
     fs = None if forced_sel is None else np.ascontiguousarray(forced_sel, np.uint8)
-    _lib.check(lib.pcbz_compress_host(
-        _lib.ptr(vol), _lib.ptr(halo), F, H, W, geo.pitch_x, geo.pitch_y, _lib.ptr(spec),
-        0 if spec is None else spec.size, 1 if temporal else 0, _lib.ptr(fs), block_size,
-        _lib.ptr(ent), _lib.ptr(sel), out.ctypes.data, cap, start.ctypes.data, length.ctypes.data,
-        raw.ctypes.data))
+    tail = (_lib.ptr(halo), F, H, W, geo.pitch_x, geo.pitch_y, _lib.ptr(spec),
+            0 if spec is None else spec.size, 1 if temporal else 0, _lib.ptr(fs), block_size,
+            _lib.ptr(ent), _lib.ptr(sel), out.ctypes.data, cap, start.ctypes.data, length.ctypes.data,
+            raw.ctypes.data)
+    if frames is None:
+        _lib.check(lib.pcbz_compress_host(_lib.ptr(vol), *tail))
+    else:
+        ptrs = (ctypes.c_void_p * F)(*[f.ctypes.data for f in frames])
+        _lib.check(lib.pcbz_compress_frames_host(ptrs, *tail))
+    mv = memoryview(out)
     payloads = []
     for f in range(F):
         blocks = []
         for b in range(nb):
             i = f * nb + b
-            piece = out[start[i]:start[i] + length[i]]
-            blocks.append(bz2_block(piece) if raw[i] else piece.tobytes())
+            piece = mv[start[i]:start[i] + length[i]]
+            if raw[i]:
+                blocks.append(bz2_block(piece))
+            else:
+                blocks.append(piece if views else piece.tobytes())
         payloads.append(tuple(blocks))
     return ent, sel, payloads
 
@@ -152,35 +176,32 @@ def _reports(ent: np.ndarray, codes: list) -> list:
 def compress_stack_detailed(stack: FrameStack, opts: CompressOptions | None = None) -> CompressResult:
     """Reference pipeline.py:76-113 semantics, batched on the device."""
     opts = opts or CompressOptions()
-    vol = np.ascontiguousarray(stack.to_array())
     geo = stack.geometry
-    F = vol.shape[0]
+    F = stack.frame_count
     forced = opts.forced
     codes = None if forced is not None else candidate_codes(opts)
     specs, reports = [], []
     payloads = [None] * F
     select_s = encode_s = 0.0
     if opts.coder == "device":
-        coded = {}
-        for a in range(0, F, GPU_CHUNK_FRAMES):
-            b = min(F, a + GPU_CHUNK_FRAMES)
-            halo = vol[a - 1] if (a > 0 and opts.temporal) else None
-            t0 = time.perf_counter()
-            fsel = None
-            if forced is not None:
-                fsel = np.array([forced.to_byte() if (a + i > 0 and opts.temporal) else forced.intra_id
-                                 for i in range(b - a)], np.uint8)
-            ent, sel, pl = encode_volume(np.ascontiguousarray(vol[a:b]), geo, codes, opts.temporal, halo,
-                                         fsel, opts.block_size)
-            encode_s += time.perf_counter() - t0
-            reports += _reports(ent, codes) if forced is None else [None] * (b - a)
-            specs += [PredictorSpec.from_byte(int(c)) for c in sel]
-            for i in range(b - a):
-                coded[a + i] = pl[i]
-        payloads = [CompressedBlocks(BlockPlan(opts.block_size, len(coded[fi])), coded[fi]) for fi in range(F)]
+        # one call over frame pointers (the library rounds the volume through
+        # the device in <= 1 GiB pieces); payloads stay views into its output
+        # buffer until the container join copies them once
+        t0 = time.perf_counter()
+        fsel = None
+        if forced is not None:
+            fsel = np.array([forced.to_byte() if (i > 0 and opts.temporal) else forced.intra_id
+                             for i in range(F)], np.uint8)
+        ent, sel, pl = encode_volume([f.samples for f in stack.frames], geo, codes, opts.temporal, None,
+                                     fsel, opts.block_size, views=True)
+        encode_s = time.perf_counter() - t0
+        reports = _reports(ent, codes) if forced is None else [None] * F
+        specs = [PredictorSpec.from_byte(int(c)) for c in sel]
+        payloads = [CompressedBlocks(BlockPlan(opts.block_size, len(p)), p) for p in pl]
         data = write_container(stack.width, stack.height, geo.pitch_x, geo.pitch_y, opts.block_size,
-                               list(zip(specs, payloads)))
+                               list(zip(specs, payloads)), joiner=_lib.join)
         return CompressResult(data, specs, reports, select_s, encode_s)
+    vol = np.ascontiguousarray(stack.to_array())
     pool = ThreadPoolExecutor(max(1, opts.workers))
     futures = []
     try:

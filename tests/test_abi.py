@@ -64,3 +64,26 @@ def test_sm100a_cubin_present():
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
     assert "sm_100a" in out.stdout
+
+
+def test_native_join_equals_bytes_join():
+    """_lib.join (pcbz_gather, the device coder's container join) is b"".join
+    for bytes, memoryviews into numpy buffers and empty parts, multithreaded
+    once the total is large."""
+    rng = np.random.default_rng(7)
+    big = rng.integers(0, 256, 24 << 20, dtype=np.uint8)
+    mv = memoryview(big)
+    parts = [b"PCBZ", b"", mv[5:5 + (9 << 20)], bytes(rng.integers(0, 256, 1000, dtype=np.uint8)),
+             mv[(9 << 20) + 11:], b"x", mv[0:0]]
+    assert _lib.join(parts, threads=8) == b"".join(parts)
+    assert _lib.join([], threads=4) == b""
+    small = [bytes([i]) * i for i in range(50)]
+    assert _lib.join(small, threads=3) == b"".join(small)
+
+
+def test_gather_rejects_bad_pieces():
+    lib = _lib.load()
+    dst = np.zeros(8, np.uint8)
+    lens = np.array([4, -1], np.int64)
+    srcs = (ctypes.c_void_p * 2)(dst.ctypes.data, dst.ctypes.data)
+    assert lib.pcbz_gather(dst.ctypes.data, srcs, lens.ctypes.data, 2, 2) == _lib.PCBZ_E_INVALID

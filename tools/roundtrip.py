@@ -35,8 +35,7 @@ def main():
     opts = CompressOptions(workers=cores, temporal=wl.temporal,
                            candidates=None if wl.temporal else tuple(
                                __import__("paper_2310_09467_b200").all_intra_specs()))
-    from paper_2310_09467_b200.pipeline import GPU_CHUNK_FRAMES
-    compress_stack_detailed(FrameStack(stack.frames[:GPU_CHUNK_FRAMES]), opts)   # warm-up: context, buffers
+    compress_stack_detailed(stack, opts)   # warm-up at full size: context, device buffers
     t0 = time.perf_counter()
     res = compress_stack_detailed(stack, opts)
     t_c = time.perf_counter() - t0
