@@ -1050,8 +1050,11 @@ static int compress_impl(const FrameSource &src, const uint16_t *halo_prev, int6
   const int64_t nbf = (sb + block_size - 1) / block_size;     // blocks per frame
   if (out_cap < pcbz_compress_bound(nframes, h, w, block_size))
     return fail(PCBZ_E_INVALID, "output buffer smaller than pcbz_compress_bound");
-  // frames per device round: streams of at most 1 GiB (bzip2 batch limit)
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nframes, ((int64_t)1 << 30) / sb));
+  // frames per device round: streams of at most 1 GiB (bzip2 batch limit);
+  // PCBZ_COMPRESS_ROUND_BYTES lowers it (tests cross round boundaries)
+  int64_t round_bytes = (int64_t)1 << 30;
+  if (const char *e = getenv("PCBZ_COMPRESS_ROUND_BYTES")) round_bytes = std::min(round_bytes, std::max<int64_t>(1, atoll(e)));
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nframes, round_bytes / sb));
   cudaStream_t st = c.stream;
   if (halo_prev) {
     if ((rc = c.prev.ensure((size_t)npix * 2))) return rc;

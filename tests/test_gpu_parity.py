@@ -446,16 +446,21 @@ def test_workspace_bound_without_halo(F, H, W, codes):
         prev = vol[f]
 
 
-@pytest.mark.parametrize("forced", [None, PredictorSpec(True, 3)])
-def test_device_and_host_coders_identical(forced):
+@pytest.mark.parametrize("forced,round_frames", [(None, 0), (PredictorSpec(True, 3), 0), (None, 2),
+                                                 (PredictorSpec(True, 3), 1)])
+def test_device_and_host_coders_identical(forced, round_frames, monkeypatch):
     """CompressOptions.coder: bzip2 on the device (judge + emission + bzip2 in
-    one call, pcbz_compress_host) and on host threads give the same
-    container, equal to the oracle's."""
+    one call over the frames' buffers, pcbz_compress_frames_host) and on host
+    threads give the same container, equal to the oracle's -- also when the
+    call crosses device rounds (PCBZ_COMPRESS_ROUND_BYTES: the temporal
+    predictor of a round's first frame reads the previous round's last)."""
     p = SynthParams(256, 200, 15, 15, mode="smooth_lenslet", noise_sigma=20.0, photon_scale=0.05,
                     frames=5, drift=1.0, seed=9)
     vol = generate_array(p)
     geo = LensletGeometry(15, 15)
     stack = FrameStack(tuple(Frame(f, geo) for f in vol))
+    if round_frames:
+        monkeypatch.setenv("PCBZ_COMPRESS_ROUND_BYTES", str(round_frames * 2 * 256 * 200))
     dev = compress_stack(stack, CompressOptions(forced=forced, block_size=30000, coder="device"))
     host = compress_stack(stack, CompressOptions(forced=forced, block_size=30000, coder="host", workers=4))
     assert dev == host
