@@ -33,6 +33,7 @@ extern "C" {
 #define PCBZ_E_CUDA (-2)      /* CUDA runtime failure: RuntimeError         */
 #define PCBZ_E_NODEVICE (-3)  /* no usable sm_100 device: RuntimeError      */
 #define PCBZ_E_INTERNAL (-4)  /* internal invariant broken: RuntimeError    */
+#define PCBZ_NEEDS_HOST 1     /* not an error: some payloads are left to libbzip2 (status[] = 1) */
 
 #define PCBZ_MAX_CANDIDATES 26
 
@@ -222,6 +223,31 @@ PCBZ_API int pcbz_compress_frames_host(const uint16_t *const *frames, const uint
                        const uint8_t *specs, int k, int temporal, const uint8_t *sel_in,
                        int64_t block_size, double *ent_out, uint8_t *sel_out, uint8_t *out,
                        size_t out_cap, int64_t *out_start, int64_t *out_len, uint8_t *raw_flag);
+
+/* bzip2 decoding on the GPU (libbzip2 1.0.8 stream format), replacing the
+ * bz2.decompress of every PCBZ block (blocks.py:84-92, pipeline.py:121-139).
+ * payloads[i] (plen[i] bytes, one bzip2 stream) decodes to out + out_off[i]
+ * (host buffer), out_len[i] bytes expected.  status[i] = 0 on entry skips
+ * payload i; on return 0 = decoded, 1 = left to the caller's libbzip2
+ * (randomised or periodic blocks, corrupt or unexpected data -- libbzip2
+ * then also raises the reference's error).  Every block CRC and the
+ * stream's combined CRC are checked. */
+PCBZ_API int pcbz_bunzip2_host(const uint8_t *const *payloads, const int64_t *plen, int n, uint8_t *out,
+                               const int64_t *out_off, const int64_t *out_len, uint8_t *status);
+
+/* decompress_stack after the container is parsed: payload i = (frame
+ * i / blocks_per_frame, block i % blocks_per_frame) of the frames' big-endian
+ * residual streams (2*h*w bytes, block_size bytes per block), decoded on the
+ * GPU, then the inverse prediction (as pcbz_reconstruct_host with sel[]) into
+ * frames_out.  host_streams (nullable; entries nullable) supplies payloads the
+ * caller decoded itself.  Returns PCBZ_NEEDS_HOST with status[i] = 1 for the
+ * payloads the caller must decode (then call again with them in
+ * host_streams); frames_out is written only when PCBZ_OK is returned. */
+PCBZ_API int pcbz_decompress_host(const uint8_t *const *payloads, const int64_t *plen, int64_t nframes,
+                                  int64_t blocks_per_frame, int64_t h, int64_t w, int64_t px, int64_t py,
+                                  int64_t block_size, const uint8_t *sel,
+                                  const uint8_t *const *host_streams, uint16_t *frames_out,
+                                  uint8_t *status);
 
 /* Testing hook: force the number of segments each (frame, candidate) stream
  * is split into (0 = automatic).  Outputs must not depend on it. */

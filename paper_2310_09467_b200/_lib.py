@@ -18,6 +18,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_native" / "libpcbz_b200.so"
 PCBZ_OK = 0
 PCBZ_E_INVALID = -1
 PCBZ_E_CUDA = -2
+PCBZ_NEEDS_HOST = 1
 PCBZ_E_NODEVICE = -3
 PCBZ_E_INTERNAL = -4
 MAX_CANDIDATES = 26
@@ -69,6 +70,9 @@ SIGNATURES = {
     "pcbz_compress_frames_host": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp,
                                            _c_int, _c_int, _vp, _c_i64, _vp, _vp, _vp, _c_size, _vp,
                                            _vp, _vp]),
+    "pcbz_bunzip2_host": (_c_int, [_vp, _vp, _c_int, _vp, _vp, _vp, _vp]),
+    "pcbz_decompress_host": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64,
+                                      _vp, _vp, _vp, _vp]),
     "pcbz_host_alloc": (_vp, [_c_size]),
     "pcbz_host_free": (_c_int, [_vp]),
     "pcbz_gather": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int]),

@@ -41,7 +41,8 @@ def _units(pitches=None):
     """(source, extra flags, object name) of every translation unit; pitches
     not in `pitches` (None = all) get an empty stub."""
     units = [("judge.cu", [], "judge.o"), ("aux_kernels.cu", [], "aux_kernels.o"),
-             ("capi.cu", [], "capi.o"), ("bzip2.cu", [], "bzip2.o")]
+             ("capi.cu", [], "capi.o"), ("bzip2.cu", [], "bzip2.o"),
+             ("bunzip2.cu", [], "bunzip2.o")]
     for px in range(MAX_FAST_PITCH + 1):
         stub = pitches is not None and px not in pitches and px != 0
         units.append(("judge_px.cu", [f"-DPCBZ_PX={px}"] + (["-DPCBZ_STUB=1"] if stub else []),

@@ -80,6 +80,29 @@ def bz2_block(chunk) -> bytes:
     return bz2.compress(chunk, BZ2_LEVEL)
 
 
+def bunzip2_blocks_device(payloads, sizes) -> list:
+    """bz2.decompress of every payload (whose decoded size is known: PCBZ
+    blocks), decoded on the GPU by csrc/bunzip2.cu (pcbz_bunzip2_host); a
+    payload the device leaves to libbzip2 (status 1) is decoded on the host."""
+    import ctypes
+    import numpy as np
+    from . import _lib
+    n = len(payloads)
+    if n == 0:
+        return []
+    ptrs = (ctypes.c_void_p * n)(*[_lib._address(p) if len(p) else None for p in payloads])
+    lens = np.array([len(p) for p in payloads], np.int64)
+    osz = np.array(sizes, np.int64)
+    off = np.zeros(n, np.int64)
+    off[1:] = np.cumsum(osz)[:-1]
+    out = np.empty(max(int(osz.sum()), 1), np.uint8)
+    status = np.ones(n, np.uint8)
+    _lib.check(_lib.load().pcbz_bunzip2_host(ptrs, lens.ctypes.data, n, out.ctypes.data, off.ctypes.data,
+                                             osz.ctypes.data, status.ctypes.data))
+    return [out[off[i]:off[i] + osz[i]].tobytes() if status[i] == 0 else bz2.decompress(payloads[i])
+            for i in range(n)]
+
+
 #: input bytes per pcbz_bzip2_host call (the device coder takes < 2^31 bytes after RLE1)
 DEVICE_BZ2_BATCH = 1 << 30
 

@@ -1175,4 +1175,75 @@ int pcbz_compress_frames_host(const uint16_t *const *frames, const uint16_t *hal
                        raw_flag);
 }
 
+int pcbz_bunzip2_host(const uint8_t *const *payloads, const int64_t *plen, int n, uint8_t *out,
+                      const int64_t *out_off, const int64_t *out_len, uint8_t *status) {
+  if (n < 0 || (n > 0 && (!payloads || !plen || !out || !out_off || !out_len || !status)))
+    return fail(PCBZ_E_INVALID, "invalid bunzip2 arguments");
+  HostCtx &c = g_ctx;
+  int rc = c.init();
+  if (rc) return rc;
+  int64_t total = 0;
+  for (int i = 0; i < n; ++i) {
+    if (plen[i] < 0 || out_len[i] < 0 || out_off[i] < 0) return fail(PCBZ_E_INVALID, "negative length or offset");
+    total = std::max(total, out_off[i] + out_len[i]);
+  }
+  if ((rc = c.stream_out.ensure((size_t)std::max<int64_t>(total, 1)))) return rc;
+  std::string err;
+  if (bzd::decode_payloads(payloads, plen, n, c.stream_out.as<uint8_t>(), out_off, out_len, status, c.stream, err))
+    return fail(PCBZ_E_CUDA, "%s", err.c_str());
+  for (int i = 0; i < n; ++i)
+    if (status[i] == 0 && out_len[i])
+      CUDA_TRY(cudaMemcpyAsync(out + out_off[i], c.stream_out.as<uint8_t>() + out_off[i], (size_t)out_len[i],
+                               cudaMemcpyDeviceToHost, c.stream));
+  CUDA_TRY(cudaStreamSynchronize(c.stream));
+  return PCBZ_OK;
+}
+
+int pcbz_decompress_host(const uint8_t *const *payloads, const int64_t *plen, int64_t nframes,
+                         int64_t blocks_per_frame, int64_t h, int64_t w, int64_t px, int64_t py,
+                         int64_t block_size, const uint8_t *sel, const uint8_t *const *host_streams,
+                         uint16_t *frames_out, uint8_t *status) {
+  int rc = validate_geometry(h, w, px, py);
+  if (rc) return rc;
+  if (nframes < 1) return fail(PCBZ_E_INVALID, "at least one frame is required");
+  if (block_size < 1) return fail(PCBZ_E_INVALID, "block_size must be >= 1");
+  const int64_t sb = 2 * h * w;
+  if (blocks_per_frame != (sb + block_size - 1) / block_size)
+    return fail(PCBZ_E_INVALID, "blocks_per_frame %lld does not match the frame size", (long long)blocks_per_frame);
+  if ((rc = check_sel(sel, nframes, false))) return rc;
+  const int64_t n = nframes * blocks_per_frame;
+  if (n > 0x7FFFFFFF) return fail(PCBZ_E_INVALID, "too many payloads");
+  HostCtx &c = g_ctx;
+  if ((rc = c.init())) return rc;
+  const size_t fb = (size_t)nframes * sb;
+  if ((rc = c.bytes.ensure(fb)) || (rc = c.frames.ensure(fb)) || (rc = c.out.ensure(fb)) ||
+      (rc = c.sel.ensure((size_t)nframes)))
+    return rc;
+  cudaStream_t st = c.stream;
+  std::vector<int64_t> off(n), len(n);
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t f = i / blocks_per_frame, b = i % blocks_per_frame;
+    off[i] = f * sb + b * block_size;
+    len[i] = std::min(block_size, sb - b * block_size);
+    status[i] = 1;
+    if (host_streams && host_streams[i]) {
+      status[i] = 0;
+      CUDA_TRY(cudaMemcpyAsync(c.bytes.as<uint8_t>() + off[i], host_streams[i], (size_t)len[i],
+                               cudaMemcpyHostToDevice, st));
+    }
+  }
+  std::string err;
+  if (bzd::decode_payloads(payloads, plen, (int)n, c.bytes.as<uint8_t>(), off.data(), len.data(), status, st, err))
+    return fail(PCBZ_E_CUDA, "%s", err.c_str());
+  for (int64_t i = 0; i < n; ++i)
+    if (status[i]) return PCBZ_NEEDS_HOST;
+  CUDA_TRY(bzd::launch_be16(c.bytes.as<uint8_t>(), (int64_t)fb / 2, c.frames.as<uint16_t>(), st));
+  CUDA_TRY(cudaMemcpyAsync(c.sel.p, sel, (size_t)nframes, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_reconstruct(c.frames.as<uint16_t>(), nullptr, nframes, h, w, (int)px, (int)py,
+                              c.sel.as<uint8_t>(), c.out.as<uint16_t>(), st));
+  CUDA_TRY(cudaMemcpyAsync(frames_out, c.out.p, fb, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return PCBZ_OK;
+}
+
 }  // extern "C"

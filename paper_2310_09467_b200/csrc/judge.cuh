@@ -2,6 +2,7 @@
 // entropy judge (reference: pkg/src/pcbz/_kernels.py, criterion.py).
 #pragma once
 #include <cstdint>
+#include <string>
 #include <cuda_runtime.h>
 
 namespace pcbz {
@@ -113,5 +114,12 @@ int compress_jobs(const uint8_t *d_in, const int64_t *in_off, int njobs, uint8_t
 size_t job_bound(int64_t len);
 const char *last_error();
 }  // namespace bz
+
+namespace bzd {  // bunzip2.cu
+int decode_payloads(const uint8_t *const *payloads, const int64_t *plen, int n, uint8_t *d_out,
+                    const int64_t *out_off, const int64_t *out_len, uint8_t *status, cudaStream_t st,
+                    std::string &err);
+cudaError_t launch_be16(const uint8_t *s, int64_t n, uint16_t *out, cudaStream_t st);
+}  // namespace bzd
 
 }  // namespace pcbz

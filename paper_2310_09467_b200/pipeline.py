@@ -372,6 +372,12 @@ def decompress_stack(data, workers: int = 1) -> FrameStack:
     """Reference pipeline.py:121-139: bzip2 on host threads, inverse
     prediction and temporal undelta on the device."""
     header, records, payloads = read_container(data)
+    fast = _decompress_device(header, records, payloads) if _lib.device_count() > 0 else None
+    if fast is not None:
+        return fast
+    # anything the device decoder leaves to libbzip2 (corrupt or unusual
+    # payloads): the whole container takes the host path below, which raises
+    # the reference's errors in frame order
     H, W = header.height, header.width
     res = np.empty((header.frame_count, H, W), np.uint16)
     # every (frame, block) payload of the container on one pool (the
@@ -408,6 +414,35 @@ def decompress_stack(data, workers: int = 1) -> FrameStack:
     _lib.check(_lib.load().pcbz_reconstruct_host(_lib.ptr(res), None, res.shape[0], H, W,
                                                  header.pitch_x, header.pitch_y, _lib.ptr(sel),
                                                  _lib.ptr(out)))
+    geo = LensletGeometry(header.pitch_x, header.pitch_y)
+    return FrameStack(tuple(Frame(f, geo) for f in out))
+
+
+def _decompress_device(header, records, payloads):
+    """Every payload bzip2-decoded on the GPU (pcbz_decompress_host: block
+    magic scan, Huffman + inverse MTF, inverse BWT by list ranking, inverse
+    RLE1, all CRCs checked) and the inverse prediction run on the decoded
+    streams without leaving the device.  None when any payload or the block
+    layout is not the one compress_stack writes (the caller's host path then
+    decodes and reports errors exactly as the reference)."""
+    H, W = header.height, header.width
+    F = header.frame_count
+    nb = -(-2 * H * W // header.block_size)
+    if any(len(p) != nb for p in payloads):
+        return None
+    flat = [p for ps in payloads for p in ps]
+    n = len(flat)
+    ptrs = (ctypes.c_void_p * n)(*[_lib._address(p) for p in flat])
+    lens = np.array([len(p) for p in flat], np.int64)
+    sel = np.array([r.spec.to_byte() for r in records], np.uint8)
+    out = np.empty((F, H, W), np.uint16)
+    status = np.ones(n, np.uint8)
+    rc = _lib.load().pcbz_decompress_host(ptrs, lens.ctypes.data, F, nb, H, W, header.pitch_x,
+                                          header.pitch_y, header.block_size, _lib.ptr(sel), None,
+                                          _lib.ptr(out), status.ctypes.data)
+    if rc == _lib.PCBZ_NEEDS_HOST:
+        return None
+    _lib.check(rc)
     geo = LensletGeometry(header.pitch_x, header.pitch_y)
     return FrameStack(tuple(Frame(f, geo) for f in out))
 

@@ -1,0 +1,116 @@
+"""GPU bzip2 decoding (csrc/bunzip2.cu via codec.bunzip2_blocks_device and
+pcbz_bunzip2_host) against the reference's bz2.decompress (blocks.py:84-92):
+identical bytes for small, multi-block, every-level and run-heavy streams;
+payloads the decoder leaves to libbzip2 (periodic blocks, corruption) still
+come out right or raise as the reference does; decompress_stack round trip
+through the all-device path."""
+import bz2
+import ctypes
+import random
+
+import numpy as np
+import pytest
+
+from paper_2310_09467_b200 import _lib
+from paper_2310_09467_b200.codec import bunzip2_blocks_device
+from paper_2310_09467_b200.lfm_synth import SynthParams, generate_array
+
+pytestmark = pytest.mark.gpu
+
+
+def _status(payloads, sizes):
+    n = len(payloads)
+    ptrs = (ctypes.c_void_p * n)(*[_lib._address(p) for p in payloads])
+    lens = np.array([len(p) for p in payloads], np.int64)
+    osz = np.array(sizes, np.int64)
+    off = np.zeros(n, np.int64)
+    off[1:] = np.cumsum(osz)[:-1]
+    out = np.empty(max(int(osz.sum()), 1), np.uint8)
+    st = np.ones(n, np.uint8)
+    _lib.check(_lib.load().pcbz_bunzip2_host(ptrs, lens.ctypes.data, n, out.ctypes.data, off.ctypes.data,
+                                             osz.ctypes.data, st.ctypes.data))
+    return st, [out[off[i]:off[i] + osz[i]].tobytes() for i in range(n)]
+
+
+def _periodic(c):
+    return any(len(c) % p == 0 and c == c[:p] * (len(c) // p) for p in range(1, len(c)))
+
+
+def _cases(seed, count):
+    rng = random.Random(seed)
+    out = [b"", b"a", b"ab", b"banana", b"abcd" * 3, bytes(range(256)), b"aaaab", b"aaaaab",
+           b"xaaaa" * 7 + b"y", bytes(rng.randrange(256) for _ in range(5000))]
+    for _ in range(count):
+        n = rng.choice([3, 9, 17, 100, 700, 2000, 20000, 120000])
+        alph = rng.choice([2, 3, 16, 256])
+        s = bytearray()
+        while len(s) < n:
+            s += bytes([rng.randrange(alph)]) * (rng.randint(1, 300) if rng.random() < 0.1 else rng.randint(1, 6))
+        out.append(bytes(s[:n]))
+    return out
+
+
+def test_small_streams_identical():
+    cases = _cases(5, 120)
+    payloads = [bz2.compress(c, 9) for c in cases]
+    st, got = _status(payloads, [len(c) for c in cases])
+    for c, g, s in zip(cases, got, st):
+        if s == 0:
+            assert g == c, (len(c), c[:24])
+        else:   # only exactly periodic blocks ("xxx", "abcd" * 3) are left to the host
+            assert _periodic(c), (len(c), c[:24])
+    assert (st == 0).mean() > 0.8
+    assert bunzip2_blocks_device(payloads, [len(c) for c in cases]) == cases
+
+
+@pytest.mark.parametrize("level", [1, 5, 9])
+def test_levels_and_multiblock(level):
+    rng = np.random.default_rng(level)
+    data = (rng.normal(0, 30, 3_000_000).astype(np.int16).astype(np.uint16)).tobytes()
+    runs = bytes(np.repeat(rng.integers(0, 256, 40000, dtype=np.uint8), rng.integers(1, 40, 40000)))
+    cases = [data, runs[:2_500_000], data[:1_000_001]]
+    payloads = [bz2.compress(c, level) for c in cases]
+    st, got = _status(payloads, [len(c) for c in cases])
+    assert list(st) == [0, 0, 0]
+    assert got == cases
+
+
+def test_residual_streams_like_the_pipeline():
+    img = generate_array(SynthParams(2048, 2048, 15, 15, mode="beads", signal_amplitude=3000,
+                                     noise_sigma=100, photon_scale=0.05, seed=2))[0]
+    from paper_2310_09467_b200.codec import split_blocks
+    stream = img.astype(">u2").tobytes()
+    chunks = [bytes(b) for b in split_blocks(stream, 4 << 20)]
+    payloads = [bz2.compress(c, 9) for c in chunks]
+    st, got = _status(payloads, [len(c) for c in chunks])
+    assert list(st) == [0] * len(chunks)
+    assert got == chunks
+
+
+def test_periodic_and_corrupt_payloads_left_to_libbzip2():
+    const = b"\x07" * (255 * 4000)             # RLE1: (07 07 07 07 FB) x 4000, an exactly periodic block
+    good = bytes(np.random.default_rng(1).integers(0, 7, 200_000, dtype=np.uint8))
+    p_const, p_good = bz2.compress(const, 9), bz2.compress(good, 9)
+    bad = bytearray(p_good)
+    bad[len(bad) // 2] ^= 0x40
+    st, got = _status([p_const, p_good, bytes(bad)], [len(const), len(good), len(good)])
+    assert st[0] == 1 and st[1] == 0 and st[2] == 1
+    assert got[1] == good
+    assert bunzip2_blocks_device([p_const, p_good], [len(const), len(good)]) == [const, good]
+    with pytest.raises((OSError, ValueError, EOFError)):
+        bunzip2_blocks_device([bytes(bad)], [len(good)])
+
+
+def test_decompress_stack_device_path_round_trip():
+    from paper_2310_09467_b200 import (CompressOptions, Frame, FrameStack, LensletGeometry,
+                                       compress_stack, decompress_stack, pipeline)
+    p = SynthParams(512, 384, 15, 15, mode="smooth_lenslet", noise_sigma=20.0, photon_scale=0.05,
+                    frames=4, drift=1.0, seed=4)
+    vol = generate_array(p)
+    stack = FrameStack(tuple(Frame(f, LensletGeometry(15, 15)) for f in vol))
+    data = compress_stack(stack, CompressOptions(block_size=100_000))
+    from paper_2310_09467_b200.codec import read_container
+    h, r, pl = read_container(data)
+    fast = pipeline._decompress_device(h, r, pl)
+    assert fast is not None and fast == stack
+    assert decompress_stack(data) == stack
