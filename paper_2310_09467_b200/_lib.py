@@ -194,3 +194,13 @@ def join(parts, threads: int | None = None) -> bytes:
         check(load().pcbz_gather(_PyBytes_AsString(out), srcs, lens.ctypes.data, n,
                                  threads or (os.cpu_count() or 1)))
     return out
+
+
+def copy_into(dst: np.ndarray, src) -> None:
+    """dst[...] = src bytes, copied by pcbz_gather on all host threads (a
+    fresh destination is first-touched in parallel)."""
+    import os
+    n = dst.nbytes
+    srcs = (ctypes.c_void_p * 1)(_address(src))
+    lens = np.array([n], np.int64)
+    check(load().pcbz_gather(dst.ctypes.data, srcs, lens.ctypes.data, 1, os.cpu_count() or 1))

@@ -435,14 +435,19 @@ def _decompress_device(header, records, payloads):
     ptrs = (ctypes.c_void_p * n)(*[_lib._address(p) for p in flat])
     lens = np.array([len(p) for p in flat], np.int64)
     sel = np.array([r.spec.to_byte() for r in records], np.uint8)
-    out = np.empty((F, H, W), np.uint16)
     status = np.ones(n, np.uint8)
+    nbytes = F * H * W * 2
+    # frames land in this thread's page-locked buffer (PCIe speed), then a
+    # multithreaded copy moves them into the returned array
+    staged = _lib.pinned_buffer(nbytes)
     rc = _lib.load().pcbz_decompress_host(ptrs, lens.ctypes.data, F, nb, H, W, header.pitch_x,
                                           header.pitch_y, header.block_size, _lib.ptr(sel), None,
-                                          _lib.ptr(out), status.ctypes.data)
+                                          staged.ctypes.data, status.ctypes.data)
     if rc == _lib.PCBZ_NEEDS_HOST:
         return None
     _lib.check(rc)
+    out = np.empty((F, H, W), np.uint16)
+    _lib.copy_into(out, staged)
     geo = LensletGeometry(header.pitch_x, header.pitch_y)
     return FrameStack(tuple(Frame(f, geo) for f in out))
 
