@@ -591,10 +591,14 @@ __global__ void mtf_tail_freq_kernel(Block *blocks, const int *ids, const uint32
 // ---------------------------------------------------------------------------
 
 // BZ2_hbMakeCodeLengths, heap operations and tie-breaks as in huffman.c
-__device__ void make_code_lengths(uint8_t *len, const uint32_t *freq, int alpha, int max_len) {
+struct HuffWork {   // BZ2_hbMakeCodeLengths work arrays (shared memory, one per table)
   int32_t heap[kMaxAlpha + 2];
   int32_t weight[kMaxAlpha * 2];
   int32_t parent[kMaxAlpha * 2];
+};
+
+__device__ void make_code_lengths(uint8_t *len, const uint32_t *freq, int alpha, int max_len, HuffWork &W) {
+  int32_t *heap = W.heap, *weight = W.weight, *parent = W.parent;
   for (int i = 0; i < alpha; ++i) weight[i + 1] = (int32_t)((freq[i] == 0 ? 1u : freq[i]) << 8);
   for (;;) {
     int n_nodes = alpha, n_heap = 0;
@@ -677,6 +681,9 @@ __global__ void __launch_bounds__(kTableThreads) tables_kernel(Block *blocks, co
   __shared__ uint32_t rfreq[kMaxGroups][kMaxAlpha];
   __shared__ uint32_t freq[kMaxAlpha];
   __shared__ unsigned long long data_bits;
+  __shared__ HuffWork hw[kMaxGroups];
+  __shared__ int32_t chunk_last[kTableThreads][kMaxGroups];
+  __shared__ unsigned long long sel_bits_sum;
   const int tid = threadIdx.x;
   const int alpha = B.n_in_use + 2;
   const int n_mtf = B.n_mtf;
@@ -721,7 +728,9 @@ __global__ void __launch_bounds__(kTableThreads) tables_kernel(Block *blocks, co
       for (int i = gs; i < ge; ++i) atomicAdd(&rfreq[bt][mv[i]], 1u);
     }
     __syncthreads();
-    if (tid < n_groups) make_code_lengths(len[tid], rfreq[tid], alpha, kMaxCodeLen);
+    // one table per warp (lane 0): the heap builds run on different schedulers
+    if ((tid & 31) == 0 && (tid >> 5) < n_groups)
+      make_code_lengths(len[tid >> 5], rfreq[tid >> 5], alpha, kMaxCodeLen, hw[tid >> 5]);
     __syncthreads();
   }
   TablesOut &T = tables[ids[blockIdx.x]];
@@ -744,26 +753,46 @@ __global__ void __launch_bounds__(kTableThreads) tables_kernel(Block *blocks, co
   unsigned long long mine = 0;
   for (int i = tid; i < n_mtf; i += blockDim.x) mine += len[sel[i / kGroupSize]][mv[i]];
   atomicAdd(&data_bits, mine);
-  if (tid == 0) {
-    // selector MTF and the header bit count (compress.c sendMTFValues)
-    uint8_t pos[kMaxGroups];
-    for (int i = 0; i < n_groups; ++i) pos[i] = (uint8_t)i;
-    int64_t sel_bits = 0;
-    uint8_t *sm = sel_mtf + B.sel_off;
-    for (int i = 0; i < n_sel; ++i) {
-      const uint8_t s = sel[i];
-      int j = 0;
-      uint8_t tmp = pos[0];
-      while (s != tmp) {
-        ++j;
-        const uint8_t t2 = tmp;
-        tmp = pos[j];
-        pos[j] = t2;
+  // selector MTF (compress.c sendMTFValues) in parallel: the MTF index of
+  // selector i is the number of other tables whose latest use before i is
+  // more recent than that of sel[i] (the initial list order 0, 1, ... acts
+  // as uses at times -1, -2, ...).  Each thread owns a contiguous run of
+  // selectors; the latest use per table before each run comes from a scan
+  // of the per-run latest uses.
+  {
+    const int per = (n_sel + kTableThreads - 1) / kTableThreads;
+    const int a = min(n_sel, tid * per), b = min(n_sel, a + per);
+    int32_t last[kMaxGroups];
+    for (int t = 0; t < kMaxGroups; ++t) last[t] = -1 - t;
+    for (int i = a; i < b; ++i) last[sel[i]] = i;
+    for (int t = 0; t < kMaxGroups; ++t) chunk_last[tid][t] = last[t];
+    if (tid == 0) sel_bits_sum = 0;
+    __syncthreads();
+    if (tid < kMaxGroups) {   // exclusive running max over the runs, per table
+      int32_t run = -1 - tid;
+      for (int k = 0; k < kTableThreads; ++k) {
+        const int32_t v = chunk_last[k][tid];
+        chunk_last[k][tid] = run;
+        run = max(run, v);
       }
-      pos[0] = tmp;
-      sm[i] = (uint8_t)j;
-      sel_bits += j + 1;
     }
+    __syncthreads();
+    for (int t = 0; t < kMaxGroups; ++t) last[t] = chunk_last[tid][t];
+    uint8_t *sm = sel_mtf + B.sel_off;
+    unsigned long long bits = 0;
+    for (int i = a; i < b; ++i) {
+      const int s0 = sel[i];
+      int j = 0;
+      for (int t = 0; t < n_groups; ++t) j += (t != s0 && last[t] > last[s0]) ? 1 : 0;
+      sm[i] = (uint8_t)j;
+      bits += (unsigned long long)(j + 1);
+      last[s0] = i;
+    }
+    atomicAdd(&sel_bits_sum, bits);
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const int64_t sel_bits = (int64_t)sel_bits_sum;
     int used16 = 0;
     for (int i = 0; i < 16; ++i) used16 += ((B.in_use[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu) ? 1 : 0;
     int64_t tab_bits = 0;
