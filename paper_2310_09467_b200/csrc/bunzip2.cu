@@ -99,27 +99,30 @@ __global__ void scan_magic_kernel(const uint8_t *in, const int64_t *off, int nst
 // ---- 2: one block: header, Huffman, RUNA/RUNB, inverse MTF ---------------------
 
 struct BitReader {       // MSB-first bit reader; every lane of a warp runs it in lockstep
-  const uint8_t *p;
+  const uint8_t *p;      // the payload; the device buffer is padded, so reads may run past len
   int64_t len, pos;      // bytes of the stream, next byte to load
   uint64_t buf;
   int nb;
   __device__ void init(const uint8_t *p_, int64_t len_, int64_t bit) {
     p = p_; len = len_; pos = bit >> 3; buf = 0; nb = 0;
     refill();
+    refill();
     nb -= (int)(bit & 7);
   }
-  __device__ __forceinline__ void refill() {   // past the end reads zeros (checked by the caller)
-    while (nb <= 56) {
-      buf = (buf << 8) | (pos < len ? p[pos] : 0u);
-      ++pos;
-      nb += 8;
-    }
+  // 32 bits, big-endian; not inlined, so the hot loop branches around it
+  // (every ~4 symbols) instead of executing it predicated on every symbol
+  __device__ __noinline__ void refill() {
+    const uint32_t w = ((uint32_t)p[pos] << 24) | ((uint32_t)p[pos + 1] << 16) |
+                       ((uint32_t)p[pos + 2] << 8) | (uint32_t)p[pos + 3];
+    buf = (buf << 32) | w;
+    pos += 4;
+    nb += 32;
   }
-  __device__ __forceinline__ uint32_t peek(int n) {
+  __device__ __forceinline__ uint32_t peek(int n) {   // n <= 32
     if (nb < n) refill();
-    return (uint32_t)(buf >> (nb - n)) & ((1u << n) - 1u);
+    return (uint32_t)(buf >> (nb - n)) & (uint32_t)((1ull << n) - 1);
   }
-  __device__ __forceinline__ uint32_t get(int n) {
+  __device__ __forceinline__ uint32_t get(int n) {    // n <= 32
     if (n == 0) return 0;
     if (nb < n) refill();
     nb -= n;
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(32 * kDecodeWarps) decode_block_kernel(
   const int EOB = n_in_use + 1;
   int group_no = -1, group_pos = 0, gsel = 0;
   int32_t nblock = 0;
-  uint8_t *out = L + (size_t)c * kSlot;
+  uint8_t *o = L + (size_t)c * kSlot;   // next output byte
   auto next_sym = [&](int &sym) -> bool {
     if (group_pos == 0) {
       if (++group_no >= n_sel) return false;
@@ -313,8 +316,9 @@ __global__ void __launch_bounds__(32 * kDecodeWarps) decode_block_kernel(
       const uint32_t front = (uint32_t)__shfl_sync(0xffffffffu, (uint32_t)x, 0) & 0xFFu;
       const uint8_t uc = S.seq[front];
       if (nblock + es > nblockMAX) return;
-      for (int32_t k = lane; k < es; k += 32) out[nblock + k] = uc;
+      for (int32_t k = lane; k < es; k += 32) o[k] = uc;
       nblock += es;
+      o += es;
       continue;
     }
     if (nblock >= nblockMAX) return;
@@ -326,15 +330,15 @@ __global__ void __launch_bounds__(32 * kDecodeWarps) decode_block_kernel(
     const uint32_t v = (uint32_t)(((((uint64_t)shi << 32) | slo) >> (8 * b)) & 0xFFu);
     const uint32_t top = __shfl_up_sync(0xffffffffu, (uint32_t)(x >> 56), 1);
     const uint64_t cin = lane == 0 ? v : top;
-    if (lane < src) {
-      x = (x << 8) | cin;
-    } else if (lane == src) {
-      const uint64_t lowmask = b ? ((1ull << (8 * b)) - 1) : 0ull;
-      const uint64_t keep = b == 7 ? 0ull : ~((1ull << (8 * (b + 1))) - 1);
-      x = (x & keep) | ((x & lowmask) << 8) | cin;
-    }
+    // lanes below src shift all eight entries, lane src the ones below b
+    const uint64_t lowmask = (1ull << (8 * b)) - 1;            // b <= 7
+    const uint64_t keep = ~((lowmask << 8) | 0xFFull);         // entries above b
+    const uint64_t shifted = (x << 8) | cin;
+    const uint64_t partial = (x & keep) | ((x & lowmask) << 8) | cin;
+    x = lane < src ? shifted : (lane == src ? partial : x);
     const uint8_t uc = S.seq[v];
-    if (lane == 0) out[nblock] = uc;
+    if (lane == 0) *o = uc;
+    ++o;
     nblock++;
     if (!next_sym(sym)) return;
   }
@@ -663,7 +667,8 @@ int decode_batch(const uint8_t *const *payloads, const int64_t *plen, const std:
   }
   const int64_t total = off[ns];
   if (total == 0) return 0;
-  BZD_TRY(g.in.ensure((size_t)total));
+  BZD_TRY(g.in.ensure((size_t)total + 64));   // padded: the bit reader loads 4 bytes at a time
+  BZD_TRY(cudaMemsetAsync(g.in.as<uint8_t>() + total, 0, 64, st));
   BZD_TRY(g.off.ensure((size_t)(ns + 1) * 8));
   for (int s = 0; s < ns; ++s)
     if (plen[ids[s]]) BZD_TRY(cudaMemcpyAsync(g.in.as<uint8_t>() + off[s], payloads[ids[s]], (size_t)plen[ids[s]], cudaMemcpyHostToDevice, st));
