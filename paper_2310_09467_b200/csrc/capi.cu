@@ -537,17 +537,23 @@ int pcbz_judge_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t n
   // Chunks alternate between two compute streams (one workspace each), so the
   // last, partly filled wave of chunk i overlaps the start of chunk i+1; the
   // segment count is planned for the whole call's pairs accordingly.
-  // The last `tail` chunks choose their segment count for their own pairs
-  // (shorter items, so the final judge -- and the download behind it --
-  // finishes sooner); the others plan for the whole call (PCBZ_HOST_TAIL).
+  // The first `head` / last `tail` chunks choose their segment count for
+  // their own pairs (shorter items: the GPU fills before many frames have
+  // arrived, and the final judge -- and the download behind it -- finishes
+  // sooner); the others plan for the whole call (PCBZ_HOST_HEAD / _TAIL).
   static const int64_t tail = [] {
     const char *e = getenv("PCBZ_HOST_TAIL");
     return (int64_t)(e ? atoll(e) : 0);
   }();
+  static const int64_t head = [] {
+    const char *e = getenv("PCBZ_HOST_HEAD");
+    return (int64_t)(e ? atoll(e) : 0);
+  }();
   auto chunk_plan = [&](int64_t i, Plan &pl) {
     const int64_t a = starts[i], n = sizes[i];
+    const bool own = i >= nchunks - tail || i < head;
     return make_plan(n, h, w, px, py, specs, k, a > 0 ? temporal != 0 : halo_prev != nullptr,
-                     temporal, false, pl, 1, 0, i >= nchunks - tail ? 0 : full.jp.npairs);
+                     temporal, false, pl, 1, 0, own ? 0 : full.jp.npairs);
   };
   size_t ws_bytes = 0;
   for (int64_t i = 0; i < nchunks; ++i) {
