@@ -492,13 +492,12 @@ __global__ void __launch_bounds__(32 * kMtfWarps) mtf_rank_kernel(const Block *b
       const uint32_t top = (uint32_t)(lst >> 56);
       uint32_t carry = __shfl_up_sync(0xffffffffu, top, 1);
       if (lane == 0) carry = s;
-      if (lane < pl) {
-        lst = (lst << 8) | carry;
-      } else if (lane == pl) {
-        const uint64_t keep = pk == 7 ? 0ull : (~0ull << (8 * (pk + 1)));
-        lst = (((lst << 8) | carry) & ~keep) | (lst & keep);
-      }
-      if (lane == q) myrank = (uint32_t)(8 * pl + pk);
+      // branch-free: lanes below pl shift all entries, lane pl those up to pk
+      const uint64_t shifted = (lst << 8) | carry;
+      const uint64_t keep = pk == 7 ? 0ull : (~0ull << (8 * (pk + 1)));
+      const uint64_t partial = (shifted & ~keep) | (lst & keep);
+      lst = lane < pl ? shifted : (lane == pl ? partial : lst);
+      myrank = lane == q ? (uint32_t)(8 * pl + pk) : myrank;
     }
     if (j < j1) ranks[B.base + j] = (uint8_t)myrank;
   }
