@@ -238,14 +238,15 @@ PCBZ_API int pcbz_bunzip2_host(const uint8_t *const *payloads, const int64_t *pl
 /* decompress_stack after the container is parsed: payload i = (frame
  * i / blocks_per_frame, block i % blocks_per_frame) of the frames' big-endian
  * residual streams (2*h*w bytes, block_size bytes per block), decoded on the
- * GPU, then the inverse prediction (as pcbz_reconstruct_host with sel[]) into
- * frames_out.  host_streams (nullable; entries nullable) supplies payloads the
+ * GPU, then the inverse prediction (as pcbz_reconstruct_host with sel[] and
+ * the reconstructed frame before frames_out[0], halo_prev, for a call that
+ * continues a series) into frames_out.  host_streams (nullable; entries nullable) supplies payloads the
  * caller decoded itself.  Returns PCBZ_NEEDS_HOST with status[i] = 1 for the
  * payloads the caller must decode (then call again with them in
  * host_streams); frames_out is written only when PCBZ_OK is returned. */
 PCBZ_API int pcbz_decompress_host(const uint8_t *const *payloads, const int64_t *plen, int64_t nframes,
                                   int64_t blocks_per_frame, int64_t h, int64_t w, int64_t px, int64_t py,
-                                  int64_t block_size, const uint8_t *sel,
+                                  int64_t block_size, const uint8_t *sel, const uint16_t *halo_prev,
                                   const uint8_t *const *host_streams, uint16_t *frames_out,
                                   uint8_t *status);
 

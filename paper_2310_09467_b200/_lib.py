@@ -72,7 +72,7 @@ SIGNATURES = {
                                            _vp, _vp]),
     "pcbz_bunzip2_host": (_c_int, [_vp, _vp, _c_int, _vp, _vp, _vp, _vp]),
     "pcbz_decompress_host": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64,
-                                      _vp, _vp, _vp, _vp]),
+                                      _vp, _vp, _vp, _vp, _vp]),
     "pcbz_host_alloc": (_vp, [_c_size]),
     "pcbz_host_free": (_c_int, [_vp]),
     "pcbz_gather": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int]),

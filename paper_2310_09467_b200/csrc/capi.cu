@@ -1207,8 +1207,8 @@ int pcbz_bunzip2_host(const uint8_t *const *payloads, const int64_t *plen, int n
 
 int pcbz_decompress_host(const uint8_t *const *payloads, const int64_t *plen, int64_t nframes,
                          int64_t blocks_per_frame, int64_t h, int64_t w, int64_t px, int64_t py,
-                         int64_t block_size, const uint8_t *sel, const uint8_t *const *host_streams,
-                         uint16_t *frames_out, uint8_t *status) {
+                         int64_t block_size, const uint8_t *sel, const uint16_t *halo_prev,
+                         const uint8_t *const *host_streams, uint16_t *frames_out, uint8_t *status) {
   int rc = validate_geometry(h, w, px, py);
   if (rc) return rc;
   if (nframes < 1) return fail(PCBZ_E_INVALID, "at least one frame is required");
@@ -1216,7 +1216,7 @@ int pcbz_decompress_host(const uint8_t *const *payloads, const int64_t *plen, in
   const int64_t sb = 2 * h * w;
   if (blocks_per_frame != (sb + block_size - 1) / block_size)
     return fail(PCBZ_E_INVALID, "blocks_per_frame %lld does not match the frame size", (long long)blocks_per_frame);
-  if ((rc = check_sel(sel, nframes, false))) return rc;
+  if ((rc = check_sel(sel, nframes, halo_prev != nullptr))) return rc;
   const int64_t n = nframes * blocks_per_frame;
   if (n > 0x7FFFFFFF) return fail(PCBZ_E_INVALID, "too many payloads");
   HostCtx &c = g_ctx;
@@ -1245,8 +1245,12 @@ int pcbz_decompress_host(const uint8_t *const *payloads, const int64_t *plen, in
     if (status[i]) return PCBZ_NEEDS_HOST;
   CUDA_TRY(bzd::launch_be16(c.bytes.as<uint8_t>(), (int64_t)fb / 2, c.frames.as<uint16_t>(), st));
   CUDA_TRY(cudaMemcpyAsync(c.sel.p, sel, (size_t)nframes, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(launch_reconstruct(c.frames.as<uint16_t>(), nullptr, nframes, h, w, (int)px, (int)py,
-                              c.sel.as<uint8_t>(), c.out.as<uint16_t>(), st));
+  if (halo_prev) {
+    if ((rc = c.prev.ensure((size_t)h * w * 2))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c.prev.p, halo_prev, (size_t)h * w * 2, cudaMemcpyHostToDevice, st));
+  }
+  CUDA_TRY(launch_reconstruct(c.frames.as<uint16_t>(), halo_prev ? c.prev.as<uint16_t>() : nullptr, nframes, h,
+                              w, (int)px, (int)py, c.sel.as<uint8_t>(), c.out.as<uint16_t>(), st));
   CUDA_TRY(cudaMemcpyAsync(frames_out, c.out.p, fb, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   return PCBZ_OK;

@@ -418,36 +418,47 @@ def decompress_stack(data, workers: int = 1) -> FrameStack:
     return FrameStack(tuple(Frame(f, geo) for f in out))
 
 
+#: decoded bytes per pcbz_decompress_host round (bounds device and page-locked memory)
+DECOMPRESS_ROUND_BYTES = 1 << 30
+
+
 def _decompress_device(header, records, payloads):
     """Every payload bzip2-decoded on the GPU (pcbz_decompress_host: block
     magic scan, Huffman + inverse MTF, inverse BWT by list ranking, inverse
     RLE1, all CRCs checked) and the inverse prediction run on the decoded
-    streams without leaving the device.  None when any payload or the block
-    layout is not the one compress_stack writes (the caller's host path then
-    decodes and reports errors exactly as the reference)."""
+    streams without leaving the device, in rounds of <= 1 GiB of frames (a
+    round's temporal first frame reads the previous round's last frame).
+    None when any payload or the block layout is not the one compress_stack
+    writes (the caller's host path then decodes and reports errors exactly as
+    the reference)."""
     H, W = header.height, header.width
     F = header.frame_count
     nb = -(-2 * H * W // header.block_size)
     if any(len(p) != nb for p in payloads):
         return None
-    flat = [p for ps in payloads for p in ps]
-    n = len(flat)
-    ptrs = (ctypes.c_void_p * n)(*[_lib._address(p) for p in flat])
-    lens = np.array([len(p) for p in flat], np.int64)
-    sel = np.array([r.spec.to_byte() for r in records], np.uint8)
-    status = np.ones(n, np.uint8)
-    nbytes = F * H * W * 2
-    # frames land in this thread's page-locked buffer (PCIe speed), then a
-    # multithreaded copy moves them into the returned array
-    staged = _lib.pinned_buffer(nbytes)
-    rc = _lib.load().pcbz_decompress_host(ptrs, lens.ctypes.data, F, nb, H, W, header.pitch_x,
-                                          header.pitch_y, header.block_size, _lib.ptr(sel), None,
-                                          staged.ctypes.data, status.ctypes.data)
-    if rc == _lib.PCBZ_NEEDS_HOST:
-        return None
-    _lib.check(rc)
+    sel_all = np.array([r.spec.to_byte() for r in records], np.uint8)
     out = np.empty((F, H, W), np.uint16)
-    _lib.copy_into(out, staged)
+    per = max(1, DECOMPRESS_ROUND_BYTES // (2 * H * W))
+    lib = _lib.load()
+    for a in range(0, F, per):
+        b = min(F, a + per)
+        flat = [p for ps in payloads[a:b] for p in ps]
+        n = len(flat)
+        ptrs = (ctypes.c_void_p * n)(*[_lib._address(p) for p in flat])
+        lens = np.array([len(p) for p in flat], np.int64)
+        sel = np.ascontiguousarray(sel_all[a:b])
+        status = np.ones(n, np.uint8)
+        # frames land in this thread's page-locked buffer (PCIe speed), then a
+        # multithreaded copy moves them into the returned array
+        staged = _lib.pinned_buffer((b - a) * H * W * 2)
+        halo = out[a - 1] if a > 0 else None
+        rc = lib.pcbz_decompress_host(ptrs, lens.ctypes.data, b - a, nb, H, W, header.pitch_x,
+                                      header.pitch_y, header.block_size, _lib.ptr(sel), _lib.ptr(halo),
+                                      None, staged.ctypes.data, status.ctypes.data)
+        if rc == _lib.PCBZ_NEEDS_HOST:
+            return None
+        _lib.check(rc)
+        _lib.copy_into(out[a:b], staged)
     geo = LensletGeometry(header.pitch_x, header.pitch_y)
     return FrameStack(tuple(Frame(f, geo) for f in out))
 

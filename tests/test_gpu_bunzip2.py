@@ -114,3 +114,20 @@ def test_decompress_stack_device_path_round_trip():
     fast = pipeline._decompress_device(h, r, pl)
     assert fast is not None and fast == stack
     assert decompress_stack(data) == stack
+
+
+def test_decompress_rounds_carry_the_temporal_halo(monkeypatch):
+    """Rounds of frames (DECOMPRESS_ROUND_BYTES): a round's temporal first
+    frame is reconstructed from the previous round's last frame."""
+    from paper_2310_09467_b200 import (CompressOptions, Frame, FrameStack, LensletGeometry,
+                                       compress_stack, decompress_stack, pipeline)
+    p = SynthParams(256, 160, 15, 15, mode="smooth_lenslet", noise_sigma=10.0, photon_scale=0.05,
+                    frames=7, drift=1.0, seed=6)
+    vol = generate_array(p)
+    stack = FrameStack(tuple(Frame(f, LensletGeometry(15, 15)) for f in vol))
+    from paper_2310_09467_b200 import PredictorSpec
+    r = pipeline.compress_stack_detailed(stack, CompressOptions(block_size=50_000,
+                                                                forced=PredictorSpec(True, 1)))
+    assert all(s.temporal for s in r.specs[1:])
+    monkeypatch.setattr(pipeline, "DECOMPRESS_ROUND_BYTES", 2 * 256 * 160 * 2)   # two frames per round
+    assert decompress_stack(r.data) == stack
