@@ -101,6 +101,7 @@ struct HostCtx {
   cudaStream_t stream = nullptr;
   cudaStream_t s_in = nullptr, s_out = nullptr;  // pcbz_judge_host copy streams
   cudaStream_t s_comp2 = nullptr;                // its second compute stream
+  std::vector<cudaStream_t> s_more;              // further compute streams (PCBZ_HOST_STREAMS)
   DevBuf frames, prev, out, ent, sel, stream_out, hist, ws, scratch, bytes;
   int init() {
     if (stream) return PCBZ_OK;
@@ -549,11 +550,19 @@ int pcbz_judge_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t n
     const char *e = getenv("PCBZ_HOST_HEAD");
     return (int64_t)(e ? atoll(e) : 0);
   }();
+  static const int edge_s = [] {   // segment count of the head / tail chunks (0: their own plan)
+    const char *e = getenv("PCBZ_HOST_EDGE_S");
+    return e ? atoi(e) : 0;
+  }();
   auto chunk_plan = [&](int64_t i, Plan &pl) {
     const int64_t a = starts[i], n = sizes[i];
     const bool own = i >= nchunks - tail || i < head;
-    return make_plan(n, h, w, px, py, specs, k, a > 0 ? temporal != 0 : halo_prev != nullptr,
-                     temporal, false, pl, 1, 0, own ? 0 : full.jp.npairs);
+    const int saved = g_seg_override;
+    if (own && edge_s > 0) g_seg_override = edge_s;
+    const int r = make_plan(n, h, w, px, py, specs, k, a > 0 ? temporal != 0 : halo_prev != nullptr,
+                            temporal, false, pl, 1, 0, own ? 0 : full.jp.npairs);
+    g_seg_override = saved;
+    return r;
   };
   size_t ws_bytes = 0;
   for (int64_t i = 0; i < nchunks; ++i) {
@@ -562,7 +571,13 @@ int pcbz_judge_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t n
     ws_bytes = std::max(ws_bytes, pl.ws_bytes);
   }
   ws_bytes = align_up(ws_bytes);
-  const int nws = nchunks > 1 ? 2 : 1;
+  // compute streams (one workspace each) that chunks rotate over
+  static const int nstreams = [] {
+    const char *e = getenv("PCBZ_HOST_STREAMS");
+    const int v = e ? atoi(e) : 2;
+    return v < 1 ? 1 : (v > 32 ? 32 : v);
+  }();
+  const int nws = (int)std::min<int64_t>(nchunks, nstreams);
   if ((rc = c.frames.ensure(fbytes)) || (rc = c.ent.ensure((size_t)nframes * k * 8)) ||
       (rc = c.sel.ensure((size_t)nframes)) || (rc = c.ws.ensure(nws * ws_bytes + 256)))
     return rc;
@@ -573,14 +588,21 @@ int pcbz_judge_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t n
     CUDA_TRY(cudaStreamCreateWithFlags(&c.s_out, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&c.s_comp2, cudaStreamNonBlocking));
   }
-  cudaStream_t comp[2] = {c.stream, c.s_comp2};
+  while ((int)c.s_more.size() + 2 < nws) {
+    cudaStream_t x;
+    CUDA_TRY(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    c.s_more.push_back(x);
+  }
+  std::vector<cudaStream_t> comp = {c.stream, c.s_comp2};
+  for (cudaStream_t x : c.s_more) comp.push_back(x);
+  comp.resize(std::max(nws, 1));
   int *d_err = reinterpret_cast<int *>(c.ws.as<char>() + nws * ws_bytes);  // shared by all chunks
   std::vector<cudaEvent_t> ev(2 * nchunks + 1);
   for (auto &e : ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  // both compute streams start after the error word is cleared
+  // every compute stream starts after the error word is cleared
   CUDA_TRY(cudaMemsetAsync(d_err, 0, 4, comp[0]));
   CUDA_TRY(cudaEventRecord(ev[2 * nchunks], comp[0]));
-  CUDA_TRY(cudaStreamWaitEvent(comp[1], ev[2 * nchunks], 0));
+  for (int q = 1; q < nws; ++q) CUDA_TRY(cudaStreamWaitEvent(comp[q], ev[2 * nchunks], 0));
   if (halo_prev)
     CUDA_TRY(cudaMemcpyAsync(c.prev.p, halo_prev, (size_t)npix * 2, cudaMemcpyHostToDevice, c.s_in));
   const uint16_t *d_frames = c.frames.as<uint16_t>();
@@ -596,8 +618,8 @@ int pcbz_judge_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t n
   for (int64_t i = 0; i < nchunks; ++i) {
     const int64_t a = starts[i], n = sizes[i];
     const size_t off = (size_t)a * npix;
-    cudaStream_t st = comp[i & 1];
-    char *ws = c.ws.as<char>() + (i & 1) * ws_bytes;
+    cudaStream_t st = comp[i % nws];
+    char *ws = c.ws.as<char>() + (i % nws) * ws_bytes;
     CUDA_TRY(cudaMemcpyAsync(c.frames.as<uint16_t>() + off, frames + off, (size_t)n * npix * 2,
                              cudaMemcpyHostToDevice, c.s_in));
     CUDA_TRY(cudaEventRecord(ev[2 * i], c.s_in));
