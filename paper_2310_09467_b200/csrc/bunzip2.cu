@@ -274,14 +274,20 @@ __global__ void __launch_bounds__(32 * kDecodeWarps) decode_block_kernel(
   int group_no = -1, group_pos = 0, gsel = 0;
   int32_t nblock = 0;
   uint8_t *o = L + (size_t)c * kSlot;   // next output byte
-  auto next_sym = [&](int &sym) -> bool {
+  // Symbol decoding in two halves, so the lookup-table load of the next code
+  // is in flight while the inverse MTF of the current symbol runs:
+  // begin_sym (group bookkeeping, peek, LUT load) and end_sym (consume).
+  auto begin_sym = [&](uint32_t &ent) -> bool {
     if (group_pos == 0) {
       if (++group_no >= n_sel) return false;
       group_pos = 50;
       gsel = selector[group_no];
     }
     group_pos--;
-    const uint32_t ent = S.lut[gsel][br.peek(kLutBits)];
+    ent = S.lut[gsel][br.peek(kLutBits)];
+    return true;
+  };
+  auto end_sym = [&](uint32_t ent, int &sym) -> bool {
     if (ent & 31u) {
       br.skip((int)(ent & 31u));
       sym = (int)(ent >> 5);
@@ -299,6 +305,10 @@ __global__ void __launch_bounds__(32 * kDecodeWarps) decode_block_kernel(
     if (k < 0 || k >= kMaxAlpha) return false;
     sym = S.perm[gsel][k];
     return true;
+  };
+  auto next_sym = [&](int &sym) -> bool {
+    uint32_t ent;
+    return begin_sym(ent) && end_sym(ent, sym);
   };
   int sym;
   if (!next_sym(sym)) return;
@@ -322,6 +332,10 @@ __global__ void __launch_bounds__(32 * kDecodeWarps) decode_block_kernel(
       continue;
     }
     if (nblock >= nblockMAX) return;
+    // the next code's table entry is loaded first (its bits follow this
+    // symbol's, which end_sym has already consumed)
+    uint32_t ent;
+    if (!begin_sym(ent)) return;
     // inverse MTF of index nn: entries 0..nn-1 move up one place, entry nn to the front
     const int nn = sym - 1;
     const int src = nn >> 3, b = nn & 7;
@@ -340,7 +354,7 @@ __global__ void __launch_bounds__(32 * kDecodeWarps) decode_block_kernel(
     if (lane == 0) *o = uc;
     ++o;
     nblock++;
-    if (!next_sym(sym)) return;
+    if (!end_sym(ent, sym)) return;
   }
   if (orig >= nblock || br.over()) return;
   if (lane == 0) {
