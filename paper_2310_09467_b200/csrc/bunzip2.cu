@@ -697,7 +697,13 @@ int decode_batch(const uint8_t *const *payloads, const int64_t *plen, const std:
   int ncand = 0;
   BZD_TRY(cudaMemcpyAsync(&ncand, g.ncand.p, 4, cudaMemcpyDeviceToHost, st));
   BZD_TRY(cudaStreamSynchronize(st));
-  if (ncand > kMaxCand) return 0;   // leave the whole batch to the host
+  // a real block holds >= ~700 KB of decoded bytes (RLE1 never expands a
+  // 900 KB block below that) plus one partial block per stream: far more
+  // magic candidates than that means adversarial data -- leave the batch to
+  // libbzip2 rather than allocating a slot per candidate
+  int64_t expect = 0;
+  for (int s = 0; s < ns; ++s) expect += out_len[ids[s]] / 700000 + 1;
+  if (ncand > kMaxCand || ncand > 4 * expect + 1024) return 0;
   std::vector<int64_t> key(ncand);
   if (ncand) BZD_TRY(cudaMemcpy(key.data(), g.ckey.p, (size_t)ncand * 8, cudaMemcpyDeviceToHost));
   std::sort(key.begin(), key.end());
