@@ -16,8 +16,8 @@
 //                          bit where the block ends.  The host keeps the
 //                          candidates that chain from bit 32 of each stream
 //                          (a spurious magic inside coded data never chains)
-//   3  inverse BWT         stable sort of (block, L[i]) -> the T vector of
-//                          decompress.c (tt[cftab[L[i]]++] = i), then list
+//   3  inverse BWT         stable multisplit of positions by L[i] -> the T
+//                          vector of decompress.c (tt[cftab[L[i]]++] = i), then list
 //                          ranking of the chain p <- T[p] from T[origPtr]
 //                          with rulers every 256 positions: rulers walk to the
 //                          next ruler, one thread per block ranks the rulers,
@@ -381,18 +381,77 @@ struct VBlock {          // a decoded block on a valid chain
   uint32_t crc;          // computed block CRC (pass 2)
 };
 
-__global__ void sort_keys_kernel(const VBlock *vb, int nvb, const uint8_t *L, uint32_t *keys,
-                                 uint32_t *vals, int64_t total) {
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    int lo = 0, hi = nvb - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (vb[mid].base <= g) lo = mid; else hi = mid - 1;
-    }
-    const int64_t i = g - vb[lo].base;
-    keys[g] = ((uint32_t)lo << 8) | L[(size_t)vb[lo].cand * kSlot + i];
-    vals[g] = (uint32_t)i;
+// T vector without a sort (decompress.c: tt[cftab[L[i]]++] = i): a stable
+// multisplit of each block's positions by byte value over 4 KB chunks --
+// per-chunk byte counts, per-block running offsets (one thread per byte
+// value walks the chunks), then every chunk places its positions in order, a
+// warp at a time, ranking equal bytes within the warp with __match_any_sync.
+constexpr int kTChunk = 4096;
+
+__global__ void tchunk_count_kernel(const VBlock *vb, const uint8_t *L, const int64_t *chunk_blk,
+                                    const int32_t *chunk_idx, int64_t nchunks, uint32_t *counts) {
+  __shared__ uint32_t h[256];
+  const int64_t t = blockIdx.x;
+  if (t >= nchunks) return;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const VBlock &B = vb[chunk_blk[t]];
+  const uint8_t *Lb = L + (size_t)B.cand * kSlot;
+  const int32_t a = chunk_idx[t] * kTChunk, e = min(B.n, a + kTChunk);
+  for (int32_t i = a + threadIdx.x; i < e; i += blockDim.x) atomicAdd(&h[Lb[i]], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) counts[t * 256 + i] = h[i];
+}
+
+// one CTA of 256 threads per block: counts -> absolute starts of every (chunk, byte)
+__global__ void __launch_bounds__(256) tchunk_offsets_kernel(const VBlock *vb, const int64_t *chunk0,
+                                                             uint32_t *counts) {
+  __shared__ uint32_t tot[256];
+  const int b = blockIdx.x, c = threadIdx.x;
+  const int64_t c0 = chunk0[b], c1 = chunk0[b + 1];
+  uint32_t run = 0;
+  for (int64_t t = c0; t < c1; ++t) {
+    const uint32_t v = counts[t * 256 + c];
+    counts[t * 256 + c] = run;
+    run += v;
+  }
+  tot[c] = run;
+  __syncthreads();
+  uint32_t base = 0;   // cftab[c]: bytes below c in the block
+  for (int k = 0; k < c; ++k) base += tot[k];
+  for (int64_t t = c0; t < c1; ++t) counts[t * 256 + c] += base;
+  (void)vb;
+}
+
+// one warp per chunk: T[start(byte) + rank] = position, in position order
+__global__ void tchunk_place_kernel(const VBlock *vb, const uint8_t *L, const int64_t *chunk_blk,
+                                    const int32_t *chunk_idx, int64_t nchunks, const uint32_t *starts,
+                                    uint32_t *T) {
+  __shared__ uint32_t next[4][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * 4 + warp;
+  if (t >= nchunks) return;
+  const VBlock &B = vb[chunk_blk[t]];
+  const uint8_t *Lb = L + (size_t)B.cand * kSlot;
+  uint32_t *Tb = T + B.base;
+  uint32_t *nx = next[warp];
+  for (int i = lane; i < 256; i += 32) nx[i] = starts[t * 256 + i];
+  __syncwarp();
+  const int32_t a = chunk_idx[t] * kTChunk, e = min(B.n, a + kTChunk);
+  for (int32_t p0 = a; p0 < e; p0 += 32) {
+    const int32_t p = p0 + lane;
+    const bool valid = p < e;
+    const uint32_t c = valid ? Lb[p] : 256u + lane;   // invalid lanes never match a byte
+    const uint32_t peers = __match_any_sync(0xffffffffu, c);
+    const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (valid && lane == leader) base = nx[c];
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (valid) Tb[base + rank] = (uint32_t)p;
+    __syncwarp();
+    if (valid && lane == leader) nx[c] = base + __popc(peers);
+    __syncwarp();
   }
 }
 
@@ -630,8 +689,8 @@ struct Buf {
 };
 
 struct Ctx {
-  Buf in, off, ckey, ncand, cand, L, vb, keys, vals, keys2, vals2, tmp, rblk, rnext, rlen, rrank, bwt;
-  Buf zs, crcacc, cblk, cidx, sel;
+  Buf in, off, ckey, ncand, cand, L, vb, vals2, rblk, rnext, rlen, rrank, bwt;
+  Buf zs, crcacc, cblk, cidx, sel, tcb, tci, tc0, tcnt;
   bool zs_ready = false;
 };
 thread_local Ctx g;
@@ -795,21 +854,36 @@ int decode_batch(const uint8_t *const *payloads, const int64_t *plen, const std:
       for (int k = 0; k < vb[i].nr; ++k) rblk[vb[i].r0 + k] = i;
     BZD_TRY(g.vb.ensure((size_t)nvb * sizeof(VBlock)));
     BZD_TRY(cudaMemcpyAsync(g.vb.p, vb.data(), (size_t)nvb * sizeof(VBlock), cudaMemcpyHostToDevice, st));
-    // 3: T vector by a stable sort of (block, L[i])
-    BZD_TRY(g.keys.ensure((size_t)tot * 4));
-    BZD_TRY(g.vals.ensure((size_t)tot * 4));
-    BZD_TRY(g.keys2.ensure((size_t)tot * 4));
-    BZD_TRY(g.vals2.ensure((size_t)tot * 4));
-    sort_keys_kernel<<<grid_of(tot), 256, 0, st>>>(g.vb.as<VBlock>(), nvb, g.L.as<uint8_t>(), g.keys.as<uint32_t>(),
-                                                   g.vals.as<uint32_t>(), tot);
-    int end_bit = 8;
-    while ((1ll << (end_bit - 8)) < nvb) ++end_bit;
-    size_t tb = 0;
-    BZD_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, g.keys.as<uint32_t>(), g.keys2.as<uint32_t>(),
-                                            g.vals.as<uint32_t>(), g.vals2.as<uint32_t>(), (int64_t)tot, 0, end_bit, st));
-    BZD_TRY(g.tmp.ensure(tb));
-    BZD_TRY(cub::DeviceRadixSort::SortPairs(g.tmp.p, tb, g.keys.as<uint32_t>(), g.keys2.as<uint32_t>(),
-                                            g.vals.as<uint32_t>(), g.vals2.as<uint32_t>(), (int64_t)tot, 0, end_bit, st));
+    // 3: T vector by a stable multisplit of each block's positions by byte
+    {
+      std::vector<int64_t> cb, c0(nvb + 1, 0);
+      std::vector<int32_t> ci;
+      for (int i = 0; i < nvb; ++i) {
+        c0[i] = (int64_t)cb.size();
+        for (int32_t k = 0; (int64_t)k * kTChunk < vb[i].n; ++k) {
+          cb.push_back(i);
+          ci.push_back(k);
+        }
+      }
+      c0[nvb] = (int64_t)cb.size();
+      const int64_t ntc = (int64_t)cb.size();
+      BZD_TRY(g.vals2.ensure((size_t)tot * 4));
+      BZD_TRY(g.tcb.ensure((size_t)std::max<int64_t>(ntc, 1) * 8));
+      BZD_TRY(g.tci.ensure((size_t)std::max<int64_t>(ntc, 1) * 4));
+      BZD_TRY(g.tc0.ensure((size_t)(nvb + 1) * 8));
+      BZD_TRY(g.tcnt.ensure((size_t)std::max<int64_t>(ntc, 1) * 256 * 4));
+      BZD_TRY(cudaMemcpyAsync(g.tcb.p, cb.data(), (size_t)ntc * 8, cudaMemcpyHostToDevice, st));
+      BZD_TRY(cudaMemcpyAsync(g.tci.p, ci.data(), (size_t)ntc * 4, cudaMemcpyHostToDevice, st));
+      BZD_TRY(cudaMemcpyAsync(g.tc0.p, c0.data(), (size_t)(nvb + 1) * 8, cudaMemcpyHostToDevice, st));
+      if (ntc) {
+        tchunk_count_kernel<<<(unsigned)ntc, 256, 0, st>>>(g.vb.as<VBlock>(), g.L.as<uint8_t>(), g.tcb.as<int64_t>(),
+                                                           g.tci.as<int32_t>(), ntc, g.tcnt.as<uint32_t>());
+        tchunk_offsets_kernel<<<nvb, 256, 0, st>>>(g.vb.as<VBlock>(), g.tc0.as<int64_t>(), g.tcnt.as<uint32_t>());
+        tchunk_place_kernel<<<(unsigned)((ntc + 3) / 4), 128, 0, st>>>(g.vb.as<VBlock>(), g.L.as<uint8_t>(),
+                                                                     g.tcb.as<int64_t>(), g.tci.as<int32_t>(), ntc,
+                                                                     g.tcnt.as<uint32_t>(), g.vals2.as<uint32_t>());
+      }
+    }
     mark("sort");
     const uint32_t *T = g.vals2.as<uint32_t>();
     chain_start_kernel<<<(nvb + 255) / 256, 256, 0, st>>>(g.vb.as<VBlock>(), nvb, T);
