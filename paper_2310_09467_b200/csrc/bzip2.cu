@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -1039,6 +1040,8 @@ int sort_rotations(Block *d_blocks, const int *d_ids, int nb, int nslots, const 
   BZ_TRY(cudaMemcpyAsync(&h_nsel, d_nsel, sizeof(int), cudaMemcpyDeviceToHost, st));
   BZ_TRY(cudaStreamSynchronize(st));
   uint32_t m = (uint32_t)h_nsel;
+  static const bool trace = getenv("PCBZ_HOST_TRACE") != nullptr;
+  if (trace) fprintf(stderr, "bwt: N %u, unresolved after 4-byte keys %u\n", N, m);
   for (uint64_t h = 4; m > 0; h *= 2) {
     pair_keys_kernel<<<grid_of(m), 256, 0, st>>>(U, m, sa, rank, block_of, d_blocks, h, keys_a, vals_a);
     tb = t_all;
@@ -1053,6 +1056,7 @@ int sort_rotations(Block *d_blocks, const int *d_ids, int nb, int nslots, const 
     BZ_TRY(cudaMemcpyAsync(&h_nsel, d_nsel, sizeof(int), cudaMemcpyDeviceToHost, st));
     BZ_TRY(cudaStreamSynchronize(st));
     m = (uint32_t)h_nsel;
+    if (trace) fprintf(stderr, "bwt: unresolved after %llu-byte prefixes %u\n", (unsigned long long)(2 * h), m);
     std::swap(U, U2);
   }
   return PCBZ_OK;
