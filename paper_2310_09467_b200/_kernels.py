@@ -71,6 +71,20 @@ def bwt_pair_hist(s) -> np.ndarray:
     return out
 
 
+def reconstruct_image(res, intra_id, px, py) -> np.ndarray:
+    """Inverse of residual_image on the device (reference _kernels.py:69-90):
+    the causal row-major recurrence as anti-diagonal wavefronts
+    (pcbz_reconstruct_host, one frame, non-temporal mode byte)."""
+    r = _img(res)
+    if not 0 <= int(intra_id) <= 12:
+        raise ValueError(f"intra predictor id must be in [0, 12], got {intra_id}")
+    out = np.empty_like(r)
+    sel = np.array([int(intra_id)], np.uint8)
+    _lib.check(_lib.load().pcbz_reconstruct_host(_lib.ptr(r), None, 1, r.shape[0], r.shape[1], int(px),
+                                                 int(py), _lib.ptr(sel), _lib.ptr(out)))
+    return out
+
+
 def temporal_delta_samples(cur: np.ndarray, prev: np.ndarray) -> np.ndarray:
     """(cur - prev) mod 2^16 on the device (reference predictors.py:116-120)."""
     c = np.ascontiguousarray(cur, dtype=np.uint16)

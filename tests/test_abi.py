@@ -87,3 +87,13 @@ def test_gather_rejects_bad_pieces():
     lens = np.array([4, -1], np.int64)
     srcs = (ctypes.c_void_p * 2)(dst.ctypes.data, dst.ctypes.data)
     assert lib.pcbz_gather(dst.ctypes.data, srcs, lens.ctypes.data, 2, 2) == _lib.PCBZ_E_INVALID
+
+
+def test_temporal_undelta_inverts_the_delta():
+    from paper_2310_09467_b200 import Frame, LensletGeometry, temporal_undelta
+    rng = np.random.default_rng(9)
+    geo = LensletGeometry(3, 3)
+    cur = rng.integers(0, 65536, (17, 11), dtype=np.uint16)
+    prev = rng.integers(0, 65536, (17, 11), dtype=np.uint16)
+    delta = ((cur.astype(np.int32) - prev.astype(np.int32)) % 65536).astype(np.uint16)
+    assert np.array_equal(temporal_undelta(Frame(delta, geo), Frame(prev, geo)).samples, cur)

@@ -131,3 +131,21 @@ def test_decompress_rounds_carry_the_temporal_halo(monkeypatch):
     assert all(s.temporal for s in r.specs[1:])
     monkeypatch.setattr(pipeline, "DECOMPRESS_ROUND_BYTES", 2 * 256 * 160 * 2)   # two frames per round
     assert decompress_stack(r.data) == stack
+
+
+def test_inverse_predictor_mirrors():
+    """unpredict_frame / invert_predictor (reference predictors.py:101-147)
+    invert predict_frame / apply_predictor exactly, every intra id, with and
+    without the temporal flag."""
+    from paper_2310_09467_b200 import (Frame, LensletGeometry, PredictorSpec, apply_predictor,
+                                       invert_predictor, predict_frame, unpredict_frame)
+    rng = np.random.default_rng(3)
+    geo = LensletGeometry(6, 5)
+    cur = Frame(rng.integers(0, 65536, (37, 53), dtype=np.uint16), geo)
+    prev = Frame(rng.integers(0, 65536, (37, 53), dtype=np.uint16), geo)
+    for i in range(13):
+        assert unpredict_frame(predict_frame(cur, i), i) == cur
+        for t in (False, True):
+            spec = PredictorSpec(t, i)
+            assert invert_predictor(apply_predictor(cur, spec, prev if t else None), spec,
+                                    prev if t else None) == cur
