@@ -144,6 +144,8 @@ class _PinnedCache(threading.local):
         self.addr, self.size = None, 0
 
     def get(self, nbytes: int) -> np.ndarray:
+        if nbytes > PINNED_MAX:   # do not pin very large buffers: pageable, not cached
+            return np.empty(max(int(nbytes), 1), np.uint8)
         if nbytes > self.size:
             lib = load()
             if self.addr:
@@ -151,11 +153,14 @@ class _PinnedCache(threading.local):
                 self.addr, self.size = None, 0
             size = max(int(nbytes), 1 << 20)
             addr = lib.pcbz_host_alloc(size)
-            if not addr:
-                check(PCBZ_E_CUDA)
+            if not addr:          # page-locked memory exhausted: pageable for this call
+                return np.empty(max(int(nbytes), 1), np.uint8)
             self.addr, self.size = addr, size
         return np.ctypeslib.as_array((ctypes.c_uint8 * self.size).from_address(self.addr))[:nbytes]
 
+
+#: largest page-locked buffer the cache keeps per thread (bigger requests get pageable memory)
+PINNED_MAX = 2 << 30
 
 _pinned = _PinnedCache()
 
