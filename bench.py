@@ -271,7 +271,8 @@ def pipeline_e2e(wl: Workload, host: np.ndarray) -> dict:
     return {"compress_GBps": raw / t_c / 1e9, "decompress_GBps": raw / t_d / 1e9,
             "compression_ratio": raw / len(data), "lossless": bool(np.array_equal(back.to_array(), host)),
             "what": "compress_stack (device judge + emission + bzip2 on the GPU, container) and "
-                    f"decompress_stack (bzip2 decoding and inverse prediction on the GPU), wall clock, "
+                    f"decompress_stack (bzip2 decoding on the GPU for large containers, on host threads for "
+                    "small ones; inverse prediction on the GPU), wall clock, "
                     "informational (not the metric)"}
 
 

@@ -101,6 +101,17 @@ def test_periodic_and_corrupt_payloads_left_to_libbzip2():
         bunzip2_blocks_device([bytes(bad)], [len(good)])
 
 
+def test_device_decode_chosen_for_large_containers():
+    """Small containers decode faster on host threads (one slow warp per
+    block vs libbzip2 per thread); the device decoder takes large ones."""
+    from paper_2310_09467_b200 import pipeline
+    from paper_2310_09467_b200.codec import ContainerHeader
+    big = ContainerHeader(2048, 2048, 100, 15, 15, 4 << 20, False)
+    small = ContainerHeader(2048, 2048, 1, 15, 15, 4 << 20, False)
+    assert pipeline._prefer_device_decode(big, [[b"x", b"y"]] * 100, 16)
+    assert not pipeline._prefer_device_decode(small, [[b"x", b"y"]], 16)
+
+
 def test_decompress_stack_device_path_round_trip():
     from paper_2310_09467_b200 import (CompressOptions, Frame, FrameStack, LensletGeometry,
                                        compress_stack, decompress_stack, pipeline)
@@ -130,6 +141,10 @@ def test_decompress_rounds_carry_the_temporal_halo(monkeypatch):
                                                                 forced=PredictorSpec(True, 1)))
     assert all(s.temporal for s in r.specs[1:])
     monkeypatch.setattr(pipeline, "DECOMPRESS_ROUND_BYTES", 2 * 256 * 160 * 2)   # two frames per round
+    from paper_2310_09467_b200.codec import read_container
+    h, recs, pl = read_container(r.data)
+    fast = pipeline._decompress_device(h, recs, pl)
+    assert fast is not None and fast == stack
     assert decompress_stack(r.data) == stack
 
 
