@@ -273,7 +273,9 @@ __global__ void __launch_bounds__(32 * kDecodeWarps) decode_block_kernel(
   const int EOB = n_in_use + 1;
   int group_no = -1, group_pos = 0, gsel = 0;
   int32_t nblock = 0;
-  uint8_t *o = L + (size_t)c * kSlot;   // next output byte
+  uint8_t *o = L + (size_t)c * kSlot;   // next output byte (after the buffered ones)
+  int pend = 0;                           // MTF bytes buffered in lanes 0..pend-1
+  uint8_t obyte = 0;
   // Symbol decoding in two halves, so the lookup-table load of the next code
   // is in flight while the inverse MTF of the current symbol runs:
   // begin_sym (group bookkeeping, peek, LUT load) and end_sym (consume).
@@ -326,6 +328,11 @@ __global__ void __launch_bounds__(32 * kDecodeWarps) decode_block_kernel(
       const uint32_t front = (uint32_t)__shfl_sync(0xffffffffu, (uint32_t)x, 0) & 0xFFu;
       const uint8_t uc = S.seq[front];
       if (nblock + es > nblockMAX) return;
+      if (pend) {            // the buffered MTF bytes precede the run
+        if (lane < pend) o[lane] = obyte;
+        o += pend;
+        pend = 0;
+      }
       for (int32_t k = lane; k < es; k += 32) o[k] = uc;
       nblock += es;
       o += es;
@@ -339,9 +346,7 @@ __global__ void __launch_bounds__(32 * kDecodeWarps) decode_block_kernel(
     // inverse MTF of index nn: entries 0..nn-1 move up one place, entry nn to the front
     const int nn = sym - 1;
     const int src = nn >> 3, b = nn & 7;
-    const uint32_t slo = __shfl_sync(0xffffffffu, (uint32_t)x, src);
-    const uint32_t shi = __shfl_sync(0xffffffffu, (uint32_t)(x >> 32), src);
-    const uint32_t v = (uint32_t)(((((uint64_t)shi << 32) | slo) >> (8 * b)) & 0xFFu);
+    const uint32_t v = __shfl_sync(0xffffffffu, (uint32_t)(x >> (8 * b)) & 0xFFu, src);
     const uint32_t top = __shfl_up_sync(0xffffffffu, (uint32_t)(x >> 56), 1);
     const uint64_t cin = lane == 0 ? v : top;
     // lanes below src shift all eight entries, lane src the ones below b
@@ -351,11 +356,17 @@ __global__ void __launch_bounds__(32 * kDecodeWarps) decode_block_kernel(
     const uint64_t partial = (x & keep) | ((x & lowmask) << 8) | cin;
     x = lane < src ? shifted : (lane == src ? partial : x);
     const uint8_t uc = S.seq[v];
-    if (lane == 0) *o = uc;
-    ++o;
+    // lane `pend` keeps this byte; 32 of them leave as one coalesced store
+    obyte = lane == pend ? uc : obyte;
+    if (++pend == 32) {
+      o[lane] = obyte;
+      o += 32;
+      pend = 0;
+    }
     nblock++;
     if (!end_sym(ent, sym)) return;
   }
+  if (pend && lane < pend) o[lane] = obyte;
   if (orig >= nblock || br.over()) return;
   if (lane == 0) {
     C.crc = crc;
