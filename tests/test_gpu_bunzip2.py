@@ -164,3 +164,26 @@ def test_inverse_predictor_mirrors():
             spec = PredictorSpec(t, i)
             assert invert_predictor(apply_predictor(cur, spec, prev if t else None), spec,
                                     prev if t else None) == cur
+
+
+def test_corrupt_payload_on_the_device_path_raises_like_the_reference():
+    """A flipped byte in one payload of a container large enough for the
+    device decoder: the block CRC check hands the container to the host path,
+    which raises BlockDecodeError (blocks.py:84-92 semantics)."""
+    from paper_2310_09467_b200 import (CompressOptions, Frame, FrameStack, LensletGeometry,
+                                       compress_stack, decompress_stack, pipeline)
+    from paper_2310_09467_b200.codec import BlockDecodeError, read_container
+    p = SynthParams(512, 512, 15, 15, mode="beads", signal_amplitude=3000, noise_sigma=100,
+                    photon_scale=0.05, frames=16, seed=8)
+    vol = generate_array(p)
+    stack = FrameStack(tuple(Frame(f, LensletGeometry(15, 15)) for f in vol))
+    data = bytearray(compress_stack(stack, CompressOptions(block_size=16384)))
+    h, recs, pl = read_container(bytes(data))
+    assert pipeline._prefer_device_decode(h, pl, 1)
+    assert decompress_stack(bytes(data)) == stack
+    victim = pl[5][3]
+    pos = bytes(data).find(bytes(victim))   # the payload's offset in the container
+    assert pos > 0
+    data[pos + len(victim) // 2] ^= 0x21
+    with pytest.raises(BlockDecodeError):
+        decompress_stack(bytes(data))
