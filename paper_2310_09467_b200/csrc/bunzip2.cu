@@ -9,11 +9,12 @@
 //                          the 48-bit block magic 0x314159265359 (blocks are
 //                          not byte-aligned and their starts are only known
 //                          after decoding the previous block)
-//   2  decode_block_kernel one thread per candidate: block header, selector
+//   2  decode_block_kernel one warp per candidate: block header, selector
 //                          MTF, delta-coded code lengths, canonical Huffman
-//                          decode, RUNA/RUNB, inverse MTF (word-shifted list)
-//                          -> the BWT last column L and its byte counts, the
-//                          bit where the block ends.  The host keeps the
+//                          decode through a 10-bit lookup table (all lanes in
+//                          lockstep), RUNA/RUNB, inverse MTF with the list in
+//                          registers (8 entries per lane) -> the BWT last
+//                          column L, the bit where the block ends.  The host keeps the
 //                          candidates that chain from bit 32 of each stream
 //                          (a spurious magic inside coded data never chains)
 //   3  inverse BWT         stable multisplit of positions by L[i] -> the T
@@ -33,8 +34,6 @@
 // is shorter than the block, trailing data, a CRC mismatch) is reported so the
 // caller decodes that payload with libbzip2, which also produces the
 // reference's exception for corrupt data.
-#include <cub/cub.cuh>
-
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
