@@ -35,6 +35,7 @@
 // caller decodes that payload with libbzip2, which also produces the
 // reference's exception for corrupt data.
 #include <algorithm>
+#include <string>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
