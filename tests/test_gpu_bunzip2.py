@@ -187,3 +187,20 @@ def test_corrupt_payload_on_the_device_path_raises_like_the_reference():
     data[pos + len(victim) // 2] ^= 0x21
     with pytest.raises(BlockDecodeError):
         decompress_stack(bytes(data))
+
+
+def test_compress_from_non_contiguous_frames():
+    """pcbz_compress_frames_host takes one pointer per frame: frames that are
+    strided views are made contiguous individually, and the container equals
+    the one from a stacked copy."""
+    from paper_2310_09467_b200 import CompressOptions, Frame, FrameStack, LensletGeometry, compress_stack
+    p = SynthParams(256, 320, 15, 15, mode="smooth_lenslet", noise_sigma=10.0, photon_scale=0.05,
+                    frames=3, drift=1.0, seed=12)
+    vol = generate_array(p)                       # [3, 320, 256]
+    wide = np.zeros((3, 320, 512), np.uint16)
+    wide[:, :, ::2] = vol                         # every frame a strided view
+    geo = LensletGeometry(15, 15)
+    views = FrameStack(tuple(Frame(wide[i, :, ::2], geo) for i in range(3)))
+    dense = FrameStack(tuple(Frame(np.ascontiguousarray(vol[i]), geo) for i in range(3)))
+    opts = CompressOptions(block_size=40_000)
+    assert compress_stack(views, opts) == compress_stack(dense, opts)
