@@ -3,7 +3,9 @@ entropy-judgement stage on the B200 (the drop-in boundary).
 
 level="kernels": replace the compiled kernels the reference looks up at call
     time (pcbz._kernels.residual_bwt_pair_hist / residual_image /
-    counting_bwt / pair_hist / bwt_pair_hist, reference _kernels.py:46-154).
+    reconstruct_image / counting_bwt / pair_hist / bwt_pair_hist, reference
+    _kernels.py:46-154) -- reconstruct_image moves the reference's own
+    decompress_stack inverse prediction (predictors.py:101-106) to the GPU.
     Entropies are then still reduced by the reference's numpy entropy2d, so
     its exact-float tests hold unchanged.
 level="api" (default): additionally replace select_predictor in every module
@@ -63,8 +65,8 @@ def install(pcbz=None, level: str = "api"):
         raise ValueError("level must be 'api' or 'kernels'")
     _lib.load()
     k = pcbz._kernels
-    for name in ("residual_bwt_pair_hist", "residual_image", "counting_bwt", "pair_hist",
-                 "bwt_pair_hist"):
+    for name in ("residual_bwt_pair_hist", "residual_image", "reconstruct_image", "counting_bwt",
+                 "pair_hist", "bwt_pair_hist"):
         setattr(k, name, getattr(_kernels, name))
     if level == "api":
         fn = _device_select(pcbz)

@@ -31,6 +31,7 @@ def test_install_api_level_rebinds_every_name(pcbz_ref):
     b200.install(pcbz_ref)
     assert pcbz_ref._kernels.residual_bwt_pair_hist is _kernels.residual_bwt_pair_hist
     assert pcbz_ref._kernels.residual_image is _kernels.residual_image
+    assert pcbz_ref._kernels.reconstruct_image is _kernels.reconstruct_image
     fn = pcbz_ref.criterion.select_predictor
     assert fn is not orig and fn.__wrapped_reference__ is orig
     assert pcbz_ref.pipeline.select_predictor is fn
