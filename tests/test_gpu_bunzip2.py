@@ -204,3 +204,18 @@ def test_compress_from_non_contiguous_frames():
     dense = FrameStack(tuple(Frame(np.ascontiguousarray(vol[i]), geo) for i in range(3)))
     opts = CompressOptions(block_size=40_000)
     assert compress_stack(views, opts) == compress_stack(dense, opts)
+
+
+def test_unusual_streams_left_to_libbzip2():
+    """Two concatenated streams, trailing bytes after the end-of-stream
+    marker, a truncated stream and an empty stream: the device decoder takes
+    only the well-formed ones (bz2.decompress semantics stay with libbzip2)."""
+    rng = np.random.default_rng(21)
+    a = bytes(rng.integers(0, 9, 50_000, dtype=np.uint8))
+    b = bytes(rng.integers(0, 200, 30_000, dtype=np.uint8))
+    pa, pb = bz2.compress(a, 9), bz2.compress(b, 9)
+    cases = [(pa + pb, a + b), (pa + b"\x00\x01", a), (pa[:-7], a), (bz2.compress(b"", 9), b""), (pa, a)]
+    st, got = _status([p for p, _ in cases], [len(x) for _, x in cases])
+    assert list(st[:3]) == [1, 1, 1]
+    assert st[3] == 0 and got[3] == b""
+    assert st[4] == 0 and got[4] == a
