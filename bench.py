@@ -30,8 +30,6 @@ import subprocess
 import sys
 import threading
 import time
-from concurrent.futures import ProcessPoolExecutor
-from dataclasses import dataclass
 from pathlib import Path
 
 import numpy as np
@@ -40,99 +38,11 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "entropy-judge GB/s raw uint16 LFM at 1/2/4/8 B200; % HBM peak; CR parity"
-INTRA = list(range(13))
-ALL26 = INTRA + [0x80 | i for i in INTRA]
-SNR_LEVELS = [  # (count, amplitude, sigma, photon) -- SURVEY.md §8(d) C2
-    (34, 20000.0, 0.0, 0.05),
-    (33, 3000.0, 100.0, 0.05),
-    (33, 3000.0, 500.0, 0.01),
-]
 
-
-@dataclass(frozen=True)
-class Workload:
-    name: str
-    description: str
-    frames: int
-    height: int
-    width: int
-    pitch: int
-    codes: tuple
-    temporal: bool
-    series: bool      # True: one series sharded over ranks (strong), False: per-rank batch (weak)
-
-
-WORKLOADS = {
-    "c2": Workload("c2", "C2: 100 independent 2048x2048 uint16 bead frames, pitch 15x15, 3 SNR levels, "
-                   "13 intra candidates, judge + emission", 100, 2048, 2048, 15, tuple(INTRA), False, False),
-    "c1": Workload("c1", "C1: one 2048x2048 bead frame (amp 3000, sigma 20, photon 0.05), pitch 15x15, "
-                   "13 intra candidates, judge + emission", 1, 2048, 2048, 15, tuple(INTRA), False, False),
-    "c3": Workload("c3", "C3 prefix: 100-frame 2048x2048 smooth_lenslet series, pitch 15x15, drift 1, "
-                   "temporal on (26 candidates from frame 1), frames sharded over ranks with a 1-frame halo",
-                   100, 2048, 2048, 15, tuple(ALL26), True, True),
-    "c4": Workload("c4", "C4: 8-frame 4096x4096 smooth_lenslet series, pitch 13x13, drift 1, temporal on "
-                   "(26 candidates), frames sharded over ranks with a 1-frame halo",
-                   8, 4096, 4096, 13, tuple(ALL26), True, True),
-}
-
-
-def c2_params():
-    from paper_2310_09467_b200.lfm_synth import SynthParams
-    out, seed = [], 0
-    for count, amp, sigma, photon in SNR_LEVELS:
-        for _ in range(count):
-            out.append(SynthParams(2048, 2048, 15, 15, mode="beads", signal_amplitude=amp,
-                                   noise_sigma=sigma, photon_scale=photon, frames=1, seed=seed))
-            seed += 1
-    return out
-
+from workloads.configs import (ALL26, INTRA, SNR_LEVELS, WORKLOADS, Workload, c2_params,  # noqa: E402
+                               make_frames, series_params)
 
 frame_params = c2_params  # used by tools/
-
-
-def _gen_one(p):
-    from paper_2310_09467_b200.lfm_synth import generate_array
-    return generate_array(p)[0]
-
-
-_SERIES = {}
-
-
-def _gen_series_frame(t):
-    from paper_2310_09467_b200.lfm_synth import noisy_frame
-    base, p = _SERIES["base"], _SERIES["params"]
-    return noisy_frame(base, p, t)
-
-
-def series_params(wl: Workload):
-    from paper_2310_09467_b200.lfm_synth import SynthParams
-    return SynthParams(wl.width, wl.height, wl.pitch, wl.pitch, mode="smooth_lenslet",
-                       signal_amplitude=20000.0, noise_sigma=20.0, photon_scale=0.05,
-                       frames=wl.frames, drift=1.0, seed=0)
-
-
-def make_frames(wl: Workload, index: range, workers: int) -> np.ndarray:
-    """Frames `index` of the workload (C2: per-frame seeds; series: one scene)."""
-    vol = np.empty((len(index), wl.height, wl.width), np.uint16)
-    if wl.name == "c1":
-        from paper_2310_09467_b200.lfm_synth import SynthParams, generate_array
-        vol[0] = generate_array(SynthParams(2048, 2048, 15, 15, mode="beads", signal_amplitude=3000.0,
-                                            noise_sigma=20.0, photon_scale=0.05, seed=0))[0]
-        return vol
-    if not wl.series:
-        params = [c2_params()[i] for i in index]
-        with ProcessPoolExecutor(max(1, workers)) as ex:
-            for i, fr in enumerate(ex.map(_gen_one, params, chunksize=2)):
-                vol[i] = fr
-        return vol
-    from paper_2310_09467_b200.lfm_synth import scene
-    p = series_params(wl)
-    _SERIES["base"], _SERIES["params"] = scene(p), p   # inherited by forked workers
-    import multiprocessing as mpm
-    with ProcessPoolExecutor(max(1, workers), mp_context=mpm.get_context("fork")) as ex:
-        for i, fr in enumerate(ex.map(_gen_series_frame, list(index), chunksize=2)):
-            vol[i] = fr
-    return vol
 
 
 def config(wl: Workload, extra=None):

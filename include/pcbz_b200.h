@@ -86,6 +86,19 @@ PCBZ_API int pcbz_bwt_pair_hist(const uint8_t *s, int64_t n, int64_t *hist_out);
 /* pcbz.criterion.entropy2d (criterion.py:86-96) of a 65536-bin histogram. */
 PCBZ_API int pcbz_entropy2d(const int64_t *counts, int64_t total, double *out);
 
+/* The transcendental of entropy2d (criterion.py:94-95: p = counts / total,
+ * p * np.log2(p)) evaluated by the host: terms[c] = (c / total) *
+ * log2(c / total) for c = 1..total, n = total + 1 entries (terms[0] unused).
+ * Copied to the current device once per (device, total) and used by every
+ * later judge / entropy call with that total, so the device's fixed-order
+ * pairwise sum reproduces the host's entropy2d bit for bit (the Python layer
+ * registers np.log2 terms, i.e. the reference's own numpy).  Without a
+ * table the device evaluates log2 itself (<= 1 ulp per term, entropies
+ * within 1e-15 relative).  Idempotent; PCBZ_E_INVALID when the tables would
+ * exceed PCBZ_TERMS_BUDGET_MB (default 4096) of device memory. */
+PCBZ_API int pcbz_register_entropy_terms(int64_t total, const double *terms, int64_t n);
+PCBZ_API int pcbz_entropy_terms_registered(int64_t total);
+
 /* ---------------------------------------------------------------------
  * API-level: the entropy judge.
  * ------------------------------------------------------------------- */

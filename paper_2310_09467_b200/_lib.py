@@ -40,6 +40,8 @@ SIGNATURES = {
     "pcbz_pair_hist": (_c_int, [_vp, _c_i64, _vp]),
     "pcbz_bwt_pair_hist": (_c_int, [_vp, _c_i64, _vp]),
     "pcbz_entropy2d": (_c_int, [_vp, _c_i64, _vp]),
+    "pcbz_register_entropy_terms": (_c_int, [_c_i64, _vp, _c_i64]),
+    "pcbz_entropy_terms_registered": (_c_int, [_c_i64]),
     "pcbz_select_predictor": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _c_int,
                                        _vp, _vp, _vp]),
     "pcbz_judge_host": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _c_int,
@@ -123,6 +125,38 @@ def ptr(a: np.ndarray | None):
         return None
     assert a.flags["C_CONTIGUOUS"], "native calls need C-contiguous buffers"
     return a.ctypes.data
+
+
+#: largest total (2*H*W - 1) whose entropy term table is registered (8 bytes per count)
+TERMS_MAX_TOTAL = 1 << 27
+_terms_lock = threading.Lock()
+
+
+def ensure_entropy_terms(total: int) -> bool:
+    """Register this host's numpy terms p * log2(p), p = c / total, for
+    every count c = 0..total with the current device (once per total), so
+    device entropies are bit-identical to the reference's numpy entropy2d
+    (criterion.py:94-95) evaluated on this host.  Returns False (device log2,
+    <= 1 ulp per term) when the table would be too large."""
+    total = int(total)
+    if total < 1 or total > TERMS_MAX_TOTAL:
+        return False
+    lib = load()
+    if lib.pcbz_entropy_terms_registered(total):
+        return True
+    with _terms_lock:
+        if lib.pcbz_entropy_terms_registered(total):
+            return True
+        # exactly the reference's evaluation: int64 counts / float(total), np.log2, product
+        p = np.arange(total + 1, dtype=np.int64) / float(total)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            t = p * np.log2(p)
+        t[0] = 0.0
+        rc = lib.pcbz_register_entropy_terms(total, t.ctypes.data, t.size)
+        if rc == PCBZ_E_INVALID:   # over the device-memory budget: device log2 for this total
+            return False
+        check(rc)
+    return True
 
 
 def version() -> str:

@@ -66,6 +66,7 @@ def entropy2d(hist: PairHistogram) -> float:
         return 0.0
     c = np.ascontiguousarray(np.where(hist.counts > 0, hist.counts, 0), dtype=np.int64)
     out = np.zeros(1, np.float64)
+    _lib.ensure_entropy_terms(int(hist.total))
     _lib.check(_lib.load().pcbz_entropy2d(_lib.ptr(c), int(hist.total), _lib.ptr(out)))
     return float(out[0])
 
@@ -79,6 +80,7 @@ def candidate_entropy(residual) -> float:
     ent = np.zeros(1, np.float64)
     sel = np.zeros(1, np.uint8)
     h, w = img.shape
+    _lib.ensure_entropy_terms(2 * h * w - 1)
     _lib.check(_lib.load().pcbz_select_predictor(_lib.ptr(img), None, h, w, 1, 1, _lib.ptr(spec), 1,
                                                  _lib.ptr(ent), _lib.ptr(sel), None))
     return float(ent[0])
@@ -141,6 +143,7 @@ def select_predictor(frame: Frame, prev: Frame | None = None, candidates=None,
     img = frame.samples
     h, w = img.shape
     use_prev = prev is not None and any(s.temporal for s in specs)
+    _lib.ensure_entropy_terms(2 * h * w - 1)
     _lib.check(_lib.load().pcbz_select_predictor(
         _lib.ptr(img), _lib.ptr(prev.samples) if use_prev else None, h, w, geo.pitch_x,
         geo.pitch_y, _lib.ptr(codes), k, _lib.ptr(ent), _lib.ptr(sel), _lib.ptr(hist)))

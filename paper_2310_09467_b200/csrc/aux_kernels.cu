@@ -80,11 +80,12 @@ __global__ void bwt_scatter_kernel(const uint8_t *s, int64_t n, int64_t nchunks,
 }
 
 __global__ void __launch_bounds__(kEntropyThreads) entropy_u64_kernel(const uint64_t *counts, double total,
+                                                                    const double *terms, int64_t nterms,
                                                                     double *out) {
   extern __shared__ uint4 smem_raw[];
   NpScratch &scr = *reinterpret_cast<NpScratch *>(smem_raw);
   auto get = [&](int bin) -> uint64_t { return counts[bin]; };
-  const double e = block_entropy(get, total, scr, nullptr);
+  const double e = block_entropy(get, total, scr, terms, false, nterms);
   if (threadIdx.x == 0) *out = e;
 }
 
@@ -156,8 +157,8 @@ cudaError_t launch_counting_bwt(const uint8_t *s, int64_t n, uint8_t *out, uint3
   return cudaGetLastError();
 }
 
-cudaError_t launch_entropy_u64(const uint64_t *counts, double total, double *out,
-                               cudaStream_t st) {
+cudaError_t launch_entropy_u64(const uint64_t *counts, double total, const double *terms,
+                               int64_t nterms, double *out, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
     const cudaError_t e = cudaFuncSetAttribute(entropy_u64_kernel,
@@ -166,7 +167,7 @@ cudaError_t launch_entropy_u64(const uint64_t *counts, double total, double *out
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  entropy_u64_kernel<<<1, kEntropyThreads, sizeof(NpScratch), st>>>(counts, total, out);
+  entropy_u64_kernel<<<1, kEntropyThreads, sizeof(NpScratch), st>>>(counts, total, terms, nterms, out);
   return cudaGetLastError();
 }
 

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -114,6 +115,26 @@ struct HostCtx {
 
 thread_local HostCtx g_ctx;
 
+// Host-registered entropy term tables (pcbz_register_entropy_terms), one per
+// (device, total), process-wide and never freed (a kernel enqueued by any
+// thread may still read one), within a memory budget.
+struct TermTable {
+  int dev;
+  int64_t total;
+  double *d;
+};
+std::mutex g_terms_mu;
+std::vector<TermTable> g_terms;
+size_t g_terms_bytes = 0;
+
+size_t terms_budget() {
+  static const size_t b = [] {
+    const char *e = getenv("PCBZ_TERMS_BUDGET_MB");
+    return (size_t)(e ? atoll(e) : 4096) << 20;
+  }();
+  return b;
+}
+
 int validate_geometry(int64_t h, int64_t w, int64_t px, int64_t py) {
   if (h < 1 || w < 1) return fail(PCBZ_E_INVALID, "frame must contain at least one sample (h=%lld w=%lld)", (long long)h, (long long)w);
   if (px < 1 || py < 1) return fail(PCBZ_E_INVALID, "pitch must be positive (px=%lld py=%lld)", (long long)px, (long long)py);
@@ -204,6 +225,18 @@ int build_lists(const uint8_t *specs, int k, bool halo, int temporal, CandLists 
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// entropy terms of a plan: the host's table for this total if registered,
+// else the per-call device table of the first kTermTable counts
+// (term_table_kernel; larger counts evaluated inline)
+bool use_registered_terms(JudgeParams &jp) {
+  int64_t nt = 0;
+  const double *t = registered_terms(2 * jp.npix - 1, &nt);
+  if (!t) return false;
+  jp.terms = t;
+  jp.nterms = nt;
+  return true;
+}
 
 // Run-length weight (in 1/16) of the two warps that own a scheduler alone
 // (judge_kernel.cuh); tunable through PCBZ_LONE_WEIGHT for measurements.
@@ -313,6 +346,8 @@ int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double 
   jp.err = d_err_shared ? d_err_shared : reinterpret_cast<int *>(ws + pl.off_err);
   jp.fscratch = reinterpret_cast<uint8_t *>(ws + pl.off_fscratch);
   jp.terms = reinterpret_cast<const double *>(ws + pl.off_terms);
+  jp.nterms = kTermTable;
+  const bool host_terms = use_registered_terms(jp);
   if (!jp.direct) {
     jp.segsum = reinterpret_cast<int16_t *>(ws + pl.off_segsum);
     jp.ghist = d_hist ? d_hist : reinterpret_cast<uint32_t *>(ws + pl.off_ghist);
@@ -337,8 +372,10 @@ int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double 
     g_trace_segments = jp.S;
   }
   CUDA_TRY(cudaMemsetAsync(ws, 0, pl.off_terms, st));   // counter + err
-  CUDA_TRY(launch_term_table((double)(2 * jp.npix - 1), reinterpret_cast<double *>(ws + pl.off_terms), st));
-  ++launches;
+  if (!host_terms) {
+    CUDA_TRY(launch_term_table((double)(2 * jp.npix - 1), reinterpret_cast<double *>(ws + pl.off_terms), st));
+    ++launches;
+  }
   CUDA_TRY(cudaMemsetAsync(d_ent, 0xFF, (size_t)jp.nframes * jp.cl.k * sizeof(double), st));  // NaN
   if (!jp.direct)
     CUDA_TRY(cudaMemsetAsync(jp.ghist, 0, (size_t)jp.nframes * jp.cl.k * 65536 * 4, st));
@@ -817,7 +854,10 @@ int pcbz_entropy2d(const int64_t *counts, int64_t total, double *out) {
   if ((rc = c.hist.ensure(65536 * 8)) || (rc = c.ent.ensure(8))) return rc;
   cudaStream_t st = c.stream;
   CUDA_TRY(cudaMemcpyAsync(c.hist.p, counts, 65536 * 8, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(launch_entropy_u64(c.hist.as<uint64_t>(), total > 0 ? (double)total : 0.0, c.ent.as<double>(), st));
+  int64_t nt = 0;
+  const double *terms = total > 0 ? registered_terms(total, &nt) : nullptr;
+  CUDA_TRY(launch_entropy_u64(c.hist.as<uint64_t>(), total > 0 ? (double)total : 0.0, terms, nt,
+                              c.ent.as<double>(), st));
   CUDA_TRY(cudaMemcpyAsync(out, c.ent.p, 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   return PCBZ_OK;
@@ -826,6 +866,42 @@ int pcbz_entropy2d(const int64_t *counts, int64_t total, double *out) {
 }  // extern "C"
 
 extern "C" {
+
+// Entropy terms evaluated by the host (e.g. the reference's own numpy):
+// terms[c] = p * log2(p) with p = c / total for c = 1..total (terms[0] is
+// unused).  Every later judge / entropy call on this device whose total
+// matches reduces these exact values (entropy.cuh), so the entropies are
+// bit-identical to the host's entropy2d.
+int pcbz_register_entropy_terms(int64_t total, const double *terms, int64_t n) {
+  if (total < 1 || n != total + 1 || !terms)
+    return fail(PCBZ_E_INVALID, "entropy term table needs total >= 1 and total + 1 entries (total=%lld n=%lld)",
+                (long long)total, (long long)n);
+  int rc = check_device();
+  if (rc) return rc;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_terms_mu);
+  for (const TermTable &t : g_terms)
+    if (t.dev == dev && t.total == total) return PCBZ_OK;
+  const size_t bytes = (size_t)n * sizeof(double);
+  if (g_terms_bytes + bytes > terms_budget())
+    return fail(PCBZ_E_INVALID, "entropy term tables would exceed PCBZ_TERMS_BUDGET_MB (%zu + %zu bytes)",
+                g_terms_bytes, bytes);
+  double *d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, bytes));
+  if (cudaMemcpy(d, terms, bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return fail(PCBZ_E_CUDA, "copy of the entropy term table failed");
+  }
+  g_terms.push_back({dev, total, d});
+  g_terms_bytes += bytes;
+  return PCBZ_OK;
+}
+
+int pcbz_entropy_terms_registered(int64_t total) {
+  int64_t nt = 0;
+  return registered_terms(total, &nt) != nullptr ? 1 : 0;
+}
 
 int pcbz_set_segment_override(int segments) {
   g_seg_override = segments > 0 ? segments : 0;
@@ -981,14 +1057,18 @@ int pcbz_judge_merge_device(int64_t nframes, int64_t h, int64_t w, int64_t px, i
   jp.segsum = const_cast<int16_t *>(d_summaries);
   jp.ent = d_ent_out;
   double *terms = nullptr;  // stream-ordered scratch: this entry point has no workspace
-  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&terms), kTermTable * sizeof(double), st));
-  CUDA_TRY(launch_term_table((double)(2 * jp.npix - 1), terms, st));
-  jp.terms = terms;
+  const bool host_terms = use_registered_terms(jp);
+  if (!host_terms) {
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&terms), kTermTable * sizeof(double), st));
+    CUDA_TRY(launch_term_table((double)(2 * jp.npix - 1), terms, st));
+    jp.terms = terms;
+    jp.nterms = kTermTable;
+  }
   CUDA_TRY(cudaMemsetAsync(d_ent_out, 0xFF, (size_t)nframes * k * sizeof(double), st));  // NaN
   CUDA_TRY(launch_finalize(jp, st));
   CUDA_TRY(launch_select(jp, d_sel_out, st));
-  CUDA_TRY(cudaFreeAsync(terms, st));
-  g_launches = 3;
+  if (terms) CUDA_TRY(cudaFreeAsync(terms, st));
+  g_launches = host_terms ? 2 : 3;
   return PCBZ_OK;
 }
 
@@ -1279,3 +1359,15 @@ int pcbz_decompress_host(const uint8_t *const *payloads, const int64_t *plen, in
 }
 
 }  // extern "C"
+
+const double *pcbz::registered_terms(int64_t total, int64_t *nterms) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_terms_mu);
+  for (const TermTable &t : g_terms)
+    if (t.dev == dev && t.total == total) {
+      *nterms = total + 1;
+      return t.d;
+    }
+  return nullptr;
+}

@@ -102,10 +102,14 @@ __device__ __forceinline__ double np_term(double c, double total) {
   return __dmul_rn(p, log2(p));
 }
 
-// terms[c] = np_term(c, total) for c < kTermTable (judge.cuh; one table per
-// call: every pair of a judge call has the same total 2*H*W - 1), so the
-// per-bin divide and log2 become one L2-resident load; identical bits by
-// construction.
+// terms[c] for c < nterms: either np_term(c, total) for c < kTermTable
+// (term_table_kernel, one table per call: every pair of a judge call has the
+// same total 2*H*W - 1), or a table the host registered for this total with
+// pcbz_register_entropy_terms -- p * log2(p) evaluated by the host's own numpy
+// for every count 0..total, so that every term, and with the emulated
+// pairwise sum the entropy, has the reference's exact bits (numpy's SIMD
+// log2 is not correctly rounded; the device's log2 differs from it in the
+// last ulp for ~0.02 % of arguments).
 
 // `get(bin)` returns the bin count (integer; 0 = empty); all threads of the
 // block (kEntropyThreads) must call this.  `terms` may be null.
@@ -113,7 +117,7 @@ __device__ __forceinline__ double np_term(double c, double total) {
 // 32w + j occupied) and synchronised.
 template <typename Get>
 __device__ double block_entropy(Get get, double total, NpScratch &S, const double *terms,
-                                bool occ_ready = false) {
+                                bool occ_ready = false, int64_t nterms = kTermTable) {
   const int t = threadIdx.x;
   // occupancy bitmap: one warp per 32-bin word (lane j reads bin 32w + j,
   // so the reads are bank-conflict free), a ballot makes the word
@@ -179,8 +183,9 @@ __device__ double block_entropy(Get get, double total, NpScratch &S, const doubl
     };
     auto term_of = [&](uint64_t c) -> double {
       if (!terms) return np_term((double)c, total);
-      const double v = __ldg(terms + (c < (uint64_t)kTermTable ? c : 0));
-      return c < (uint64_t)kTermTable ? v : np_term((double)c, total);
+      const bool in = c < (uint64_t)nterms;
+      const double v = __ldg(terms + (in ? c : 0));
+      return in ? v : np_term((double)c, total);
     };
     auto next_term = [&]() -> double { return term_of(get(next_bin())); };
     // eight terms at a time: bin indices first (bitmap walk), then all eight

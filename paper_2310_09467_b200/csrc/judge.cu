@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
     const uint32_t c = c16[bin];
     return c < 0xFFFFu ? c : __ldcg(G + bin);
   };
-  const double e = block_entropy(get, (double)(2 * P.npix - 1), scr, P.terms, true);
+  const double e = block_entropy(get, (double)(2 * P.npix - 1), scr, P.terms, true, P.nterms);
   if (threadIdx.x == 0) P.ent[pr.slot] = e;
 }
 

@@ -68,7 +68,8 @@ struct JudgeParams {
   int fast_px;              // >0: 8-pixel chunk path instantiated for pitch_x; 0: generic
   int lone_weight;          // run-length weight (x16) of warps alone on a scheduler
   double *ent;              // [nframes][k] (NaN = not scored)
-  const double *terms;      // [65536] entropy terms of this call's total (entropy.cuh)
+  const double *terms;      // [nterms] entropy terms of this call's total (entropy.cuh)
+  int64_t nterms;           // kTermTable (device table) or total + 1 (host-registered table)
   uint32_t *ghist;          // [nframes*k][65536] when !direct
   int16_t *segsum;          // [nbands][nframes*k][S][2][256] when !direct
   uint8_t *fscratch;        // [gridDim.x][kJudgeThreads][256]
@@ -102,7 +103,10 @@ cudaError_t launch_counting_bwt(const uint8_t *s, int64_t n, uint8_t *out, uint3
                                 size_t scratch_words, cudaStream_t st);
 size_t counting_bwt_scratch_words(int64_t n);
 cudaError_t launch_term_table(double total, double *terms, cudaStream_t st);
-cudaError_t launch_entropy_u64(const uint64_t *counts, double total, double *out, cudaStream_t st);
+cudaError_t launch_entropy_u64(const uint64_t *counts, double total, const double *terms,
+                               int64_t nterms, double *out, cudaStream_t st);
+// host-registered entropy term table of `total` on the current device (capi.cu), or nullptr
+const double *registered_terms(int64_t total, int64_t *nterms);
 cudaError_t launch_reconstruct(const uint16_t *res, const uint16_t *halo, int64_t nframes,
                                int64_t h, int64_t w, int px, int py, const uint8_t *sel,
                                uint16_t *out, cudaStream_t st);

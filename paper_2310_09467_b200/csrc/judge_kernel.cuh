@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
           for (int i = 0; i < ns; ++i) c += spill_w[i] == (uint32_t)bin ? kSpill : 0u;
         return c;
       };
-      const double e = block_entropy(get, (double)(2 * P.npix - 1), scr, P.terms);
+      const double e = block_entropy(get, (double)(2 * P.npix - 1), scr, P.terms, false, P.nterms);
       if (tid == 0) P.ent[pr.slot] = e;
     } else {
       // flush into the pair's global histogram and publish the summary

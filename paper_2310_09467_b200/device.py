@@ -32,6 +32,8 @@ class DeviceJudge:
         self.temporal = 1 if temporal else 0
         self.device = torch.device(device or "cuda")
         lib = _lib.load()
+        with torch.cuda.device(self.device):
+            _lib.ensure_entropy_terms(2 * H * W - 1)
         ws = lib.pcbz_judge_workspace_size(F, H, W, self.k, 1 if want_hist else 0)
         if ws == 0:
             raise ValueError("invalid judge shape")
@@ -88,6 +90,8 @@ class BandJudge:
         self.band, self.nbands = int(band), int(nbands)
         self.device = torch.device(device or "cuda")
         lib = _lib.load()
+        with torch.cuda.device(self.device):
+            _lib.ensure_entropy_terms(2 * H * W - 1)
         S, sb, ws = ctypes.c_int(), ctypes.c_size_t(), ctypes.c_size_t()
         _lib.check(lib.pcbz_band_layout(F, H, W, self.px, self.py, self.codes.ctypes.data, self.k,
                                         self.temporal, self.has_halo, self.nbands, ctypes.byref(S),

@@ -46,6 +46,7 @@ def _device_select(pcbz):
         ent = np.zeros(codes.size, np.float64)
         sel = np.zeros(1, np.uint8)
         geo = frame.geometry
+        _lib.ensure_entropy_terms(2 * img.size - 1)
         _lib.check(_lib.load().pcbz_select_predictor(
             _lib.ptr(img), _lib.ptr(pv), img.shape[0], img.shape[1], geo.pitch_x, geo.pitch_y,
             _lib.ptr(codes), codes.size, _lib.ptr(ent), _lib.ptr(sel), None))

@@ -89,6 +89,7 @@ def judge_volume(vol: np.ndarray, geo: LensletGeometry, codes: list, temporal: b
         ent = np.empty((F, spec.size), np.float64)
         sel = np.empty(F, np.uint8)
         stream = np.empty((F, 2 * H * W), np.uint8) if want_stream else None
+    _lib.ensure_entropy_terms(2 * H * W - 1)
     _lib.check(_lib.load().pcbz_judge_host(
         _lib.ptr(vol), _lib.ptr(halo), F, H, W, geo.pitch_x, geo.pitch_y, _lib.ptr(spec), spec.size,
         1 if temporal else 0, _lib.ptr(ent), _lib.ptr(sel), _lib.ptr(stream)))
@@ -117,6 +118,8 @@ def encode_volume(vol, geo: LensletGeometry, codes, temporal: bool,
         if any(f.shape != (H, W) for f in frames):
             raise ValueError("all frames must have the same shape")
     lib = _lib.load()
+    if forced_sel is None:
+        _lib.ensure_entropy_terms(2 * H * W - 1)
     nb = -(-2 * H * W // block_size)
     cap = lib.pcbz_compress_bound(F, H, W, block_size)
     # views: payloads land in this thread's page-locked buffer (valid until

@@ -58,6 +58,25 @@ def golden_c1():
     return json.loads((GOLDEN / "c1_2048.json").read_text())
 
 
+def log2_fingerprint() -> str:
+    """sha256 of this host's np.log2 over the entropy probabilities of a
+    2048x2048 frame (p = c / (2*2048*2048 - 1), c = 1..65535) and 65536
+    random doubles in (0, 1].  numpy picks its log2 implementation by CPU
+    features at run time (not correctly rounded on AVX-512 hosts), so the
+    reference's entropies are bit-reproducible only on hosts with the same
+    fingerprint as the one that generated the goldens."""
+    N = 2 * 2048 * 2048 - 1
+    p = np.arange(1, 65536, dtype=np.int64) / float(N)
+    q = 1.0 - np.random.default_rng(0).random(65536)
+    return sha(np.concatenate([np.log2(p), np.log2(q)]))
+
+
+@pytest.fixture(scope="session")
+def same_log2_as_golden() -> bool:
+    want = json.loads((GOLDEN / "log2_fingerprint.json").read_text())["sha256"]
+    return log2_fingerprint() == want
+
+
 def golden_hist(arrays, name, fi, code):
     h = np.zeros(65536, np.int64)
     h[arrays[f"{name}/f{fi}/c{code}/bins"]] = arrays[f"{name}/f{fi}/c{code}/counts"]

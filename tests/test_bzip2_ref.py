@@ -11,7 +11,7 @@ import pytest
 
 import bzip2_ref as R
 import oracle
-from paper_2310_09467_b200.lfm_synth import SynthParams, generate_array
+from workloads.lfm_synth import SynthParams, generate_array
 
 
 def _cases(seed, count):

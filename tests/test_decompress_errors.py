@@ -12,7 +12,7 @@ import pytest
 import oracle
 from paper_2310_09467_b200 import BlockDecodeError, CorruptContainerError, decompress_stack
 from paper_2310_09467_b200.codec import HEADER_SIZE
-from paper_2310_09467_b200.lfm_synth import SynthParams, generate_array
+from workloads.lfm_synth import SynthParams, generate_array
 
 
 @pytest.fixture(scope="module")

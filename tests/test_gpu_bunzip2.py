@@ -13,7 +13,7 @@ import pytest
 
 from paper_2310_09467_b200 import _lib
 from paper_2310_09467_b200.codec import bunzip2_blocks_device
-from paper_2310_09467_b200.lfm_synth import SynthParams, generate_array
+from workloads.lfm_synth import SynthParams, generate_array
 
 pytestmark = pytest.mark.gpu
 

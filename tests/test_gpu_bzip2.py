@@ -10,7 +10,7 @@ import pytest
 
 import oracle
 from paper_2310_09467_b200.codec import bz2_blocks_device
-from paper_2310_09467_b200.lfm_synth import SynthParams, generate_array
+from workloads.lfm_synth import SynthParams, generate_array
 
 pytestmark = pytest.mark.gpu
 

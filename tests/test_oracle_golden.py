@@ -79,7 +79,7 @@ def test_small_cases_containers(golden_small):
 
 @pytest.mark.slow
 def test_medium_cases(golden_medium):
-    from paper_2310_09467_b200.lfm_synth import SynthParams, generate_array
+    from workloads.lfm_synth import SynthParams, generate_array
     for case in golden_medium:
         p = case["params"]
         vol = generate_array(SynthParams(**p))
@@ -99,7 +99,7 @@ def test_medium_cases(golden_medium):
 
 @pytest.mark.slow
 def test_c1_full_size_histograms(golden_c1):
-    from paper_2310_09467_b200.lfm_synth import SynthParams, generate_array
+    from workloads.lfm_synth import SynthParams, generate_array
     vol = generate_array(SynthParams(**golden_c1["params"]))
     entries, selected, hists = oracle.select_predictor(vol[0], None, list(range(13)), 15, 15)
     assert [sha(h) for h in hists] == golden_c1["hist_sha"]

@@ -12,7 +12,7 @@ import torch.multiprocessing as mp
 import oracle
 from conftest import sha
 from paper_2310_09467_b200.core import LensletGeometry
-from paper_2310_09467_b200.lfm_synth import SynthParams, generate_array
+from workloads.lfm_synth import SynthParams, generate_array
 from paper_2310_09467_b200.shard import compress_sharded, plan_frame_shards
 
 

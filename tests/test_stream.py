@@ -12,7 +12,7 @@ from conftest import sha
 from paper_2310_09467_b200 import CompressOptions, PredictorSpec
 from paper_2310_09467_b200.codec import ContainerWriter, write_container, CompressedBlocks, BlockPlan
 from paper_2310_09467_b200.core import LensletGeometry
-from paper_2310_09467_b200.lfm_synth import SynthParams, generate_array
+from workloads.lfm_synth import SynthParams, generate_array
 from paper_2310_09467_b200.pipeline import compress_stream
 
 

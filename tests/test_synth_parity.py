@@ -3,7 +3,7 @@ the reference, tests/golden/synth_hashes.json).  CPU only."""
 import pytest
 
 from conftest import sha
-from paper_2310_09467_b200.lfm_synth import SynthParams, generate_array
+from workloads.lfm_synth import SynthParams, generate_array
 
 FAST = ["small_smooth", "small_beads"]
 SLOW = ["c1_beads_2048_p15", "c2_high_seed1", "c2_mid_seed40", "c2_low_seed80", "c3_series_prefix3"]

@@ -17,6 +17,8 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import bench  # noqa: E402
+import workloads.configs as wc  # noqa: E402
+import workloads.configs as wc  # noqa: E402
 from paper_2310_09467_b200 import pipeline  # noqa: E402
 from paper_2310_09467_b200.core import LensletGeometry  # noqa: E402
 
@@ -24,7 +26,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 100
 params = bench.frame_params()[:n]
 from concurrent.futures import ProcessPoolExecutor  # noqa: E402
 with ProcessPoolExecutor(os.cpu_count() or 1) as ex:
-    vol = np.stack(list(ex.map(bench._gen_one, params)))
+    vol = np.stack(list(ex.map(wc._gen_one, params)))
 H, W = vol.shape[1:]
 pinned = torch.empty(vol.shape, dtype=torch.uint16).pin_memory()
 pinned.numpy()[...] = vol

@@ -20,7 +20,7 @@ from paper_2310_09467_b200.device import DeviceJudge  # noqa: E402
 n = int(os.environ.get("PCBZ_PROFILE_FRAMES", "12"))
 params = bench.frame_params()
 pick = [params[i] for i in np.linspace(0, len(params) - 1, n).astype(int)]
-from paper_2310_09467_b200.lfm_synth import generate_array  # noqa: E402
+from workloads.lfm_synth import generate_array  # noqa: E402
 vol = np.stack([generate_array(p)[0] for p in pick])
 frames = torch.from_numpy(vol).cuda()
 codes = [int(c) for c in os.environ.get("PCBZ_PROFILE_CODES", ",".join(map(str, range(13)))).split(",")]

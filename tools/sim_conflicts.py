@@ -9,7 +9,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parents[1]
 sys.path[:0] = [str(ROOT), str(ROOT / "oracle")]
 import oracle  # noqa: E402
-from paper_2310_09467_b200.lfm_synth import SynthParams, generate_array  # noqa: E402
+from workloads.lfm_synth import SynthParams, generate_array  # noqa: E402
 
 
 def events(res):

@@ -20,6 +20,8 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 import bench  # noqa: E402
+import workloads.configs as wc  # noqa: E402
+import workloads.configs as wc  # noqa: E402
 from paper_2310_09467_b200 import CompressOptions, LensletGeometry  # noqa: E402
 from paper_2310_09467_b200.pipeline import compress_stream  # noqa: E402
 
@@ -54,16 +56,16 @@ def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
     chunk = int(sys.argv[2]) if len(sys.argv) > 2 else 32
     wl = bench.Workload("c3", "C3", n, 2048, 2048, 15, tuple(bench.ALL26), True, True)
-    from paper_2310_09467_b200.lfm_synth import scene
+    from workloads.lfm_synth import scene
     p = bench.series_params(wl)
-    bench._SERIES["base"], bench._SERIES["params"] = scene(p), p   # inherited by forked workers
+    wc._SERIES["base"], wc._SERIES["params"] = scene(p), p   # inherited by forked workers
     cores = os.cpu_count() or 1
     gen_procs = max(1, cores // 2)
     ctx = mp.get_context("fork")
     sink = CountingSink()
     t0 = time.perf_counter()
     with ctx.Pool(gen_procs) as pool:
-        frames = pool.imap(bench._gen_series_frame, range(n), chunksize=2)
+        frames = pool.imap(wc._gen_series_frame, range(n), chunksize=2)
         res = compress_stream(frames, LensletGeometry(15, 15), sink,
                               CompressOptions(workers=cores), nframes=n, chunk_frames=chunk)
     dt = time.perf_counter() - t0

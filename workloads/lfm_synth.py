@@ -121,6 +121,6 @@ def generate_array(p: SynthParams, frames: range | None = None) -> np.ndarray:
 
 def generate(p: SynthParams):
     """FrameStack like reference synth.generate (synth.py:128-142)."""
-    from .core import FrameStack, LensletGeometry
+    from paper_2310_09467_b200.core import FrameStack, LensletGeometry
 
     return FrameStack.from_array(generate_array(p), LensletGeometry(p.pitch_x, p.pitch_y))
