@@ -45,36 +45,48 @@ from workloads.configs import (ALL26, INTRA, SNR_LEVELS, WORKLOADS, Workload, c2
 frame_params = c2_params  # used by tools/
 
 
-def config(wl: Workload, extra=None):
+def config(wl: Workload, world: int = 1, shard: str = "frames"):
+    """The workload description -- identical on both arms (ours / reference)."""
     nbytes = wl.frames * 2 * wl.height * wl.width
     c = {"workload": wl.description, "frames": wl.frames, "height": wl.height, "width": wl.width,
          "pitch": [wl.pitch, wl.pitch], "candidates": len(wl.codes), "temporal": wl.temporal,
          "l2_policy": (f"inputs ({nbytes / 1e6:.0f} MB/GPU) larger than L2 (126 MB), no flush"
                        if nbytes > 126e6 else "input smaller than L2: L2 flushed (256 MB write) before every step")}
-    if extra:
-        c.update(extra)
+    if shard == "bands":
+        c["parallelism"] = (f"within-frame bands x{world} (NCCL all-reduce of partial pair histograms + "
+                            "all-gather of segment summaries)")
+    elif world > 1:
+        c["parallelism"] = (f"frame shards x{world} (1-frame halo, no collective)" if wl.series
+                            else f"replicas x{world} (no collective)")
+    else:
+        c["parallelism"] = "single GPU"
     return c
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons, sampled every 50 ms for the
+    whole run from a background reader; `summary(t0, t1)` keeps the rows
+    that arrived inside a region (perf_counter times)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []   # (t, fields)
         self.proc = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                  "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
+            t0 = time.perf_counter()
+            while not self.rows and time.perf_counter() - t0 < 5.0:   # first row = sampler live
+                time.sleep(0.02)
         except OSError:
             self.proc = None
         return self
@@ -83,22 +95,23 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 6:
-                self.rows.append(parts)
+                self.rows.append((time.perf_counter(), parts))
 
-    def __exit__(self, *exc):
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
-    def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v.lower() == "active"})
+    def summary(self, t0: float, t1: float):
+        rows = [r for t, r in self.rows if t0 <= t <= t1 + 0.06]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        num = lambda s: s.replace(".", "").isdigit()  # noqa: E731
+        sm = [float(r[0]) for r in rows if num(r[0])]
+        reasons = sorted({n for r in rows for n, v in zip(self.NAMES, r[2:]) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "sm_max_mhz": float(rows[0][1]) if num(rows[0][1]) else None,
+                "reasons": reasons, "samples": len(rows), "window_s": round(t1 - t0, 3)}
 
 
 def measured_peak_hbm():
@@ -113,27 +126,100 @@ def profile_json(name):
     return json.loads(p.read_text()) if p.exists() else None
 
 
-def cpu_reference_sample(wl: Workload, vol: np.ndarray, nthreads: int):
-    """Time the CPU port of the reference path (oracle: C restatement, pthreads
-    over (frame, candidate) like the reference's ThreadPool) on `vol`;
-    returns (GB/s raw, seconds, frames)."""
+def _oracle():
     sys.path.insert(0, str(ROOT / "oracle"))
-    import oracle
+    import oracle   # the checker / CPU baseline only (never the measured path)
+    return oracle
+
+
+def cpu_reference_sample(wl: Workload, vol: np.ndarray, nthreads: int, halo=None):
+    """Time the CPU port of the reference path (oracle/pcbz_oracle.c: pthreads
+    over (frame, candidate) like the reference's ThreadPool, criterion.py:
+    165-169) on `vol`; returns (GB/s raw, seconds, (ent, sel, streams)).
+    Series: frame f is judged against frame f-1 (the halo for f = 0); a
+    series' first frame without a halo gets the intra candidates only
+    (pipeline.py:67-73, 87), its temporal entropies are NaN."""
+    oracle = _oracle()
     oracle.select_batch(vol[:1, :64, :64], None, INTRA, wl.pitch, wl.pitch, nthreads=1)   # load/warm
-    prevs = None
-    codes = list(wl.codes)
-    if wl.temporal:
-        prevs = np.concatenate([vol[:1], vol[:-1]])   # frame 0 scored against itself (timing only)
+    codes = sorted(wl.codes)
     t0 = time.perf_counter()
-    oracle.select_batch(vol, prevs, codes, wl.pitch, wl.pitch, nthreads=nthreads)
+    if not wl.temporal:
+        out = oracle.select_batch(vol, None, codes, wl.pitch, wl.pitch, nthreads=nthreads)
+    elif halo is not None:
+        prevs = np.concatenate([halo[None], vol[:-1]])
+        out = oracle.select_batch(vol, prevs, codes, wl.pitch, wl.pitch, nthreads=nthreads)
+    else:
+        e0, s0, st0 = oracle.select_batch(vol[:1], None, [c for c in codes if not c & 0x80], wl.pitch,
+                                          wl.pitch, nthreads=nthreads)
+        e1, s1, st1 = oracle.select_batch(vol[1:], vol[:-1], codes, wl.pitch, wl.pitch, nthreads=nthreads)
+        ent = np.full((vol.shape[0], len(codes)), np.nan)
+        ent[0, [i for i, c in enumerate(codes) if not c & 0x80]] = e0[0]
+        ent[1:] = e1
+        out = (ent, np.concatenate([s0, s1]), np.concatenate([st0, st1]))
     dt = time.perf_counter() - t0
-    return vol.shape[0] * 2 * wl.height * wl.width / dt / 1e9, dt, vol.shape[0]
+    return vol.shape[0] * 2 * wl.height * wl.width / dt / 1e9, dt, out
+
+
+def numba_reference_sample(wl: Workload, vol: np.ndarray, cores: int) -> dict:
+    """The reference's own CPU path (pcbz installed under baseline/_ref,
+    numba kernels) on a bounded sample of the
+    workload: select_predictor (criterion.py:136-173) at workers 1 and
+    `cores`, and compress_stack_detailed's select / encode split
+    (pipeline.py:76-113).  Informational second baseline."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "pcbz").exists():
+        return {"unavailable": "baseline/_ref not installed"}
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/pcbz_numba_cache")
+    sys.path.insert(0, str(ref))
+    try:
+        import pcbz
+        from pcbz import _kernels as rk
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": f"import pcbz failed: {e!r}"}
+    finally:
+        sys.path.remove(str(ref))
+    t0 = time.perf_counter()
+    rk.warm_up()
+    warm = time.perf_counter() - t0
+    geo = pcbz.LensletGeometry(wl.pitch, wl.pitch)
+    fr = [pcbz.Frame(np.ascontiguousarray(v), geo) for v in vol]
+    codes = [pcbz.PredictorSpec.from_byte(c) for c in wl.codes if not c & 0x80]
+    nbytes = 2 * wl.height * wl.width
+    out = {"what": "reference pcbz (baseline/_ref, numba) on this host, intra candidates, frames of this workload",
+           "jit_warm_up_s": warm, "cpu": _cpu_model()}
+    for w, nf in ((1, 1), (cores, min(len(fr), 4))):
+        t0 = time.perf_counter()
+        for f in fr[:nf]:
+            pcbz.select_predictor(f, None, codes, workers=w)
+        dt = time.perf_counter() - t0
+        out[f"select_predictor_workers{w}"] = {"frames": nf, "s_per_frame": dt / nf,
+                                               "GBps": nf * nbytes / dt / 1e9}
+    stack = pcbz.FrameStack(tuple(fr[:2]))
+    r = pcbz.compress_stack_detailed(stack, pcbz.CompressOptions(workers=cores, temporal=False,
+                                                                  candidates=tuple(codes)))
+    out["compress_stack_detailed"] = {"frames": 2, "workers": cores, "select_s": r.select_seconds,
+                                      "encode_s": r.encode_seconds,
+                                      "GBps": 2 * nbytes / (r.select_seconds + r.encode_seconds) / 1e9}
+    return out
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args, wl: Workload):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: the reference path on this box's host cores, rank 0
+    only; the C restatement of the reference (the reference itself is
+    Python/numba, faster-than-reference port = conservative ratio)."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return 0
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     cores = os.cpu_count() or 1
     nf = min(wl.frames, int(os.environ.get("PCBZ_REF_SAMPLE_FRAMES", str(wl.frames))))
     vol = make_frames(wl, range(nf), cores)
@@ -146,22 +232,71 @@ def run_reference(args, wl: Workload):
     t = statistics.mean(times)
     v = nf * 2 * wl.height * wl.width / t / 1e9
     sample = (f"{nf} of the {wl.frames} workload frames per step, judge ({len(wl.codes)} candidates) "
-              f"+ emission, C port of the reference path on {cores} threads")
-    print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+              f"+ emission, C port of the reference path (oracle/pcbz_oracle.c) on {cores} threads")
+    res = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong" if wl.series else "weak", "vs_baseline": None, "dtype": "u16",
-        "data": "synthetic", "config": config(wl, {"sample_frames_per_step": nf}),
-        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample},
+        "data": "synthetic (reference synth.generate, bit-identical)", "config": config(wl, world, args.shard),
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample,
+                         "cpu": _cpu_model()},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
+    }
+    if not args.no_cpu_baseline:
+        res["reference_numba"] = numba_reference_sample(wl, vol, cores)
+    print(json.dumps(res), flush=True)
     return 0
 
 
-def pipeline_e2e(wl: Workload, host: np.ndarray) -> dict:
+def parity_vs_oracle(wl: Workload, host, halo, sel, ent, streams, oracle_out, pipeline_container, block_size):
+    """Bench-side parity record: the device's modes / streams / entropies
+    against the oracle's (the cpu_baseline leg's outputs on the same frames)
+    and, when the informational pipeline ran, its container against one
+    assembled from the oracle's streams with host bzip2 (container.py:84-106,
+    blocks.py:73-81) -- the metric's "CR parity"."""
+    o_ent, o_sel, o_streams = oracle_out
+    n = o_sel.shape[0]
+    order = sorted(wl.codes)
+    mask = ~np.isnan(ent[:n])
+    if not np.array_equal(mask, ~np.isnan(o_ent)):
+        raise RuntimeError("device and oracle scored different candidate sets")
+    rel = np.abs(ent[:n][mask] - o_ent[mask]) / np.maximum(np.abs(o_ent[mask]), 1e-300)
+    p = {"frames_checked": int(n), "of_frames": int(sel.shape[0]),
+         "modes_equal": bool(np.array_equal(sel[:n], o_sel)),
+         "streams_equal": bool(np.array_equal(streams[:n], o_streams)),
+         "entropy_max_rel_vs_oracle": float(rel.max()) if rel.size else 0.0,
+         "entropy_tolerance": 1e-9,
+         "oracle": "oracle/pcbz_oracle.c (C restatement of _kernels.py:157-204, criterion.py:86-173; "
+                   "sequential fp64 sum, so entropies agree to ~1e-16 rather than bit for bit)"}
+    p["entropies_within_tolerance"] = bool(p["entropy_max_rel_vs_oracle"] <= 1e-9)
+    if pipeline_container is not None and n == sel.shape[0]:
+        import bz2
+        from concurrent.futures import ThreadPoolExecutor
+        oracle = _oracle()
+        jobs = [(f, i) for f in range(n) for i in range(-(-o_streams.shape[1] // block_size))]
+
+        def enc(j):
+            f, i = j
+            return bz2.compress(o_streams[f, i * block_size:(i + 1) * block_size].tobytes(), 9)
+
+        with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
+            blocks = list(ex.map(enc, jobs))
+        per = -(-o_streams.shape[1] // block_size)
+        frames = [(int(o_sel[f]), blocks[f * per:(f + 1) * per]) for f in range(n)]
+        want = oracle.write_container(wl.width, wl.height, wl.pitch, wl.pitch, block_size, frames)
+        p["container_equal"] = want == pipeline_container
+        p["container_bytes"] = len(pipeline_container)
+        p["compression_ratio"] = host.nbytes / len(pipeline_container)
+    p["all_equal"] = bool(p["modes_equal"] and p["streams_equal"] and p["entropies_within_tolerance"]
+                          and p.get("container_equal", True))
+    return p
+
+
+def pipeline_e2e(wl: Workload, host: np.ndarray):
     """Informational: the whole compressor on this rank's frames --
     compress_stack (device judge + emission + bzip2, container) and
-    decompress_stack -- wall-clock once after a warm-up, lossless checked."""
+    decompress_stack -- wall-clock once after a warm-up, lossless checked.
+    Returns (record, container bytes)."""
     from paper_2310_09467_b200 import (CompressOptions, Frame, FrameStack, LensletGeometry,
                                        all_intra_specs, compress_stack_detailed, decompress_stack)
     geo = LensletGeometry(wl.pitch, wl.pitch)
@@ -183,7 +318,54 @@ def pipeline_e2e(wl: Workload, host: np.ndarray) -> dict:
             "what": "compress_stack (device judge + emission + bzip2 on the GPU, container) and "
                     f"decompress_stack (bzip2 decoding on the GPU for large containers, on host threads for "
                     "small ones; inverse prediction on the GPU), wall clock, "
-                    "informational (not the metric)"}
+                    "informational (not the metric)"}, data, opts.block_size
+
+
+class Ranks:
+    """Barrier / max / sum over the ranks of this job (torch.distributed; a
+    single process when world == 1).  Works on any backend (nccl on the GPU
+    box, gloo in tests/test_bench_launch.py)."""
+
+    def __init__(self, world: int, device):
+        self.world, self.device = world, device
+
+    def barrier(self):
+        import torch
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier()
+        if self.device.type == "cuda":
+            torch.cuda.synchronize(self.device)
+
+    def _reduce(self, x: float, op) -> float:
+        if self.world == 1:
+            return x
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device=self.device)
+        dist.all_reduce(t, op=getattr(dist.ReduceOp, op))
+        return float(t.item())
+
+    def max(self, x: float) -> float:
+        return self._reduce(x, "MAX")
+
+    def sum(self, x: float) -> float:
+        return self._reduce(x, "SUM")
+
+
+def rank_frames(wl: Workload, world: int, rank: int, cores: int):
+    """This rank's frames: a series is split into contiguous shards with a
+    one-frame halo (pipeline.py:85-108: frame i needs only frames i and
+    i-1); an independent batch (C2) is replicated (weak scaling).
+    Returns (frames [n,H,W], halo frame or None, first frame index)."""
+    from paper_2310_09467_b200.shard import plan_frame_shards
+    if wl.series:
+        shard = plan_frame_shards(wl.frames, world, wl.temporal)[rank]
+        first = shard.halo if shard.halo is not None else shard.begin
+        host_all = make_frames(wl, range(first, shard.end), max(1, cores // world))
+        halo = host_all[0] if shard.halo is not None else None
+        return host_all[shard.begin - first:], halo, shard.begin
+    return make_frames(wl, range(wl.frames), max(1, cores // world)), None, 0
 
 
 def run_gpu(args, wl: Workload):
@@ -197,22 +379,13 @@ def run_gpu(args, wl: Workload):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-
     from paper_2310_09467_b200 import LensletGeometry, pipeline
     from paper_2310_09467_b200.device import DeviceJudge, collect_timing, set_profiling
-    from paper_2310_09467_b200.shard import plan_frame_shards
 
+    clk = ClockSampler(local).start()
     cores = os.cpu_count() or 1
     H, W = wl.height, wl.width
-    if wl.series:   # strong scaling: this rank's shard of the series (+ halo frame)
-        shard = plan_frame_shards(wl.frames, world, wl.temporal)[rank]
-        first = shard.halo if shard.halo is not None else shard.begin
-        host_all = make_frames(wl, range(first, shard.end), max(1, cores // world))
-        host = host_all[shard.begin - first:]
-        halo_np = host_all[0] if shard.halo is not None else None
-    else:           # weak scaling: every rank judges its own full batch
-        host = make_frames(wl, range(wl.frames), max(1, cores // world))
-        halo_np = None
+    host, halo_np, _ = rank_frames(wl, world, rank, cores)
     nloc = host.shape[0]
     pinned = torch.empty((nloc, H, W), dtype=torch.uint16).pin_memory()
     pinned.numpy()[...] = host
@@ -223,64 +396,50 @@ def run_gpu(args, wl: Workload):
     raw_bytes_local = nloc * 2 * H * W
     small = raw_bytes_local <= 126e6
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if small else None
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def sum_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+    ranks = Ranks(world, dev)
 
     # ---- device-resident timed region ----------------------------------------
     for _ in range(args.warmup):
         judge(frames, halo)
-    barrier()
+    ranks.barrier()
     set_profiling(True)
     collect_timing()
     step_ms = []
-    with ClockSampler(local) as clk:
-        barrier()
-        if small:   # inputs fit in L2: flush it between steps (outside the timed events)
-            for _ in range(args.steps):
-                flush_buf.fill_(1)
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                judge(frames, halo)
-                e1.record(stream)
-                e1.synchronize()
-                step_ms.append(e0.elapsed_time(e1))
-            ms_local = sum(step_ms) / len(step_ms)
-        else:
+    ranks.barrier()
+    t_dev0 = time.perf_counter()
+    if small:   # inputs fit in L2: flush it between steps (outside the timed events)
+        for _ in range(args.steps):
+            flush_buf.fill_(1)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            for _ in range(args.steps):
-                judge(frames, halo)
+            judge(frames, halo)
             e1.record(stream)
-            barrier()
-            ms_local = e0.elapsed_time(e1) / args.steps
-        barrier()
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+        ms_local = sum(step_ms) / len(step_ms)
+    else:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            judge(frames, halo)
+        e1.record(stream)
+        ranks.barrier()
+        ms_local = e0.elapsed_time(e1) / args.steps
+    ranks.barrier()
+    t_dev1 = time.perf_counter()
     set_profiling(False)
-    ms = max_over_ranks(ms_local)
+    ms = ranks.max(ms_local)
     hist_ms_sum, judge_ms_sum, launches = collect_timing()
-    hist_ms = max_over_ranks(hist_ms_sum / args.steps)
-    raw_bytes = sum_over_ranks(raw_bytes_local)
+    hist_ms = ranks.max(hist_ms_sum / args.steps)
+    raw_bytes = ranks.sum(raw_bytes_local)
     value = raw_bytes / (ms * 1e-3) / 1e9
+    sel_dev = judge.sel.cpu().numpy()
+    ent_dev = judge.ent.cpu().numpy()
 
     # ---- end to end through the public host API (pinned buffers) -------------
+    # at least ~1.5 s of steps so the clock sampler sees the region
     geo = LensletGeometry(wl.pitch, wl.pitch)
     vol_np = pinned.numpy()
     codes = list(wl.codes)
@@ -288,19 +447,22 @@ def run_gpu(args, wl: Workload):
     sel_h = torch.empty(nloc, dtype=torch.uint8).pin_memory().numpy()
     stream_h = torch.empty((nloc, 2 * H * W), dtype=torch.uint8).pin_memory().numpy()
     out = (ent_h, sel_h, stream_h)
+    t0 = time.perf_counter()
     pipeline.judge_volume(vol_np, geo, codes, wl.temporal, halo=halo_np, out=out)
-    e2e_steps = max(1, min(args.steps, 5))
-    with ClockSampler(local) as clk_e2e:
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            pipeline.judge_volume(vol_np, geo, codes, wl.temporal, halo=halo_np, out=out)
-        e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
+    one = time.perf_counter() - t0
+    e2e_steps = int(ranks.max(float(max(args.steps, min(200, int(1.5 / max(one, 1e-4)) + 1)))))
+    ranks.barrier()
+    t_e0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        pipeline.judge_volume(vol_np, geo, codes, wl.temporal, halo=halo_np, out=out)
+    t_e1 = time.perf_counter()
+    e2e_s = ranks.max((t_e1 - t_e0) / e2e_steps)
     e2e_value = raw_bytes / e2e_s / 1e9
-    if not np.array_equal(sel_h, judge.sel.cpu().numpy()):
-        raise RuntimeError("e2e and device-resident selections differ")
+    if not (np.array_equal(sel_h, sel_dev) and np.array_equal(ent_h, ent_dev, equal_nan=True)):
+        raise RuntimeError("e2e and device-resident judge outputs differ")
 
     if rank != 0:
+        clk.stop()
         if world > 1:
             dist.destroy_process_group()
         return 0
@@ -308,24 +470,25 @@ def run_gpu(args, wl: Workload):
     peak, peak_kind = measured_peak_hbm()
     alg_bytes_hist = raw_bytes_local * (2 if wl.temporal else 1)  # frames (+ previous frames) read once
     achieved = alg_bytes_hist / (hist_ms * 1e-3) / 1e9
-    traffic = None
     tf = profile_json("latest_hist_traffic.json")
-    if tf and tf.get("workload", "").startswith("bench.py C2") and wl.name == "c2":
-        traffic = tf.get("bytes_per_launch")
+    traffic = tf.get("bytes_per_launch") if (tf and tf.get("workload", "").startswith("bench.py C2")
+                                            and wl.name == "c2") else None
     events = sum((len(codes) if (f > 0 or halo_np is not None or not wl.temporal) else 13)
                  for f in range(nloc)) * (2 * H * W)
     ev_rate = events / (hist_ms * 1e-3)
     roof = profile_json("smem_roof.json")
-    lsu_pct = tf.get("l1tex_lsu_data_pipe_pct_of_peak") if (tf and wl.name == "c2") else None
+    lsu_pct = tf.get("l1tex_lsu_data_pipe_pct_of_peak") if (traffic is not None) else None
     res = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong" if wl.series else "weak",
         "vs_baseline": None, "dtype": "u16", "data": "synthetic (reference synth.generate, bit-identical)",
-        "config": config(wl, {"parallelism": (f"frame shards x{world} (1-frame halo, no collective)" if wl.series
-                                              else f"replicas x{world} (no collective)") if world > 1 else "single GPU"}),
+        "config": config(wl, world, "frames"),
         "roofline": {"bound": "hbm", "kernel": "judge_hist_kernel", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "traffic_source": (f"profiles/latest_hist_traffic.json: {tf.get('source', 'ncu --set full')} "
+                                        f"(a committed capture of this kernel on this workload, not this run)")
+                     if traffic is not None else None,
                      "hist_kernel_ms": hist_ms, "algorithmic_bytes_per_launch": alg_bytes_hist,
                      "stage_frac": (raw_bytes_local * (3 if wl.temporal else 2) / (ms * 1e-3) / 1e9) / peak},
         "secondary_roofline": {
@@ -335,23 +498,30 @@ def run_gpu(args, wl: Workload):
             "frac": ev_rate / roof["atoms_random_lane_ops_per_s"] if roof else None,
             "peak_source": "profiles/smem_roof.json (microbenchmark, random 32-bit words)" if roof else None,
             "smem_data_pipe_pct_of_peak_ncu": lsu_pct,
-            "smem_data_pipe_source": ("profiles/latest_hist_traffic.json (ncu --set full of this kernel in this "
-                                      "command)") if lsu_pct is not None else None},
+            "smem_data_pipe_source": "profiles/latest_hist_traffic.json (committed ncu capture, not this run)"
+            if lsu_pct is not None else None},
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": raw_bytes_local,
-                "d2h_bytes_per_step": stream_h.nbytes + ent_h.nbytes + sel_h.nbytes,
+                "d2h_bytes_per_step": stream_h.nbytes + ent_h.nbytes + sel_h.nbytes, "steps": e2e_steps,
                 "api": "paper_2310_09467_b200.pipeline.judge_volume (pcbz_judge_host)",
-                "clocks": clk_e2e.summary()},
+                "clocks": clk.summary(t_e0, t_e1)},
         "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "clocks": clk.summary(t_dev0, t_dev1),
     }
+    clk.stop()
+    container = block_size = None
     if not args.no_pipeline:
-        res["pipeline_e2e"] = pipeline_e2e(wl, host)
+        res["pipeline_e2e"], container, block_size = pipeline_e2e(wl, host)
     if not args.no_cpu_baseline:
         nf = min(nloc, int(os.environ.get("PCBZ_CPU_SAMPLE_FRAMES", "100")))
-        v, dt, nfr = cpu_reference_sample(wl, host[:nf], cores)
+        v, dt, oracle_out = cpu_reference_sample(wl, host[:nf], cores, halo_np)
         res["cpu_baseline"] = {"value": v, "unit": "GB/s", "cores": cores, "kind": "port",
-                               "sample": f"{nfr} frames of the workload, judge ({len(codes)} candidates) + "
-                                         f"emission, C port of the reference path, {dt:.2f} s wall"}
+                               "sample": f"{nf} frames of the workload, judge ({len(codes)} candidates) + "
+                                         f"emission, C port of the reference path, {dt:.2f} s wall",
+                               "cpu": _cpu_model()}
+        res["parity"] = parity_vs_oracle(wl, host, halo_np, sel_h, ent_h, stream_h, oracle_out, container,
+                                         block_size)
+        if args.numba_baseline:
+            res["reference_numba"] = numba_reference_sample(wl, host, cores)
     print(json.dumps(res), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -387,34 +557,26 @@ def run_gpu_bands(args, wl: Workload):
     judge = BandJudge((F, H, W), (wl.pitch, wl.pitch), wl.codes, wl.temporal, False, rank, world,
                       device=dev)
     stream = torch.cuda.current_stream(dev)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    ranks = Ranks(world, dev)
+    barrier, max_over_ranks = ranks.barrier, ranks.max
+    clk = ClockSampler(local).start()
 
     for _ in range(args.warmup):
         judge(frames)
     barrier()
     set_profiling(True)
     collect_timing()
-    with ClockSampler(local) as clk:
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            judge(frames)
-        e1.record(stream)
-        barrier()
-        ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    barrier()
+    t_dev0 = time.perf_counter()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        judge(frames)
+    e1.record(stream)
+    barrier()
+    t_dev1 = time.perf_counter()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     set_profiling(False)
     hist_ms_sum, _, _ = collect_timing()
     hist_ms = max_over_ranks(hist_ms_sum / args.steps)
@@ -436,16 +598,19 @@ def run_gpu_bands(args, wl: Workload):
         sel_h.copy_(judge.sel, non_blocking=True)
         torch.cuda.synchronize(dev)
 
+    t0 = time.perf_counter()
     e2e_step()
-    e2e_steps = max(1, min(args.steps, 5))
-    with ClockSampler(local) as clk_e2e:
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            e2e_step()
-        e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
+    one = time.perf_counter() - t0
+    e2e_steps = int(max_over_ranks(float(max(args.steps, min(200, int(1.5 / max(one, 1e-4)) + 1)))))
+    barrier()
+    t_e0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    t_e1 = time.perf_counter()
+    e2e_s = max_over_ranks((t_e1 - t_e0) / e2e_steps)
     if not np.array_equal(sel_h.numpy(), sel_dev):
         raise RuntimeError("e2e and device-resident selections differ")
+    clk.stop()
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -458,17 +623,16 @@ def run_gpu_bands(args, wl: Workload):
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u16", "data": "synthetic (reference synth.generate, bit-identical)",
-        "config": config(wl, {"parallelism": f"within-frame bands x{world} (NCCL all-reduce of partial "
-                                             "pair histograms + all-gather of segment summaries)"}),
+        "config": config(wl, world, "bands"),
         "roofline": {"bound": "hbm", "kernel": "judge_hist_kernel (band partial)", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                      "peak_kind": peak_kind, "hist_kernel_ms": hist_ms, "algorithmic_bytes_per_launch": alg},
         "e2e": {"value": raw_bytes / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": band_h.numel() + F,
                 "api": "paper_2310_09467_b200.device.BandJudge (pcbz_judge_band_device / merge / emit_band)",
-                "clocks": clk_e2e.summary()},
+                "clocks": clk.summary(t_e0, t_e1), "steps": e2e_steps},
         "gpu_launches": (4 if judge.stream is not None else 3) * args.steps,
-        "clocks": clk.summary(),
+        "clocks": clk.summary(t_dev0, t_dev1),
     }
     print(json.dumps(res), flush=True)
     if world > 1:
@@ -476,7 +640,25 @@ def run_gpu_bands(args, wl: Workload):
     return 0
 
 
-def main():
+def launch_plan(args, argv, n_visible: int, port: int):
+    """The command that re-runs this script as `args.gpus` ranks (one per
+    GPU) under torch.distributed.run, or an error message."""
+    if args.gpus < 1:
+        return None, f"--gpus must be >= 1 (got {args.gpus})"
+    if args.gpus > n_visible:
+        return None, f"--gpus {args.gpus} needs {args.gpus} visible GPUs, this node has {n_visible}"
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *argv], None
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -484,13 +666,33 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--numba-baseline", action="store_true",
+                    help="also time the reference's own numba path (baseline/_ref) on a sample")
     ap.add_argument("--no-pipeline", action="store_true", help="skip the informational pipeline_e2e")
     ap.add_argument("--shard", choices=["frames", "bands"], default="frames",
                     help="N>1: frame shards / replicas (default) or within-frame bands (c1, c4)")
-    args = ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse_args(argv)
     wl = WORKLOADS[args.workload]
+    if args.warmup < 3 and args.impl == "ours":
+        print(f"bench.py: --warmup {args.warmup} < 3 is not a valid measurement", file=sys.stderr)
     if args.impl == "reference":
         return run_reference(args, wl)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        import torch
+        cmd, err = launch_plan(args, argv, torch.cuda.device_count(), _free_port())
+        if err:
+            print(f"bench.py: {err}", file=sys.stderr)
+            return 2
+        return subprocess.call(cmd)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
     if args.shard == "bands":
         return run_gpu_bands(args, wl)
     return run_gpu(args, wl)

@@ -8,6 +8,7 @@ RuntimeError for device failures).
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -139,7 +140,7 @@ def ensure_entropy_terms(total: int) -> bool:
     (criterion.py:94-95) evaluated on this host.  Returns False (device log2,
     <= 1 ulp per term) when the table would be too large."""
     total = int(total)
-    if total < 1 or total > TERMS_MAX_TOTAL:
+    if total < 1 or total > int(os.environ.get("PCBZ_TERMS_MAX_TOTAL", TERMS_MAX_TOTAL)):
         return False
     lib = load()
     if lib.pcbz_entropy_terms_registered(total):

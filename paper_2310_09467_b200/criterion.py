@@ -124,6 +124,56 @@ def validated_specs(candidates, have_prev: bool) -> list:
     return specs
 
 
+#: selection guard (SURVEY.md §8(c) parity protocol item 3): when the device
+#: reduced its own log2 terms (no host term table for this total), a frame
+#: whose best and runner-up entropies differ by less than this relative gap
+#: is re-scored on the host with the reference's numpy formula.
+NEAR_TIE_REL = 1e-12
+#: frames re-scored by the guard in this process (tests read it)
+rescored = 0
+
+
+def host_entropy2d(counts: np.ndarray, total: int) -> float:
+    """The reference's entropy2d (criterion.py:86-96) in numpy, for the
+    near-tie guard."""
+    if total <= 0:
+        return 0.0
+    c = counts[counts > 0]
+    p = c / float(total)
+    return float(-(p * np.log2(p)).sum())
+
+
+def near_tie_rows(ent: np.ndarray) -> np.ndarray:
+    """Indices of rows of `ent` ([F, k], NaN = not scored) whose two smallest
+    entropies differ by less than NEAR_TIE_REL relative."""
+    e = np.where(np.isnan(ent), np.inf, ent)
+    if e.shape[1] < 2:
+        return np.zeros(0, np.int64)
+    two = np.partition(e, 1, axis=1)[:, :2]
+    gap = two[:, 1] - two[:, 0]
+    return np.nonzero(np.isfinite(two[:, 1]) & (gap <= NEAR_TIE_REL * np.abs(two[:, 1])))[0]
+
+
+def rescore_on_host(img: np.ndarray, prev: np.ndarray | None, codes: np.ndarray, px: int, py: int):
+    """Device histograms of `codes` on one frame, entropies by the host's
+    numpy entropy2d, argmin (entropy, byte): (ent [k], selected byte)."""
+    global rescored
+    h, w = img.shape
+    k = codes.size
+    ent = np.zeros(k, np.float64)
+    sel = np.zeros(1, np.uint8)
+    hist = np.zeros((k, 65536), np.int64)
+    use_prev = prev is not None and bool((codes & 0x80).any())
+    _lib.check(_lib.load().pcbz_select_predictor(
+        _lib.ptr(img), _lib.ptr(prev) if use_prev else None, h, w, px, py, _lib.ptr(codes), k,
+        _lib.ptr(ent), _lib.ptr(sel), _lib.ptr(hist)))
+    total = 2 * h * w - 1
+    ent = np.array([host_entropy2d(hh, total) for hh in hist])
+    best = min(range(k), key=lambda i: (ent[i], int(codes[i])))
+    rescored += 1
+    return ent, int(codes[best])
+
+
 def select_predictor(frame: Frame, prev: Frame | None = None, candidates=None,
                      workers: int = 1, return_histograms: bool = False):
     """Score every candidate on the device and pick argmin (entropy, byte)
@@ -143,10 +193,13 @@ def select_predictor(frame: Frame, prev: Frame | None = None, candidates=None,
     img = frame.samples
     h, w = img.shape
     use_prev = prev is not None and any(s.temporal for s in specs)
-    _lib.ensure_entropy_terms(2 * h * w - 1)
+    exact = _lib.ensure_entropy_terms(2 * h * w - 1)
     _lib.check(_lib.load().pcbz_select_predictor(
         _lib.ptr(img), _lib.ptr(prev.samples) if use_prev else None, h, w, geo.pitch_x,
         geo.pitch_y, _lib.ptr(codes), k, _lib.ptr(ent), _lib.ptr(sel), _lib.ptr(hist)))
+    if not exact and near_tie_rows(ent[None]).size:
+        ent, sel[0] = rescore_on_host(img, prev.samples if use_prev else None, codes,
+                                      geo.pitch_x, geo.pitch_y)
     report = EntropyReport(entries=tuple((s, float(e)) for s, e in zip(specs, ent)),
                            selected=PredictorSpec.from_byte(int(sel[0])))
     return (report, hist) if return_histograms else report

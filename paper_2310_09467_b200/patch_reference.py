@@ -11,7 +11,13 @@ level="kernels": replace the compiled kernels the reference looks up at call
 level="api" (default): additionally replace select_predictor in every module
     that bound it by name -- pcbz.criterion, pcbz.pipeline (pipeline.py:22),
     pcbz.cli (cli.py:22) and the package namespace -- with one batched device
-    call per frame (entropies via the device's fixed-order fp64 reduction).
+    call per frame.  The device reduces this host's numpy p*log2(p) terms
+    (registered once per frame size, _lib.ensure_entropy_terms) in numpy's
+    pairwise order, so the entropies have the reference entropy2d's exact
+    bits; for frame sizes without a term table (> 2^26 pixels) the device's
+    own log2 is used and near ties are re-scored on the host
+    (criterion.NEAR_TIE_REL).  tests/test_reference_suite.py runs the
+    reference's own test suite under both levels.
 """
 from __future__ import annotations
 
@@ -19,7 +25,7 @@ import sys
 
 import numpy as np
 
-from . import _kernels, _lib
+from . import _kernels, _lib, criterion
 
 
 def _device_select(pcbz):
@@ -46,10 +52,12 @@ def _device_select(pcbz):
         ent = np.zeros(codes.size, np.float64)
         sel = np.zeros(1, np.uint8)
         geo = frame.geometry
-        _lib.ensure_entropy_terms(2 * img.size - 1)
+        exact = _lib.ensure_entropy_terms(2 * img.size - 1)
         _lib.check(_lib.load().pcbz_select_predictor(
             _lib.ptr(img), _lib.ptr(pv), img.shape[0], img.shape[1], geo.pitch_x, geo.pitch_y,
             _lib.ptr(codes), codes.size, _lib.ptr(ent), _lib.ptr(sel), None))
+        if not exact and criterion.near_tie_rows(ent[None]).size:
+            ent, sel[0] = criterion.rescore_on_host(img, pv, codes, geo.pitch_x, geo.pitch_y)
         entries = tuple(zip(specs, (float(e) for e in ent)))
         return crit.EntropyReport(entries=entries, selected=Spec.from_byte(int(sel[0])))
 

@@ -18,7 +18,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _lib
+from . import _lib, criterion
 from .codec import (DEFAULT_BLOCK_SIZE, BlockDecodeError, BlockPlan, CompressedBlocks,
                     CorruptContainerError, bz2_block, read_container, split_blocks, write_container)
 from .core import Frame, FrameStack, LensletGeometry, PredictorSpec, unpack_symbols
@@ -89,11 +89,29 @@ def judge_volume(vol: np.ndarray, geo: LensletGeometry, codes: list, temporal: b
         ent = np.empty((F, spec.size), np.float64)
         sel = np.empty(F, np.uint8)
         stream = np.empty((F, 2 * H * W), np.uint8) if want_stream else None
-    _lib.ensure_entropy_terms(2 * H * W - 1)
+    exact = _lib.ensure_entropy_terms(2 * H * W - 1)
     _lib.check(_lib.load().pcbz_judge_host(
         _lib.ptr(vol), _lib.ptr(halo), F, H, W, geo.pitch_x, geo.pitch_y, _lib.ptr(spec), spec.size,
         1 if temporal else 0, _lib.ptr(ent), _lib.ptr(sel), _lib.ptr(stream)))
+    if not exact:
+        _guard_near_ties(vol, halo, geo, spec, temporal, ent, sel, stream)
     return ent, sel, stream
+
+
+def _guard_near_ties(vol, halo, geo, spec, temporal, ent, sel, stream):
+    """Near-tie selection guard (criterion.NEAR_TIE_REL) for totals without a
+    host term table: re-score those frames with host numpy entropies and
+    re-emit a frame whose selection changes."""
+    for f in criterion.near_tie_rows(ent):
+        prev = (vol[f - 1] if f > 0 else halo) if temporal else None
+        scored = ~np.isnan(ent[f])
+        e, best = criterion.rescore_on_host(vol[f], prev, spec[scored], geo.pitch_x, geo.pitch_y)
+        ent[f, scored] = e
+        if best != sel[f]:
+            sel[f] = best
+            if stream is not None:
+                stream[f] = emit_volume(vol[f:f + 1], geo, sel[f:f + 1],
+                                        prev if (best & 0x80) else None)[0]
 
 
 def encode_volume(vol, geo: LensletGeometry, codes, temporal: bool,
@@ -118,8 +136,13 @@ def encode_volume(vol, geo: LensletGeometry, codes, temporal: bool,
         if any(f.shape != (H, W) for f in frames):
             raise ValueError("all frames must have the same shape")
     lib = _lib.load()
-    if forced_sel is None:
-        _lib.ensure_entropy_terms(2 * H * W - 1)
+    if forced_sel is None and codes is not None and not _lib.ensure_entropy_terms(2 * H * W - 1):
+        # no host term table for this total: judge with the near-tie guard
+        # first, then code the selected modes
+        v = vol if frames is None else np.stack(frames)
+        ent0, sel0, _ = judge_volume(v, geo, list(codes), temporal, halo=halo, want_stream=False)
+        _, _, payloads = encode_volume(v, geo, None, temporal, halo, sel0, block_size, views)
+        return ent0, sel0, payloads
     nb = -(-2 * H * W // block_size)
     cap = lib.pcbz_compress_bound(F, H, W, block_size)
     # views: payloads land in this thread's page-locked buffer (valid until

@@ -482,3 +482,33 @@ def test_device_and_host_coders_identical(forced, round_frames, monkeypatch):
     want, _ = oracle.compress_stack(vol, 15, 15, forced=None if forced is None else forced.to_byte(),
                                     block_size=30000)
     assert sha(dev) == sha(want)
+
+
+def test_near_tie_guard_without_term_table(monkeypatch):
+    """Frame sizes with no host term table (PCBZ_TERMS_MAX_TOTAL below the
+    total) use the device's own log2; a best / runner-up gap below
+    NEAR_TIE_REL is re-scored with host numpy entropies (SURVEY §8(c) item
+    3).  Pitch (1, 1) makes ids 1 and 5 (and 2/6, ...) exact ties."""
+    monkeypatch.setenv("PCBZ_TERMS_MAX_TOTAL", "0")
+    rng = np.random.default_rng(11)
+    vol = rng.integers(0, 4096, (3, 37, 53), dtype=np.uint16)   # a total no other test registers
+    geo = LensletGeometry(1, 1)
+    codes = [1, 5, 0x81, 0x85]
+    before = criterion.rescored
+    rep = criterion.select_predictor(Frame(vol[1], geo), Frame(vol[0], geo),
+                                     candidates=[PredictorSpec.from_byte(c) for c in codes])
+    assert criterion.rescored > before
+    entries, best, hists = oracle.select_predictor(vol[1], vol[0], codes, 1, 1)
+    assert [e for _, e in rep.entries] == [e for _, e in entries]
+    assert rep.selected.to_byte() == best
+    before = criterion.rescored
+    ent, sel, streams = pipeline.judge_volume(vol, geo, codes, temporal=True)
+    assert criterion.rescored > before
+    prev = None
+    for f in range(3):
+        cands = codes if prev is not None else [1, 5]
+        entries, best, _ = oracle.select_predictor(vol[f], prev, cands, 1, 1)
+        assert sel[f] == best
+        assert [ent[f, codes.index(c)] for c, _ in entries] == [e for _, e in entries]
+        assert streams[f].tobytes() == oracle.emit_stream(vol[f], prev, best, 1, 1)
+        prev = vol[f]
