@@ -155,11 +155,17 @@ class BandJudge:
 
     def __call__(self, frames, halo=None, group=None, stream=None):
         """partial -> all-reduce / all-gather over `group` -> merge -> emit."""
+        import contextlib
+
         from .shard import band_collective
 
-        return band_collective(lambda: self.partial(frames, halo, stream), self.summaries,
-                               lambda: self.merge(stream), lambda: self.emit(frames, halo, stream),
-                               self.nbands, group)
+        # the collectives order against torch's current stream: run the whole
+        # partial -> collective -> merge -> emit sequence on `stream` as current
+        ctx = self.torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+        with ctx:
+            return band_collective(lambda: self.partial(frames, halo, stream), self.summaries,
+                                   lambda: self.merge(stream), lambda: self.emit(frames, halo, stream),
+                                   self.nbands, group)
 
 
 def set_profiling(on: bool) -> None:

@@ -439,9 +439,14 @@ def decompress_stack(data, workers: int = 1) -> FrameStack:
             raise CorruptContainerError(f"frame {i}: {exc}") from exc
     sel = np.array([r.spec.to_byte() for r in records], np.uint8)
     out = np.empty_like(res)
-    _lib.check(_lib.load().pcbz_reconstruct_host(_lib.ptr(res), None, res.shape[0], H, W,
-                                                 header.pitch_x, header.pitch_y, _lib.ptr(sel),
-                                                 _lib.ptr(out)))
+    # inverse prediction in rounds of <= DECOMPRESS_ROUND_BYTES of frames (a
+    # round's first frame reads the previous round's last reconstructed one)
+    per = max(1, DECOMPRESS_ROUND_BYTES // (2 * H * W))
+    for a in range(0, res.shape[0], per):
+        b = min(res.shape[0], a + per)
+        _lib.check(_lib.load().pcbz_reconstruct_host(
+            _lib.ptr(res[a:b]), _lib.ptr(out[a - 1]) if a > 0 else None, b - a, H, W,
+            header.pitch_x, header.pitch_y, _lib.ptr(np.ascontiguousarray(sel[a:b])), _lib.ptr(out[a:b])))
     geo = LensletGeometry(header.pitch_x, header.pitch_y)
     return FrameStack(tuple(Frame(f, geo) for f in out))
 
@@ -496,11 +501,45 @@ def _decompress_device(header, records, payloads):
                                       header.pitch_y, header.block_size, _lib.ptr(sel), _lib.ptr(halo),
                                       None, staged.ctypes.data, status.ctypes.data)
         if rc == _lib.PCBZ_NEEDS_HOST:
-            return None
+            # blocks the device leaves to libbzip2 (e.g. exactly periodic
+            # ones): decode only those here and call again with them
+            host = _host_decode_blocks(flat, status, nb, 2 * H * W, header.block_size)
+            if host is None:    # a real decode error: the host path reports it
+                return None
+            hs = (ctypes.c_void_p * n)(*[None if d is None else _lib._address(d) for d in host])
+            rc = lib.pcbz_decompress_host(ptrs, lens.ctypes.data, b - a, nb, H, W, header.pitch_x,
+                                          header.pitch_y, header.block_size, _lib.ptr(sel), _lib.ptr(halo),
+                                          hs, staged.ctypes.data, status.ctypes.data)
+            if rc == _lib.PCBZ_NEEDS_HOST:
+                return None
         _lib.check(rc)
         _lib.copy_into(out[a:b], staged)
     geo = LensletGeometry(header.pitch_x, header.pitch_y)
     return FrameStack(tuple(Frame(f, geo) for f in out))
+
+
+def _host_decode_blocks(flat, status, nb: int, stream_bytes: int, block_size: int):
+    """libbzip2 on host threads for the payloads with status 1: a list with
+    the decoded bytes at those positions (None elsewhere), or None when one
+    of them does not decode to its block's length."""
+    need = [int(i) for i in np.nonzero(status)[0]]
+
+    def one(i):
+        try:
+            d = bz2.decompress(bytes(flat[i]))
+        except (OSError, EOFError, ValueError):
+            return None
+        want = min(block_size, stream_bytes - (i % nb) * block_size)
+        return d if len(d) == want else None
+
+    with ThreadPoolExecutor(min(len(need), 16) or 1) as pool:
+        got = list(pool.map(one, need))
+    if any(d is None for d in got):
+        return None
+    host = [None] * len(flat)
+    for i, d in zip(need, got):
+        host[i] = d
+    return host
 
 
 @dataclass

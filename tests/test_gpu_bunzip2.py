@@ -219,3 +219,26 @@ def test_unusual_streams_left_to_libbzip2():
     assert list(st[:3]) == [1, 1, 1]
     assert st[3] == 0 and got[3] == b""
     assert st[4] == 0 and got[4] == a
+
+
+def test_periodic_block_decoded_alone_on_host(monkeypatch):
+    """A container with one exactly periodic block (a constant frame; the
+    device decoder leaves it to libbzip2) still decodes on the device: only
+    that payload goes through bz2.decompress, then the call is repeated
+    with it supplied (pcbz_decompress_host host_streams)."""
+    from paper_2310_09467_b200 import (CompressOptions, Frame, FrameStack, LensletGeometry, PredictorSpec,
+                                       compress_stack, decompress_stack, pipeline)
+    geo = LensletGeometry(15, 15)
+    vol = generate_array(SynthParams(256, 192, 15, 15, mode="beads", signal_amplitude=3000.0,
+                                     noise_sigma=20.0, photon_scale=0.05, frames=4, seed=3))
+    vol[2] = 77                                    # constant frame: residual id 0 is periodic
+    stack = FrameStack(tuple(Frame(f, geo) for f in vol))
+    data = compress_stack(stack, CompressOptions(forced=PredictorSpec(False, 0), block_size=32768))
+    calls = []
+    real = bz2.decompress
+    monkeypatch.setattr(pipeline.bz2, "decompress", lambda b: calls.append(len(b)) or real(b))
+    monkeypatch.setattr(pipeline, "_prefer_device_decode", lambda *a: True)
+    back = decompress_stack(data, workers=4)
+    assert np.array_equal(back.to_array(), vol)
+    nb = -(-2 * 256 * 192 // 32768)
+    assert len(calls) == nb, calls                # frame 2's periodic blocks only, not the container's 4 * nb
