@@ -170,28 +170,40 @@ def device_count() -> int:
 
 # ---- host memory helpers (whole-compressor path) ------------------------------
 
+class _PinnedBlock:
+    """One pcbz_host_alloc block, freed when the last array viewing it goes."""
+
+    def __init__(self, size: int):
+        self.addr = load().pcbz_host_alloc(size)
+        self.size = size
+
+    def __del__(self):
+        if self.addr:
+            load().pcbz_host_free(self.addr)
+            self.addr = None
+
+
 class _PinnedCache(threading.local):
     """Grow-only page-locked buffer per thread (pcbz_host_alloc): device->host
-    payload copies land in it at PCIe speed.  Valid until the same thread
-    asks for a larger one."""
+    payload copies land in it at PCIe speed.  The contents are valid until
+    the same thread asks for a buffer again; the memory itself stays alive
+    as long as an array handed out views it (each array keeps its block)."""
 
     def __init__(self):
-        self.addr, self.size = None, 0
+        self.block = None
 
     def get(self, nbytes: int) -> np.ndarray:
         if nbytes > PINNED_MAX:   # do not pin very large buffers: pageable, not cached
             return np.empty(max(int(nbytes), 1), np.uint8)
-        if nbytes > self.size:
-            lib = load()
-            if self.addr:
-                lib.pcbz_host_free(self.addr)
-                self.addr, self.size = None, 0
-            size = max(int(nbytes), 1 << 20)
-            addr = lib.pcbz_host_alloc(size)
-            if not addr:          # page-locked memory exhausted: pageable for this call
+        if self.block is None or nbytes > self.block.size:
+            self.block = None     # the old block lives on in the arrays still viewing it
+            blk = _PinnedBlock(max(int(nbytes), 1 << 20))
+            if not blk.addr:      # page-locked memory exhausted: pageable for this call
                 return np.empty(max(int(nbytes), 1), np.uint8)
-            self.addr, self.size = addr, size
-        return np.ctypeslib.as_array((ctypes.c_uint8 * self.size).from_address(self.addr))[:nbytes]
+            self.block = blk
+        buf = (ctypes.c_uint8 * self.block.size).from_address(self.block.addr)
+        buf._pcbz_owner = self.block   # ndarray.base -> buf -> block
+        return np.ctypeslib.as_array(buf)[:nbytes]
 
 
 #: largest page-locked buffer the cache keeps per thread (bigger requests get pageable memory)
