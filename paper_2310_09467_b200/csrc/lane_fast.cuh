@@ -44,6 +44,60 @@ __device__ __forceinline__ ChunkRows ld_chunk_rows(const uint16_t *s, const uint
   return c;
 }
 
+// Row pointers of the chunk a lane loads next (PCBZ_INCPTR): advanced by
+// one chunk per iteration instead of re-deriving y * W + x0 and the
+// out-of-frame selects per chunk; rows above the frame point at the zero
+// chunk with a zero step.  Re-derived only at a row change.
+struct RowPtrs {
+  const uint16_t *x, *t1, *ts, *px, *pt1, *pts;
+  int d1, ds;  // element step of the T1 / TS rows: 8, or 0 on the zero chunk
+};
+
+template <bool TEMP, bool NT1, bool NTS>
+__device__ __forceinline__ RowPtrs row_ptrs(const uint16_t *s, const uint16_t *p, int W, int py, int y,
+                                            int x0) {
+  const uint16_t *z = reinterpret_cast<const uint16_t *>(&g_zero_chunk);
+  const int64_t off = (int64_t)y * W + x0;
+  RowPtrs r;
+  r.d1 = y >= 1 ? 8 : 0;
+  r.ds = y >= py ? 8 : 0;
+  r.x = s + off;
+  r.t1 = NT1 && y >= 1 ? s + off - W : z;
+  r.ts = NTS && y >= py ? s + off - (int64_t)py * W : z;
+  if constexpr (TEMP) {
+    r.px = p + off;
+    r.pt1 = NT1 && y >= 1 ? p + off - W : z;
+    r.pts = NTS && y >= py ? p + off - (int64_t)py * W : z;
+  }
+  return r;
+}
+
+template <bool TEMP, bool NT1, bool NTS>
+__device__ __forceinline__ void advance(RowPtrs &r) {
+  r.x += 8;
+  if constexpr (NT1) r.t1 += r.d1;
+  if constexpr (NTS) r.ts += r.ds;
+  if constexpr (TEMP) {
+    r.px += 8;
+    if constexpr (NT1) r.pt1 += r.d1;
+    if constexpr (NTS) r.pts += r.ds;
+  }
+}
+
+template <bool TEMP, bool NT1, bool NTS>
+__device__ __forceinline__ ChunkRows ld_ptrs(const RowPtrs &r) {
+  ChunkRows c;
+  c.X = ldg_v4_pinned(r.x);
+  if constexpr (NT1) c.T1 = ldg_v4_pinned(r.t1);
+  if constexpr (NTS) c.TS = ldg_v4_pinned(r.ts);
+  if constexpr (TEMP) {
+    c.pX = ldg_v4_pinned(r.px);
+    if constexpr (NT1) c.pT1 = ldg_v4_pinned(r.pt1);
+    if constexpr (NTS) c.pTS = ldg_v4_pinned(r.pts);
+  }
+  return c;
+}
+
 __device__ __forceinline__ uint4 sub16x2_4(const uint4 &a, const uint4 &b) {
   return make_uint4(sub16x2(a.x, b.x), sub16x2(a.y, b.y), sub16x2(a.z, b.z), sub16x2(a.w, b.w));
 }
@@ -238,7 +292,15 @@ __device__ PCBZ_LANE_ATTR void lane_fast(const uint16_t *__restrict__ src,
     // (profiles/r01_notes.md): rows two chunks ahead, a software pipeline
     // (residuals of c+1 beside the events of c), two chunks per iteration
     // with ping-pong pending atomics, lane_fast inlined into the kernel.
+#ifndef PCBZ_INCPTR
+#define PCBZ_INCPTR 0
+#endif
+#if PCBZ_INCPTR
+    RowPtrs rp = row_ptrs<TEMP, kT1, kTS>(src, prv, W, py, y, x0);
+    ChunkRows cur = ld_ptrs<TEMP, kT1, kTS>(rp);
+#else
     ChunkRows cur = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, y, x0);
+#endif
     Pending pd;
 #pragma unroll
     for (int e = 0; e < 16; ++e) { pd.old[e] = 0; pd.word[e] = ~0u; }
@@ -246,8 +308,16 @@ __device__ PCBZ_LANE_ATTR void lane_fast(const uint16_t *__restrict__ src,
       int y1 = y, x1 = x0 + 8;
       if (x1 == W) { x1 = 0; ++y1; }
       const bool more = c + 1 < nch;
+#if PCBZ_INCPTR
+      if (more) {
+        if (x1 == 0 && (y1 == 1 || y1 == py)) rp = row_ptrs<TEMP, kT1, kTS>(src, prv, W, py, y1, 0);
+        else advance<TEMP, kT1, kTS>(rp);   // rows are contiguous across a row change
+      }
+      const ChunkRows nxt = ld_ptrs<TEMP, kT1, kTS>(rp);
+#else
       const ChunkRows nxt = ld_chunk_rows<TEMP, kT1, kTS>(src, prv, W, py, more ? y1 : y,
                                                          more ? x1 : x0);
+#endif
       uint4 X, T1, TS;
       source_rows<TEMP, kT1, kTS>(cur, X, T1, TS);
       uint32_t r[8];

@@ -14,6 +14,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import bench  # noqa: E402
+from workloads.configs import _gen_one  # noqa: E402
 from paper_2310_09467_b200.device import DeviceJudge, collect_timing, set_profiling  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 52
@@ -22,7 +23,7 @@ pick = [params[i] for i in np.linspace(0, len(params) - 1, n).astype(int)]
 
 from concurrent.futures import ProcessPoolExecutor  # noqa: E402
 with ProcessPoolExecutor(os.cpu_count() or 1) as ex:
-    vol = np.stack(list(ex.map(bench._gen_one, pick)))
+    vol = np.stack(list(ex.map(_gen_one, pick)))
 frames = torch.from_numpy(vol).cuda()
 judge = DeviceJudge(vol.shape, (15, 15), list(range(13)), temporal=False)
 for _ in range(2):

@@ -8,11 +8,13 @@ sys.path.insert(0, str(ROOT))
 from paper_2310_09467_b200 import build_native  # noqa: E402
 
 VARIANTS = {
-    "half_lsb": ("PCBZ_HALF_MSB=0",),
-    "half_msb": ("PCBZ_HALF_MSB=1",),
-    "half_lsb_noswz": ("PCBZ_HALF_MSB=0", "PCBZ_SWIZZLE=0"),
     "base": (),
+    "incptr": ("PCBZ_INCPTR=1",),
+    "defer": ("PCBZ_DEFER=1",),
+    "incptr_defer": ("PCBZ_INCPTR=1", "PCBZ_DEFER=1"),
     "inline": ("PCBZ_LANE_INLINE=1",),
+    "incptr_inline": ("PCBZ_INCPTR=1", "PCBZ_LANE_INLINE=1"),
+    "half_lsb": ("PCBZ_HALF_MSB=0",),
 }
 
 def build_from_git(rev: str, name: str):

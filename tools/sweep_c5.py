@@ -23,6 +23,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import bench  # noqa: E402
+from workloads.configs import _gen_one  # noqa: E402
 from paper_2310_09467_b200 import _lib  # noqa: E402
 from paper_2310_09467_b200.device import DeviceJudge, collect_timing, set_profiling  # noqa: E402
 
@@ -45,7 +46,7 @@ def main():
     params = bench.c2_params()
     pick = [params[i] for i in np.linspace(0, len(params) - 1, n).astype(int)]
     with ProcessPoolExecutor(os.cpu_count() or 1) as ex:
-        vol = np.stack(list(ex.map(bench._gen_one, pick)))
+        vol = np.stack(list(ex.map(_gen_one, pick)))
     frames = torch.from_numpy(vol).cuda()
     raw = vol.nbytes
     lib = _lib.load()
