@@ -53,8 +53,8 @@ def config(wl: Workload, world: int = 1, shard: str = "frames"):
          "l2_policy": (f"inputs ({nbytes / 1e6:.0f} MB/GPU) larger than L2 (126 MB), no flush"
                        if nbytes > 126e6 else "input smaller than L2: L2 flushed (256 MB write) before every step")}
     if shard == "bands":
-        c["parallelism"] = (f"within-frame bands x{world} (NCCL all-reduce of partial pair histograms + "
-                            "all-gather of segment summaries)")
+        c["parallelism"] = (f"within-frame bands x{world} (NCCL reduce-scatter of partial pair histograms, "
+                            "all-to-all of segment summaries, owner-computes merge, all-gather of entropies)")
     elif world > 1:
         c["parallelism"] = (f"frame shards x{world} (1-frame halo, no collective)" if wl.series
                             else f"replicas x{world} (no collective)")
@@ -629,9 +629,9 @@ def run_gpu_bands(args, wl: Workload):
                      "peak_kind": peak_kind, "hist_kernel_ms": hist_ms, "algorithmic_bytes_per_launch": alg},
         "e2e": {"value": raw_bytes / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": band_h.numel() + F,
-                "api": "paper_2310_09467_b200.device.BandJudge (pcbz_judge_band_device / merge / emit_band)",
+                "api": "paper_2310_09467_b200.device.BandJudge (pcbz_judge_band_device, reduce-scatter + all-to-all, pcbz_judge_merge_slots_device, all-gather, pcbz_judge_select_device, pcbz_emit_band_device)",
                 "clocks": clk.summary(t_e0, t_e1), "steps": e2e_steps},
-        "gpu_launches": (4 if judge.stream is not None else 3) * args.steps,
+        "gpu_launches": (5 if judge.stream is not None else 4) * args.steps,  # band hist + reduce, owned merge, select, emit
         "clocks": clk.summary(t_dev0, t_dev1),
     }
     print(json.dumps(res), flush=True)

@@ -188,6 +188,22 @@ PCBZ_API int pcbz_judge_merge_device(int64_t nframes, int64_t h, int64_t w, int6
                             const uint8_t *specs, int k, int temporal, int has_halo, int nbands,
                             uint32_t *d_hist_inout, const int16_t *d_summaries, double *d_ent_out,
                             uint8_t *d_sel_out, void *stream);
+/* Owner-computes merge (the scalable form of pcbz_judge_merge_device): the
+ * ranks reduce-SCATTER the partial histograms so that rank r holds the sums
+ * of slots [slot_begin, slot_begin + slot_count) (d_hist_owned
+ * [slot_count][65536] u32), all-to-all the summaries so that it holds every
+ * band's summaries of those slots (d_summaries_owned
+ * [nbands][slot_count][S][2][256] i16), and finishes only those slots:
+ * d_ent_owned[slot_count] (NaN = not scored / past the last slot).  The
+ * entropies are then all-gathered and pcbz_judge_select_device takes the
+ * argmin over (entropy, byte) of every frame (criterion.py:171-173).
+ * Identical, bit for bit, to pcbz_judge_merge_device. */
+PCBZ_API int pcbz_judge_merge_slots_device(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py,
+                                  const uint8_t *specs, int k, int temporal, int has_halo, int nbands,
+                                  int64_t slot_begin, int64_t slot_count, uint32_t *d_hist_owned,
+                                  const int16_t *d_summaries_owned, double *d_ent_owned, void *stream);
+PCBZ_API int pcbz_judge_select_device(int64_t nframes, const uint8_t *specs, int k, int temporal, int has_halo,
+                             const double *d_ent, uint8_t *d_sel_out, void *stream);
 PCBZ_API int pcbz_emit_band_device(const uint16_t *d_frames, const uint16_t *d_halo_prev, int64_t nframes,
                           int64_t h, int64_t w, int64_t px, int64_t py, const uint8_t *d_sel,
                           int band, int nbands, uint8_t *d_stream_out, void *stream);

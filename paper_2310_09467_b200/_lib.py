@@ -61,6 +61,10 @@ SIGNATURES = {
                                         _vp]),
     "pcbz_judge_merge_device": (_c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _c_int,
                                          _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp]),
+    "pcbz_judge_merge_slots_device": (_c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _c_int,
+                                               _c_int, _c_int, _c_int, _c_i64, _c_i64, _vp, _vp, _vp,
+                                               _vp]),
+    "pcbz_judge_select_device": (_c_int, [_c_i64, _vp, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
     "pcbz_emit_band_device": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp,
                                        _c_int, _c_int, _vp, _vp]),
     "pcbz_bzip2_bound": (_c_size, [_vp, _c_int]),

@@ -193,7 +193,8 @@ struct Plan {
   JudgeParams jp{};
   int grid = 0;
   size_t ws_bytes = 0;
-  size_t off_counter = 0, off_err = 0, off_terms = 0, off_fscratch = 0, off_segsum = 0, off_ghist = 0;
+  size_t off_counter = 0, off_err = 0, off_terms = 0, off_fscratch = 0, off_segsum = 0, off_ghist = 0,
+         off_part = 0;
 };
 
 // Relative cost class of scoring one predictor byte (per-item trace,
@@ -264,6 +265,7 @@ void layout_workspace(Plan &pl, int64_t nframes, int k, bool want_hist) {
     const size_t sums = jp.nbands > 1 ? 0 : (size_t)nframes * k * jp.S * 512 * sizeof(int16_t);
     pl.off_segsum = off; off = align_up(off + sums);
     pl.off_ghist = off; off = align_up(off + (want_hist ? 0 : (size_t)nframes * k * 65536 * 4));
+    pl.off_part = off; off = align_up(off + (size_t)items * kPartWords * sizeof(uint32_t));
   }
   pl.ws_bytes = off;
 }
@@ -351,6 +353,7 @@ int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double 
   if (!jp.direct) {
     jp.segsum = reinterpret_cast<int16_t *>(ws + pl.off_segsum);
     jp.ghist = d_hist ? d_hist : reinterpret_cast<uint32_t *>(ws + pl.off_ghist);
+    jp.part = reinterpret_cast<uint32_t *>(ws + pl.off_part);
   }
   TimedCall tc{nullptr, nullptr, nullptr, 0};
   if (g_profile) {
@@ -377,10 +380,9 @@ int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double 
     ++launches;
   }
   CUDA_TRY(cudaMemsetAsync(d_ent, 0xFF, (size_t)jp.nframes * jp.cl.k * sizeof(double), st));  // NaN
-  if (!jp.direct)
-    CUDA_TRY(cudaMemsetAsync(jp.ghist, 0, (size_t)jp.nframes * jp.cl.k * 65536 * 4, st));
   CUDA_TRY(launch_judge(jp, pl.grid, st));
   ++launches;
+  if (!jp.direct) { CUDA_TRY(launch_reduce_parts(jp, st)); ++launches; }
   if (g_profile) cudaEventRecord(tc.e1, st);
   if (!jp.direct) { CUDA_TRY(launch_finalize(jp, st)); ++launches; }
   CUDA_TRY(launch_select(jp, d_sel, st));
@@ -1023,6 +1025,7 @@ int pcbz_judge_band_device(const uint16_t *d_frames, const uint16_t *d_halo_prev
   jp.err = reinterpret_cast<int *>(ws + pl.off_err);
   jp.fscratch = reinterpret_cast<uint8_t *>(ws + pl.off_fscratch);
   jp.ghist = d_hist_out;
+  jp.part = reinterpret_cast<uint32_t *>(ws + pl.off_part);
   // the kernel writes band 0's slot of the summary array: point it at this band
   jp.segsum = d_summary_out - (size_t)band * jp.nslots * jp.S * 512;
   TimedCall tc{nullptr, nullptr, nullptr, 1};
@@ -1031,9 +1034,9 @@ int pcbz_judge_band_device(const uint16_t *d_frames, const uint16_t *d_halo_prev
     cudaEventRecord(tc.e0, st);
   }
   CUDA_TRY(cudaMemsetAsync(ws, 0, pl.off_fscratch, st));
-  CUDA_TRY(cudaMemsetAsync(d_hist_out, 0, (size_t)jp.nslots * 65536 * 4, st));
   CUDA_TRY(launch_judge(jp, pl.grid, st));
-  g_launches = 1;
+  CUDA_TRY(launch_reduce_parts(jp, st));   // writes every row of d_hist_out
+  g_launches = 2;
   if (g_profile) {
     cudaEventRecord(tc.e1, st);
     cudaEventRecord(tc.e2, st);
@@ -1069,6 +1072,57 @@ int pcbz_judge_merge_device(int64_t nframes, int64_t h, int64_t w, int64_t px, i
   CUDA_TRY(launch_select(jp, d_sel_out, st));
   if (terms) CUDA_TRY(cudaFreeAsync(terms, st));
   g_launches = host_terms ? 2 : 3;
+  return PCBZ_OK;
+}
+
+int pcbz_judge_merge_slots_device(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py,
+                                  const uint8_t *specs, int k, int temporal, int has_halo, int nbands,
+                                  int64_t slot_begin, int64_t slot_count, uint32_t *d_hist_owned,
+                                  const int16_t *d_summaries_owned, double *d_ent_owned, void *stream) {
+  int rc = check_device();
+  if (rc) return rc;
+  if (slot_begin < 0 || slot_count < 0)
+    return fail(PCBZ_E_INVALID, "invalid slot range [%lld, +%lld)", (long long)slot_begin, (long long)slot_count);
+  Plan pl;
+  rc = make_plan(nframes, h, w, px, py, specs, k, has_halo != 0, temporal, true, pl, nbands, 0);
+  if (rc) return rc;
+  JudgeParams &jp = pl.jp;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  g_launches = 0;
+  if (slot_count == 0) return PCBZ_OK;
+  jp.slot0 = slot_begin;
+  jp.slot_count = slot_count;
+  jp.nslots = slot_count;           // stride of the owned summaries [nbands][slot_count][S][512]
+  jp.ghist = d_hist_owned;
+  jp.segsum = const_cast<int16_t *>(d_summaries_owned);
+  jp.ent = d_ent_owned;
+  double *terms = nullptr;
+  const bool host_terms = use_registered_terms(jp);
+  if (!host_terms) {
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&terms), kTermTable * sizeof(double), st));
+    CUDA_TRY(launch_term_table((double)(2 * jp.npix - 1), terms, st));
+    jp.terms = terms;
+    jp.nterms = kTermTable;
+  }
+  CUDA_TRY(cudaMemsetAsync(d_ent_owned, 0xFF, (size_t)slot_count * sizeof(double), st));  // NaN
+  CUDA_TRY(launch_finalize_slots(jp, st));
+  if (terms) CUDA_TRY(cudaFreeAsync(terms, st));
+  g_launches = host_terms ? 1 : 2;
+  return PCBZ_OK;
+}
+
+int pcbz_judge_select_device(int64_t nframes, const uint8_t *specs, int k, int temporal, int has_halo,
+                             const double *d_ent, uint8_t *d_sel_out, void *stream) {
+  int rc = check_device();
+  if (rc) return rc;
+  if (nframes < 1) return fail(PCBZ_E_INVALID, "at least one frame is required");
+  if ((rc = validate_specs(specs, k))) return rc;
+  JudgeParams jp{};
+  if ((rc = build_lists(specs, k, has_halo != 0, temporal, jp.cl))) return rc;
+  jp.nframes = nframes;
+  jp.ent = const_cast<double *>(d_ent);
+  CUDA_TRY(launch_select(jp, d_sel_out, static_cast<cudaStream_t>(stream)));
+  g_launches = 1;
   return PCBZ_OK;
 }
 

@@ -16,8 +16,22 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
   NpScratch &scr = *reinterpret_cast<NpScratch *>(c16 + 65536);
   int *s_first = reinterpret_cast<int *>(reinterpret_cast<char *>(&scr) + sizeof(NpScratch));
   int *s_last = s_first + 256;
-  const PairRef pr = pair_ref(P, blockIdx.x);
-  uint32_t *G = P.ghist + (size_t)pr.slot * 65536;
+  // per-pair mode: block = pair; slot mode (owner-computes band merge):
+  // block = slot - slot0 of this rank's slots, whose histograms, summaries
+  // and entropies are stored at that local index
+  PairRef pr;
+  int64_t lslot;
+  if (P.slot_count > 0) {
+    const int64_t slot = P.slot0 + blockIdx.x;
+    const int64_t pair = slot_pair(P, slot);
+    if (pair < 0) return;  // unscored (entropy stays NaN) or padding
+    pr = pair_ref(P, pair);
+    lslot = blockIdx.x;
+  } else {
+    pr = pair_ref(P, blockIdx.x);
+    lslot = pr.slot;
+  }
+  uint32_t *G = P.ghist + (size_t)lslot * 65536;
   // the pair's segment summaries in stream order, staged in the (not yet
   // used) count buffer when they fit: 16-byte loads instead of a dependent
   // chain of 2-byte loads per key
@@ -27,7 +41,7 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
     uint4 *dst = reinterpret_cast<uint4 *>(c16);
     for (int b = 0; b < P.nbands; ++b) {
       const uint4 *src = reinterpret_cast<const uint4 *>(
-          P.segsum + ((size_t)b * P.nslots + pr.slot) * P.S * 512);
+          P.segsum + ((size_t)b * P.nslots + lslot) * P.S * 512);
       for (int i = threadIdx.x; i < P.S * 64; i += kEntropyThreads) dst[b * P.S * 64 + i] = __ldcg(src + i);
     }
     __syncthreads();
@@ -35,7 +49,7 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
   auto seg_sum = [&](int g) -> const int16_t * {
     if (staged) return reinterpret_cast<const int16_t *>(c16) + (size_t)g * 512;
     const int b = g / P.S, s = g - b * P.S;
-    return P.segsum + (((size_t)b * P.nslots + pr.slot) * P.S + s) * 512;
+    return P.segsum + (((size_t)b * P.nslots + lslot) * P.S + s) * 512;
   };
   for (int v = threadIdx.x; v < 256; v += kEntropyThreads) {
     int carried = -1, first = -1;
@@ -99,7 +113,48 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
     return c < 0xFFFFu ? c : __ldcg(G + bin);
   };
   const double e = block_entropy(get, (double)(2 * P.npix - 1), scr, P.terms, true, P.nterms);
-  if (threadIdx.x == 0) P.ent[pr.slot] = e;
+  if (threadIdx.x == 0) P.ent[lslot] = e;
+}
+
+// Sum of a slot's S per-item partial histograms (packed u16 words in the
+// shared-memory layout + spilled bins) into ghist[slot] as u32 bins; zero
+// rows for unscored slots.  Block = (slot, 1024-word chunk): coalesced word
+// reads per item, bins of consecutive words land in one 128-byte segment.
+constexpr int kReduceThreads = 256;
+constexpr int kReduceWords = 1024;
+
+__global__ void __launch_bounds__(kReduceThreads) judge_reduce_kernel(const JudgeParams P) {
+  __shared__ uint32_t sp[2 * kReduceWords];  // spilled counts of this chunk's bins
+  const int64_t slot = blockIdx.x;
+  const int64_t pair = slot_pair(P, slot);
+  const int w0 = blockIdx.y * kReduceWords;
+  uint32_t *G = P.ghist + (size_t)slot * 65536;
+  for (int i = threadIdx.x; i < 2 * kReduceWords; i += kReduceThreads) sp[i] = 0;
+  __syncthreads();
+  if (pair >= 0) {
+    for (int s = 0; s < P.S; ++s) {
+      const uint32_t *ps = P.part + (size_t)(pair * P.S + s) * kPartWords + kPartSpill;
+      const int n = (int)__ldcg(ps);
+      for (int i = threadIdx.x; i < n; i += kReduceThreads) {
+        const uint32_t bin = __ldcg(ps + 4 + i);
+        const int wd = (int)word_of_bin(bin) - w0;
+        if (wd >= 0 && wd < kReduceWords) atomicAdd(&sp[2 * wd + bin_half(bin)], kSpill);
+      }
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < kReduceWords; j += kReduceThreads) {
+    const int w = w0 + j;
+    uint32_t lo = sp[2 * j], hi = sp[2 * j + 1];
+    if (pair >= 0)
+      for (int s = 0; s < P.S; ++s) {
+        const uint32_t v = __ldcg(P.part + (size_t)(pair * P.S + s) * kPartWords + w);
+        lo += v & 0xFFFFu;
+        hi += v >> 16;
+      }
+    G[bin_of_word(w, 0)] = lo;
+    G[bin_of_word(w, 1)] = hi;
+  }
 }
 
 // argmin over (entropy, byte) per frame (criterion.py:171-173): the lists
@@ -177,6 +232,17 @@ cudaError_t launch_emit_any(const EmitParams &p, cudaStream_t st) {
 
 cudaError_t launch_finalize(const JudgeParams &p, cudaStream_t st) {
   judge_finalize_kernel<<<(unsigned)p.npairs, kEntropyThreads, kFinalizeSmemBytes, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_parts(const JudgeParams &p, cudaStream_t st) {
+  judge_reduce_kernel<<<dim3((unsigned)p.nslots, kHistWords / kReduceWords), kReduceThreads, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize_slots(const JudgeParams &p, cudaStream_t st) {
+  if (p.slot_count <= 0) return cudaSuccess;
+  judge_finalize_kernel<<<(unsigned)p.slot_count, kEntropyThreads, kFinalizeSmemBytes, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -20,6 +20,11 @@ constexpr int64_t kMinItemPixels = 1 << 18;    // smaller work items lose to per
 constexpr int kEntropyThreads = 192;           // all entropy reductions use this shape
 constexpr int kMaxFastPitch = 16;              // fast path: pitch_x <= 16 (template parameter)
 constexpr int kTermTable = 65536;              // precomputed entropy terms per call (entropy.cuh)
+// per-item partial histogram of a multi-segment / band judge: the item's
+// packed u16 words as they sit in shared memory, its spill count and its
+// spilled bins (each + kSpill), written with plain stores (judge_kernel.cuh)
+constexpr int kPartSpill = kHistWords;         // word index of the spill count
+constexpr int kPartWords = kHistWords + 4 + kSpillCap;   // 16-byte multiple
 
 constexpr size_t kJudgeSmemBytes =
     (size_t)(kHistWords + kDummyWords + kLastWords * kJudgeThreads + kSpillCap) * sizeof(uint32_t);
@@ -70,7 +75,10 @@ struct JudgeParams {
   double *ent;              // [nframes][k] (NaN = not scored)
   const double *terms;      // [nterms] entropy terms of this call's total (entropy.cuh)
   int64_t nterms;           // kTermTable (device table) or total + 1 (host-registered table)
-  uint32_t *ghist;          // [nframes*k][65536] when !direct
+  uint32_t *ghist;          // [nframes*k][65536] when !direct (summed over segments)
+  uint32_t *part;           // [items][kPartWords] per-item partial histograms when !direct
+  int64_t slot0, slot_count;  // slot-range finalize (owner-computes band merge): slots
+                              // [slot0, slot0 + slot_count); slot_count 0 = per-pair mode
   int16_t *segsum;          // [nbands][nframes*k][S][2][256] when !direct
   uint8_t *fscratch;        // [gridDim.x][kJudgeThreads][256]
   int *counter;             // dynamic item counter (zeroed before launch)
@@ -90,6 +98,11 @@ struct EmitParams {
 // launchers (judge.cu)
 cudaError_t launch_judge(const JudgeParams &p, int grid, cudaStream_t st);
 cudaError_t launch_finalize(const JudgeParams &p, cudaStream_t st);
+// sum every scored slot's S item partials (+ spills) into ghist[slot], zero
+// rows for unscored slots
+cudaError_t launch_reduce_parts(const JudgeParams &p, cudaStream_t st);
+// finalize of slots [p.slot0, p.slot0 + p.slot_count) (one block per slot)
+cudaError_t launch_finalize_slots(const JudgeParams &p, cudaStream_t st);
 cudaError_t launch_select(const JudgeParams &p, uint8_t *sel, cudaStream_t st);
 cudaError_t launch_emit(const EmitParams &p, cudaStream_t st);       // per pixel, any shape
 cudaError_t launch_emit_any(const EmitParams &p, cudaStream_t st);   // chunked when possible

@@ -58,6 +58,23 @@ __device__ __forceinline__ PairRef pair_ref(const JudgeParams &P, int64_t pair) 
   return r;
 }
 
+// inverse of pair_ref: the pair index of output slot `slot` (frame * k +
+// candidate index), or -1 when that (frame, candidate) is not scored
+__device__ __forceinline__ int64_t slot_pair(const JudgeParams &P, int64_t slot) {
+  const int64_t f = slot / P.cl.k;
+  const int idx = (int)(slot - f * P.cl.k);
+  if (f >= P.nframes) return -1;
+  const int kk = f == 0 ? P.cl.kA : P.cl.kB;
+  const uint8_t *ix = f == 0 ? P.cl.idxA : P.cl.idxB;
+  const uint8_t *ord = f == 0 ? P.cl.ordA : P.cl.ordB;
+  int j = -1;
+  for (int t = 0; t < kk; ++t) j = ix[t] == idx ? t : j;
+  if (j < 0) return -1;
+  int q = 0;
+  for (int t = 0; t < kk; ++t) q = ord[t] == j ? t : q;
+  return f == 0 ? q : P.cl.kA + (f - 1) * P.cl.kB + q;
+}
+
 // ---------------------------------------------------------------------------
 // histogram word layout
 // ---------------------------------------------------------------------------
@@ -546,15 +563,15 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
       const double e = block_entropy(get, (double)(2 * P.npix - 1), scr, P.terms, false, P.nterms);
       if (tid == 0) P.ent[pr.slot] = e;
     } else {
-      // flush into the pair's global histogram and publish the summary
-      uint32_t *G = P.ghist + (size_t)pr.slot * 65536;
-      for (int w = tid; w < kHistWords; w += kJudgeThreads) {
-        const uint32_t v = hist_w[w];
-        if (v & 0xFFFFu) atomicAdd(&G[bin_of_word(w, 0)], v & 0xFFFFu);
-        if (v >> 16) atomicAdd(&G[bin_of_word(w, 1)], v >> 16);
-      }
+      // publish the item's partial histogram (coalesced plain stores of the
+      // packed words; launch_reduce_parts sums a pair's items) and summary
+      uint4 *dst = reinterpret_cast<uint4 *>(P.part + (size_t)item * kPartWords);
+      const uint4 *src4 = reinterpret_cast<const uint4 *>(hist_w);
+      for (int i = tid; i < kHistWords / 4; i += kJudgeThreads) __stcg(dst + i, src4[i]);
       const int ns = min(s_nspill, kSpillCap);
-      for (int i = tid; i < ns; i += kJudgeThreads) atomicAdd(&G[spill_w[i]], kSpill);
+      uint32_t *pspill = P.part + (size_t)item * kPartWords + kPartSpill;
+      if (tid == 0) pspill[0] = (uint32_t)ns;
+      for (int i = tid; i < ns; i += kJudgeThreads) pspill[4 + i] = spill_w[i];
       int16_t *sum = P.segsum + (((size_t)P.band * P.nslots + pr.slot) * P.S + seg) * 512;
       for (int v = tid; v < 256; v += kJudgeThreads) {
         sum[v] = (int16_t)s_first[v];

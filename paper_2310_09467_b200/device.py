@@ -63,21 +63,24 @@ class DeviceJudge:
 
 class BandJudge:
     """One rank's share of a judge whose streams are split into `nbands`
-    within-frame pixel bands (pcbz_judge_band_device / _merge_device /
-    _emit_band_device; include/pcbz_b200.h).  Frames and halo are resident on
-    every rank; each rank scores its band, the partial histograms are summed
-    and the segment summaries gathered across ranks (shard.band_collective),
-    then every rank finishes the identical entropies / modes and emits its
-    band of every stream.
+    within-frame pixel bands (pcbz_judge_band_device / _merge_slots_device /
+    _select_device / _emit_band_device; include/pcbz_b200.h).  Frames and
+    halo are resident on every rank; each rank scores its band, the partial
+    histograms are reduce-scattered and the segment summaries exchanged
+    all-to-all so that rank r finishes slots [r*q, (r+1)*q) only, the
+    entropies are all-gathered and every rank takes the same argmin and
+    emits its band of every stream (shard.band_collective).
 
-    Buffers: hist [F*k, 65536] int32 (partial, then summed in place),
-    summary [F*k*S*512] int16 (this band), summaries [nbands, F*k*S*512]
-    (gathered, band order), ent [F, k], sel [F], stream [F, 2*(end-begin)].
+    Buffers (shard.BandBuffers): hist / summary (this band's partials),
+    hist_owned / summ_owned / ent_owned (this rank's slots), ent_all; ent
+    [F, k] is a view of ent_all, sel [F], stream [F, 2*(end-begin)].
     """
 
     def __init__(self, frames_shape, pitch, codes, temporal: bool, has_halo: bool, band: int,
                  nbands: int, want_stream: bool = True, device=None):
         import torch
+
+        from .shard import BandBuffers
 
         self.torch = torch
         F, H, W = frames_shape
@@ -101,14 +104,23 @@ class BandJudge:
         _lib.check(lib.pcbz_band_range(H, W, self.nbands, self.band, ctypes.byref(b0), ctypes.byref(b1)))
         self.pix_begin, self.pix_end = b0.value, b1.value
         dev = self.device
+        self.nslots = F * self.k
         self.workspace = torch.empty(max(ws.value, 1), dtype=torch.uint8, device=dev)
-        self.hist = torch.empty((F * self.k, 65536), dtype=torch.int32, device=dev)
-        self.summary = torch.empty(sb.value // 2, dtype=torch.int16, device=dev)
-        self.summaries = torch.empty((self.nbands, sb.value // 2), dtype=torch.int16, device=dev)
-        self.ent = torch.empty((F, self.k), dtype=torch.float64, device=dev)
+        self.buf = BandBuffers.allocate(self.nslots, self.nbands, self.segments * 512, dev)
+        self.q = self.buf.owned
+        self.slot_begin = self.band * self.q
+        self.ent = self.buf.ent_all[:self.nslots].view(F, self.k)
         self.sel = torch.empty(F, dtype=torch.uint8, device=dev)
         self.stream = (torch.empty((F, 2 * (self.pix_end - self.pix_begin)), dtype=torch.uint8, device=dev)
                        if want_stream else None)
+
+    @property
+    def hist(self):
+        return self.buf.hist
+
+    @property
+    def summary(self):
+        return self.buf.summary
 
     def _st(self, stream):
         t = self.torch
@@ -127,19 +139,27 @@ class BandJudge:
         rc = _lib.load().pcbz_judge_band_device(
             frames.data_ptr(), halo.data_ptr() if halo is not None else None, self.F, self.H,
             self.W, self.px, self.py, self.codes.ctypes.data, self.k, self.temporal, self.band,
-            self.nbands, self.hist.data_ptr(), self.summary.data_ptr(), self.workspace.data_ptr(),
+            self.nbands, self.buf.hist.data_ptr(), self.buf.summary.data_ptr(), self.workspace.data_ptr(),
             self.workspace.numel(), self._st(stream))
         _lib.check(rc)
-        return self.hist, self.summary
+        return self.buf.hist, self.buf.summary
 
-    def merge(self, stream=None):
-        """Entropies and modes from the SUMMED hist and GATHERED summaries."""
-        rc = _lib.load().pcbz_judge_merge_device(
+    def merge_owned(self, stream=None):
+        """Entropies of this rank's slots from buf.hist_owned / buf.summ_owned."""
+        rc = _lib.load().pcbz_judge_merge_slots_device(
             self.F, self.H, self.W, self.px, self.py, self.codes.ctypes.data, self.k, self.temporal,
-            self.has_halo, self.nbands, self.hist.data_ptr(), self.summaries.data_ptr(),
-            self.ent.data_ptr(), self.sel.data_ptr(), self._st(stream))
+            self.has_halo, self.nbands, self.slot_begin, self.q, self.buf.hist_owned.data_ptr(),
+            self.buf.summ_owned.data_ptr(), self.buf.ent_owned.data_ptr(), self._st(stream))
         _lib.check(rc)
-        return self.ent, self.sel
+        return self.buf.ent_owned
+
+    def select(self, stream=None):
+        """Every frame's argmin from the gathered entropies."""
+        rc = _lib.load().pcbz_judge_select_device(
+            self.F, self.codes.ctypes.data, self.k, self.temporal, self.has_halo,
+            self.buf.ent_all.data_ptr(), self.sel.data_ptr(), self._st(stream))
+        _lib.check(rc)
+        return self.sel
 
     def emit(self, frames, halo=None, stream=None):
         """This band's residual bytes of every frame under self.sel."""
@@ -154,18 +174,21 @@ class BandJudge:
         return self.stream
 
     def __call__(self, frames, halo=None, group=None, stream=None):
-        """partial -> all-reduce / all-gather over `group` -> merge -> emit."""
+        """partial -> reduce-scatter / all-to-all -> owned merge -> all-gather
+        -> argmin -> emit (shard.band_collective)."""
         import contextlib
 
         from .shard import band_collective
 
         # the collectives order against torch's current stream: run the whole
-        # partial -> collective -> merge -> emit sequence on `stream` as current
+        # sequence on `stream` as current
         ctx = self.torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
         with ctx:
-            return band_collective(lambda: self.partial(frames, halo, stream), self.summaries,
-                                   lambda: self.merge(stream), lambda: self.emit(frames, halo, stream),
-                                   self.nbands, group)
+            _, sel, out = band_collective(lambda: self.partial(frames, halo, stream),
+                                          lambda: self.merge_owned(stream), lambda: self.select(stream),
+                                          lambda: self.emit(frames, halo, stream), self.buf, self.nbands,
+                                          group)
+        return self.ent, sel, out
 
 
 def set_profiling(on: bool) -> None:

@@ -89,30 +89,97 @@ def band_rows(h: int, w: int, py: int, nbands: int, band: int):
     return merged
 
 
-def band_collective(partial_fn, summaries_out, merge_fn, emit_fn, nbands: int, group=None):
-    """Within-frame band sharding: the one exchange step of a
-    band-split judge.  partial_fn() -> (hist [P, 65536] int32, summary [n]
-    int16) for this rank's band; the histograms are SUMMED in place over the
-    group and the summaries GATHERED in rank (= band) order into
-    summaries_out [nbands, n]; merge_fn() then finishes entropies and modes
-    (identical on every rank) and emit_fn() writes this rank's band of the
-    streams.  Backend-agnostic: NCCL on device tensors, gloo on CPU tensors
-    (tests/test_sharding.py drives it with the oracle's band restatement)."""
+@dataclass
+class BandBuffers:
+    """Tensors of one rank's band exchange (torch, device or CPU).  q =
+    ceil(slots / nbands) slots are owned per rank (the last rank's tail is
+    padding: zero histograms, never scored).
+
+    hist        [nbands*q, 65536] int32  this band's partial pair counts
+    summary     [nbands*q, L] int16      this band's segment summaries (L = S*512)
+    hist_owned  [q, 65536] int32         sums over bands of the owned slots
+    summ_owned  [nbands, q, L] int16     every band's summaries of the owned slots
+    ent_owned   [q] float64              entropies of the owned slots
+    ent_all     [nbands*q] float64       every slot's entropy (first slots = [F, k])
+    """
+    hist: object
+    summary: object
+    hist_owned: object
+    summ_owned: object
+    ent_owned: object
+    ent_all: object
+
+    @staticmethod
+    def allocate(nslots: int, nbands: int, summary_len: int, device=None):
+        import torch
+        q = -(-nslots // nbands)
+        hist = torch.zeros((nbands * q, 65536), dtype=torch.int32, device=device)
+        summary = torch.full((nbands * q, summary_len), -1, dtype=torch.int16, device=device)
+        if nbands == 1:   # no exchange: the owned views are the partial buffers themselves
+            ent = torch.empty(q, dtype=torch.float64, device=device)
+            return BandBuffers(hist, summary, hist, summary.view(1, q, summary_len), ent, ent)
+        return BandBuffers(hist, summary, torch.empty((q, 65536), dtype=torch.int32, device=device),
+                           torch.empty((nbands, q, summary_len), dtype=torch.int16, device=device),
+                           torch.empty(q, dtype=torch.float64, device=device),
+                           torch.empty(nbands * q, dtype=torch.float64, device=device))
+
+    @property
+    def owned(self) -> int:
+        return self.hist_owned.shape[0]
+
+
+def band_collective(partial_fn, merge_owned_fn, select_fn, emit_fn, buf: BandBuffers, nbands: int,
+                    group=None):
+    """Within-frame band sharding, owner-computes: every rank
+    scores its band of every stream (partial_fn fills buf.hist and
+    buf.summary), the partial histograms are REDUCE-SCATTERED so that rank r
+    owns the sums of slots [r*q, (r+1)*q), the segment summaries go
+    ALL-TO-ALL so that it holds every band's summaries of those slots,
+    merge_owned_fn finishes only the owned slots (seams, entropies ->
+    buf.ent_owned), the entropies are ALL-GATHERED (8 bytes per slot) and
+    select_fn takes every frame's argmin; emit_fn writes this rank's band of
+    every stream.  Each rank merges 1/nbands of the pairs and moves
+    (nbands-1)/nbands of its partial histograms once.  Backend-agnostic:
+    NCCL on device tensors, gloo on CPU tensors (tests/test_sharding.py)."""
     import torch
     import torch.distributed as dist
 
-    hist, summary = partial_fn()
+    partial_fn()
     if nbands > 1:
-        dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
-        if summary.is_cuda:  # NCCL: one gather straight into the band-ordered buffer
-            dist.all_gather_into_tensor(summaries_out.view(-1), summary, group=group)
-        else:  # gloo has no int16: move the (even-length) summaries as int32 pairs
-            dist.all_gather(list(summaries_out.view(torch.int32).unbind(0)),
-                            summary.view(torch.int32), group=group)
-    else:
-        summaries_out[0].copy_(summary)
-    ent, sel = merge_fn()
-    return ent, sel, emit_fn()
+        dist.reduce_scatter_tensor(buf.hist_owned, buf.hist, op=dist.ReduceOp.SUM, group=group)
+        # summaries as int32 pairs (gloo has no int16; L is even)
+        dist.all_to_all_single(buf.summ_owned.view(torch.int32).view(-1),
+                               buf.summary.view(torch.int32).view(-1), group=group)
+    merge_owned_fn()
+    if nbands > 1:
+        dist.all_gather_into_tensor(buf.ent_all, buf.ent_owned, group=group)
+    sel = select_fn()
+    return buf.ent_all, sel, emit_fn()
+
+
+def emulate_band_exchange(judges) -> None:
+    """Single-process stand-in for band_collective's exchange over the
+    BandJudges of ALL bands held by one process (one GPU): reduce-scatter =
+    sum of the bands' partial rows of each owner's slots, all-to-all = the
+    bands' summary rows of those slots, all-gather = concatenation of the
+    owned entropies.  Used by the one-GPU parity tests and
+    tools/band_projection.py; nothing waits on another rank."""
+    n = len(judges)
+    q = judges[0].q
+    for r, jr in enumerate(judges):
+        if n > 1:
+            rows = slice(r * q, (r + 1) * q)
+            jr.buf.hist_owned.copy_(sum(j.buf.hist[rows] for j in judges[1:]) + judges[0].buf.hist[rows])
+            for b, jb in enumerate(judges):
+                jr.buf.summ_owned[b].copy_(jb.buf.summary[rows])
+        jr.merge_owned()
+    if n > 1:
+        import torch
+        ent_all = torch.cat([j.buf.ent_owned for j in judges])
+        for j in judges:
+            j.buf.ent_all.copy_(ent_all)
+    for j in judges:
+        j.select()
 
 
 def compress_sharded(vol: np.ndarray, geo, codes, temporal: bool, block_size: int,

@@ -70,6 +70,56 @@ def band_partial(streams, npix, p0, p1, S):
     return hist.astype(np.int32), summ
 
 
+def finish_slot(hist_row, seq, npix):
+    """Seams of one slot (its summaries `seq` [segments, 2, 256] in stream
+    order) added to hist_row (int64, in place); returns the entropy."""
+    fb = np.full(256, -1)
+    lb = np.full(256, -1)
+    for v in range(256):
+        carried = first = -1
+        for f, l in zip(seq[:, 0, v], seq[:, 1, v]):
+            if f < 0:
+                continue
+            if carried >= 0:
+                hist_row[(carried << 8) | f] += 1
+            else:
+                first = f
+            carried = l
+        fb[v], lb[v] = first, carried
+    carried = -1
+    for v in range(256):
+        if fb[v] < 0:
+            continue
+        if carried >= 0:
+            hist_row[(carried << 8) | fb[v]] += 1
+        carried = lb[v]
+    return oracle.entropy2d(hist_row, 2 * npix - 1)
+
+
+def merge_slots(hist_owned, summ_owned, streams, slot0, npix):
+    """Owner-computes merge of slots [slot0, slot0 + q): hist_owned [q, 65536]
+    (summed over bands), summ_owned [nbands, q, S, 2, 256]; NaN for unscored
+    slots and padding."""
+    q = hist_owned.shape[0]
+    ent = np.full(q, np.nan)
+    for i in range(q):
+        slot = slot0 + i
+        if slot >= len(streams) or streams[slot] is None:
+            continue
+        seq = summ_owned[:, i].reshape(-1, 2, 256)
+        ent[i] = finish_slot(hist_owned[i].astype(np.int64).copy(), seq, npix)
+    return ent
+
+
+def select(ent, codes):
+    """argmin over (entropy, byte) per frame (criterion.py:171-173)."""
+    sel = np.zeros(ent.shape[0], np.uint8)
+    for f in range(ent.shape[0]):
+        scored = [i for i in range(len(codes)) if not np.isnan(ent[f, i])]
+        sel[f] = codes[min(scored, key=lambda i: (ent[f, i], codes[i]))]
+    return sel
+
+
 def merge(hist_sum, summaries, streams, codes, nframes, npix, temporal, has_halo):
     """Seams across segments and buckets, entropies (numpy's, criterion.py:86-96)
     and the argmin over (entropy, byte) (criterion.py:171-173)."""

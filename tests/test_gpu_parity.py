@@ -351,28 +351,40 @@ def _band_view(vol_t, halo_t, shape, pitch, nbands, band, seed):
     return v, h
 
 
-def _run_bands(vol_t, halo_t, shape, pitch, codes, temporal, nbands, rows_only=False):
+def _run_bands(vol_t, halo_t, shape, pitch, codes, temporal, nbands, rows_only=False, replicated=False):
     """All bands of a band-sharded judge on one GPU, one after another; the
-    rank collective (sum of histograms, band-ordered gather of summaries) is
-    done with torch ops -- no rank waits on another."""
+    rank exchange (reduce-scatter, all-to-all, all-gather) is emulated with
+    torch ops (shard.emulate_band_exchange) -- no rank waits on another.
+    replicated=True merges every slot on one rank instead
+    (pcbz_judge_merge_device on the summed histograms)."""
     import torch
+    from paper_2310_09467_b200 import _lib
     from paper_2310_09467_b200.device import BandJudge
+    from paper_2310_09467_b200.shard import emulate_band_exchange
     judges = [BandJudge(shape, pitch, codes, temporal, halo_t is not None, b, nbands)
               for b in range(nbands)]
     views = [(_band_view(vol_t, halo_t, shape, pitch, nbands, b, 100 + b) if rows_only
               else (vol_t, halo_t)) for b in range(nbands)]
-    total = None
     for j in judges:
-        h, s = j.partial(*views[j.band])
-        total = h.clone() if total is None else total + h
-        judges[0].summaries[j.band].copy_(s)
+        j.partial(*views[j.band])
     j0 = judges[0]
-    j0.hist.copy_(total)
-    ent, sel = j0.merge()
-    streams = []
-    for j in judges:
-        j.sel.copy_(sel)
-        streams.append(j.emit(*views[j.band]).clone())
+    if replicated:
+        n = j0.nslots
+        total = sum(j.hist[:n] for j in judges[1:]) + j0.hist[:n]
+        summaries = torch.stack([j.summary[:n].reshape(-1) for j in judges])
+        ent = torch.empty((j0.F, j0.k), dtype=torch.float64, device="cuda")
+        sel = torch.empty(j0.F, dtype=torch.uint8, device="cuda")
+        _lib.check(_lib.load().pcbz_judge_merge_device(
+            j0.F, j0.H, j0.W, j0.px, j0.py, j0.codes.ctypes.data, j0.k, j0.temporal, j0.has_halo,
+            nbands, total.data_ptr(), summaries.data_ptr(), ent.data_ptr(), sel.data_ptr(), None))
+        for j in judges:
+            j.sel.copy_(sel)
+    else:
+        emulate_band_exchange(judges)
+        ent, sel = j0.ent, j0.sel
+        for j in judges[1:]:
+            assert torch.equal(j.sel, sel)
+    streams = [j.emit(*views[j.band]).clone() for j in judges]
     torch.cuda.synchronize()
     return ent.cpu().numpy(), sel.cpu().numpy(), torch.cat(streams, dim=1).cpu().numpy()
 
@@ -381,10 +393,11 @@ def _run_bands(vol_t, halo_t, shape, pitch, codes, temporal, nbands, rows_only=F
     ((3, 96, 128), (15, 15), True, 2), ((3, 96, 128), (15, 15), True, 3),
     ((3, 96, 128), (15, 15), True, 8), ((2, 61, 75), (6, 5), False, 3),
     ((2, 40, 48), (17, 9), False, 5), ((1, 64, 64), (13, 13), False, 1)])
-@pytest.mark.parametrize("rows_only", [False, True])
-def test_band_sharded_judge_equals_whole_frames(shape, pitch, halo, nbands, rows_only):
-    """pcbz_judge_band_device x nbands + merge == pcbz_judge_device, bit for bit
-    (entropies, modes), and the concatenated band streams == whole streams."""
+@pytest.mark.parametrize("rows_only,replicated", [(False, False), (True, False), (False, True)])
+def test_band_sharded_judge_equals_whole_frames(shape, pitch, halo, nbands, rows_only, replicated):
+    """pcbz_judge_band_device x nbands + the owner-computes merge (or the
+    replicated merge) == pcbz_judge_device, bit for bit (entropies, modes),
+    and the concatenated band streams == whole streams."""
     import torch
     from paper_2310_09467_b200.device import DeviceJudge
     F, H, W = shape
@@ -396,7 +409,7 @@ def test_band_sharded_judge_equals_whole_frames(shape, pitch, halo, nbands, rows
     codes = list(range(13)) + [0x80 | i for i in range(13)]
     whole = DeviceJudge(shape, pitch, codes, temporal=True)
     e0, s0, st0 = (x.cpu().numpy() for x in whole(frames, halo_t))
-    ent, sel, streams = _run_bands(frames, halo_t, shape, pitch, codes, True, nbands, rows_only)
+    ent, sel, streams = _run_bands(frames, halo_t, shape, pitch, codes, True, nbands, rows_only, replicated)
     assert np.array_equal(ent, e0, equal_nan=True)
     assert np.array_equal(sel, s0)
     assert np.array_equal(streams, st0)
@@ -512,3 +525,20 @@ def test_near_tie_guard_without_term_table(monkeypatch):
         assert [ent[f, codes.index(c)] for c, _ in entries] == [e for _, e in entries]
         assert streams[f].tobytes() == oracle.emit_stream(vol[f], prev, best, 1, 1)
         prev = vol[f]
+
+
+def test_band_sharded_c4_frames_26_candidates():
+    """C4 frames (2 x 4096^2, pitch 13, 26 candidates) over 8 bands: the
+    owner-computes band judge equals the whole-frame judge bit for bit."""
+    import torch
+    from paper_2310_09467_b200.device import DeviceJudge
+    from workloads.configs import WORKLOADS, make_frames
+    wl = WORKLOADS["c4"]
+    vol = make_frames(wl, range(2), 8)
+    frames = torch.from_numpy(vol).cuda()
+    whole = DeviceJudge(vol.shape, (13, 13), wl.codes, temporal=True)
+    e0, s0, st0 = (x.cpu().numpy() for x in whole(frames))
+    ent, sel, streams = _run_bands(frames, None, vol.shape, (13, 13), list(wl.codes), True, 8)
+    assert np.array_equal(ent, e0, equal_nan=True)
+    assert np.array_equal(sel, s0)
+    assert np.array_equal(streams, st0)

@@ -1,11 +1,12 @@
 """Per-rank cost of within-frame band sharding, measured on ONE GPU.
 
 For N bands, each band's partial judge (pcbz_judge_band_device) is timed
-alone -- what rank b would run -- plus the merge (finalize + argmin, run by
-every rank) and one band's emission.  No rank waits on another (the bands run
+alone -- what rank b would run -- plus the owner-computes merge of its
+1/N of the slots (pcbz_judge_merge_slots_device), the argmin and one band's
+emission.  No rank waits on another (the bands run
 as separate, independent launches), so this is a measurement of per-rank
-compute, not an emulation of the collective; the collective's payload (sum
-of K x 256 KiB histograms per frame, gather of the segment summaries) is
+compute, not an emulation of the collective; the collective's payload (reduce-scatter of the K x 256 KiB histograms per
+frame, all-to-all of the segment summaries, all-gather of the entropies) is
 reported in bytes.
 
     python tools/band_projection.py [c4|c1] [steps]
@@ -21,6 +22,7 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 from paper_2310_09467_b200.device import BandJudge, DeviceJudge  # noqa: E402
+from paper_2310_09467_b200.shard import emulate_band_exchange  # noqa: E402
 
 
 def timed(fn, steps):
@@ -53,23 +55,22 @@ def main():
     for n in (1, 2, 4, 8):
         judges = [BandJudge((F, H, W), pitch, wl.codes, wl.temporal, False, b, n) for b in range(n)]
         part = [timed(lambda j=j: j.partial(frames), steps) for j in judges]
-        # collective stand-in (sum + band-ordered copy) so the merge sees real inputs
-        total = sum(j.hist for j in judges[1:]) + judges[0].hist if n > 1 else judges[0].hist
-        judges[0].hist.copy_(total)
-        for j in judges:
-            judges[0].summaries[j.band].copy_(j.summary)
-        t_merge = timed(lambda: judges[0].merge(), steps)
+        emulate_band_exchange(judges)          # collective stand-in: real inputs for the merge
         if not torch.equal(judges[0].sel, sel_ref):
             raise RuntimeError(f"band-merged modes differ from the whole-frame judge (N={n})")
-        for j in judges:
-            j.sel.copy_(judges[0].sel)
+        t_merge = max(timed(lambda j=j: j.merge_owned(), steps) for j in judges)
+        t_select = timed(lambda: judges[0].select(), steps)
         t_emit = max(timed(lambda j=j: j.emit(frames), steps) for j in judges)
-        per_rank = max(part) + t_merge + t_emit
+        per_rank = max(part) + t_merge + t_select + t_emit
+        q = judges[0].q
         print(json.dumps({
-            "workload": name, "bands": n, "partial_ms_per_band": part, "merge_ms": t_merge,
+            "workload": name, "bands": n, "segments_per_band": judges[0].segments,
+            "partial_ms_per_band": part, "merge_owned_ms_max_rank": t_merge, "select_ms": t_select,
             "emit_ms_max_band": t_emit, "per_rank_compute_ms": per_rank,
-            "allreduce_bytes": judges[0].hist.numel() * 4,
-            "allgather_bytes_per_rank": judges[0].summary.numel() * 2,
+            "owned_slots_per_rank": q,
+            "reduce_scatter_bytes_sent_per_rank": (n - 1) * q * 65536 * 4,
+            "all_to_all_bytes_sent_per_rank": (n - 1) * q * judges[0].segments * 512 * 2,
+            "all_gather_bytes_per_rank": q * 8,
             "GBps_raw_excluding_collective": raw / (per_rank * 1e-3) / 1e9}), flush=True)
 
 
