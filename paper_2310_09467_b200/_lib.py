@@ -178,12 +178,14 @@ class _PinnedBlock:
     """One pcbz_host_alloc block, freed when the last array viewing it goes."""
 
     def __init__(self, size: int):
-        self.addr = load().pcbz_host_alloc(size)
+        lib = load()
+        self._free = lib.pcbz_host_free   # bound now: __del__ may run at interpreter exit
+        self.addr = lib.pcbz_host_alloc(size)
         self.size = size
 
     def __del__(self):
         if self.addr:
-            load().pcbz_host_free(self.addr)
+            self._free(self.addr)
             self.addr = None
 
 

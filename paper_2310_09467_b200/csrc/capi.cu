@@ -163,13 +163,24 @@ int validate_specs(const uint8_t *specs, int k) {
 //  * otherwise the fewest power-of-two segments giving >= 8 waves (C2 1300
 //    pairs and C3: S = 1, no flush / finalize; C4 4096^2 x 195 pairs: S = 8).
 // Items stay >= kMinItemPixels, below which per-item overhead dominates.
-int choose_segments(int64_t npairs, int64_t npix, bool want_hist) {
+int choose_segments(int64_t npairs, int64_t npix, bool want_hist, bool band = false) {
   (void)want_hist;
-  static const int64_t target_waves = [] {
+  static const int64_t whole_waves = [] {
     const char *e = getenv("PCBZ_TARGET_WAVES");
     const int64_t v = e ? atoll(e) : 8;
     return v < 1 ? 1 : v;
   }();
+  // a band's items are nbands times smaller, so the per-item overhead (run
+  // starts, in-CTA stitch, partial flush) weighs more against the tail: C4
+  // partial per rank (ms) for S = 2 / 4 / 8 at 2 bands 7.21 / 6.19 / 6.55,
+  // 4 bands 3.64 / 3.24 / 3.97, 8 bands 1.84 / 1.90 / 2.26
+  // (profiles/r02_band_sweep.jsonl): >= 5 waves
+  static const int64_t band_waves = [] {
+    const char *e = getenv("PCBZ_BAND_TARGET_WAVES");
+    const int64_t v = e ? atoll(e) : 5;
+    return v < 1 ? 1 : v;
+  }();
+  const int64_t target_waves = band ? band_waves : whole_waves;
   const int64_t nsm = num_sms_cached();
   const int64_t s_min = std::max<int64_t>(1, (npix + kMaxSegPixels - 1) / kMaxSegPixels);
   const int64_t s_cap = std::max<int64_t>(s_min, std::min<int64_t>(4096, npix / kMinItemPixels));
@@ -295,7 +306,8 @@ int make_plan(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py, con
   jp.nslots = nframes * k;
   const int64_t band_pix = (jp.npix + nbands - 1) / nbands;
   jp.S = g_seg_override > 0 ? (int)std::min<int64_t>(g_seg_override, band_pix)
-                            : choose_segments(sched_pairs > 0 ? sched_pairs : jp.npairs, band_pix, want_hist);
+                            : choose_segments(sched_pairs > 0 ? sched_pairs : jp.npairs, band_pix, want_hist,
+                                              nbands > 1);
   if ((jp.npix + (int64_t)jp.S * nbands - 1) / ((int64_t)jp.S * nbands) > kMaxSegPixels)
     return fail(PCBZ_E_INVALID, "segment override %d leaves segments above %lld pixels", jp.S,
                 (long long)kMaxSegPixels);
@@ -324,7 +336,7 @@ size_t workspace_upper_bound(int64_t nframes, int64_t h, int64_t w, int k, bool 
       jp.npairs = ka + (nframes - 1) * kb;
       jp.nbands = nbands;
       jp.S = g_seg_override > 0 ? (int)std::min<int64_t>(g_seg_override, band_pix)
-                                : choose_segments(jp.npairs, band_pix, want_hist);
+                                : choose_segments(jp.npairs, band_pix, want_hist, nbands > 1);
       jp.direct = (jp.S == 1 && nbands == 1 && !want_hist) ? 1 : 0;
       layout_workspace(pl, nframes, k, want_hist);
       best = std::max(best, pl.ws_bytes);

@@ -451,8 +451,11 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
     }
     uint4 *h4 = reinterpret_cast<uint4 *>(hist_w);
     for (int i = tid; i < (kHistWords + kDummyWords) / 4; i += kJudgeThreads) h4[i] = make_uint4(0, 0, 0, 0);
-    for (int w = tid; w < kLastWords * kJudgeThreads; w += kJudgeThreads)
-      last_w[w] = kUnseenCode | (kUnseenCode << 16);
+    {
+      const uint32_t u2 = kUnseenCode | (kUnseenCode << 16);
+      uint4 *l4 = reinterpret_cast<uint4 *>(last_w);
+      for (int w = tid; w < kLastWords * kJudgeThreads / 4; w += kJudgeThreads) l4[w] = make_uint4(u2, u2, u2, u2);
+    }
     __syncthreads();
     const int64_t item = s_item;
     if (item >= nitems) break;
@@ -487,8 +490,15 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
                    sb + len * (tid + 1) / kJudgeThreads, cs);
     }
     __syncthreads();
-    for (int w = tid; w < kHistWords; w += kJudgeThreads)
-      if (hist_w[w] & 0x80008000u) claim_word(cs, (uint32_t)w);
+    for (int w4 = tid; w4 < kHistWords / 4; w4 += kJudgeThreads) {
+      const uint4 q = reinterpret_cast<const uint4 *>(hist_w)[w4];
+      if ((q.x | q.y | q.z | q.w) & 0x80008000u) {
+        if (q.x & 0x80008000u) claim_word(cs, 4u * w4);
+        if (q.y & 0x80008000u) claim_word(cs, 4u * w4 + 1);
+        if (q.z & 0x80008000u) claim_word(cs, 4u * w4 + 2);
+        if (q.w & 0x80008000u) claim_word(cs, 4u * w4 + 3);
+      }
+    }
     __syncthreads();
 
     // ---- stitch the 192 runs in stream order (segment-summary combine) -----
@@ -498,29 +508,84 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
     {
       const int warp = tid >> 5, lane = tid & 31;
       int kf0 = -1, kl0 = -1, kf1 = -1, kl1 = -1;  // keys k = lane and k = 32 + lane
-      for (int v = warp, k = 0; v < 256; v += kJudgeThreads / 32, ++k) {
-        const uint16_t *col = reinterpret_cast<const uint16_t *>(last_w) + v * kJudgeThreads;
-        // col[lane_slot(j)] = entry of lane j
-        int carry = -1, first = -1;
-        for (int b = 0; b < kJudgeThreads; b += 32) {
-          const int j = b + lane;
-          const uint32_t code = col[lane_slot(j)];
-          const bool seen = code != kUnseenCode;
-          const int e = (int)(code >> 7);  // last pred of run j (if seen)
-          const int f = Fcta[(size_t)v * kJudgeThreads + j];
-          const uint32_t m = __ballot_sync(0xffffffffu, seen);
-          const uint32_t lower = m & ((1u << lane) - 1u);
-          const int from = __shfl_sync(0xffffffffu, e, lower ? 31 - __clz(lower) : 0);
-          const int before = lower ? from : carry;
-          if (seen && before >= 0) hist_inc_now(cs, ((uint32_t)before << 8) | (uint32_t)f);
-          if (m) {
-            if (first < 0) first = __shfl_sync(0xffffffffu, f, __ffs(m) - 1);
-            carry = __shfl_sync(0xffffffffu, e, 31 - __clz(m));
+      // first preds of the runs (global scratch, L2 latency): the warp's next
+      // key's six loads are issued while the current key is stitched
+      constexpr int kSteps = kJudgeThreads / 32;
+      constexpr int kWarps = kJudgeThreads / 32;
+      // two keys per iteration (v, v + kWarps): 12 independent ballot /
+      // shuffle sets, then 12 seam atomics, one carry check
+      int fnext[2][kSteps];
+      auto load_f = [&](int v, int (&dst)[kSteps]) {
+#pragma unroll
+        for (int t = 0; t < kSteps; ++t)
+          dst[t] = v < 256 ? Fcta[(size_t)v * kJudgeThreads + t * 32 + lane] : 0;
+      };
+      load_f(warp, fnext[0]);
+      load_f(warp + kWarps, fnext[1]);
+      for (int v = warp, k = 0; v < 256; v += 2 * kWarps, k += 2) {
+        int fcur[2][kSteps];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int t = 0; t < kSteps; ++t) fcur[u][t] = fnext[u][t];
+        if (v + 2 * kWarps < 256) {
+          load_f(v + 2 * kWarps, fnext[0]);
+          load_f(v + 3 * kWarps, fnext[1]);
+        }
+        int carry[2] = {-1, -1}, first[2] = {-1, -1};
+        uint32_t seam[2][kSteps];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int vu = min(v + u * kWarps, 255);   // a missing second key reads key 255, then is dropped
+          const uint16_t *col = reinterpret_cast<const uint16_t *>(last_w) + vu * kJudgeThreads;
+#pragma unroll
+          for (int t = 0; t < kSteps; ++t) {
+            const uint32_t code = col[lane_slot(32 * t + lane)];  // entry of run 32t + lane
+            const bool seen = code != kUnseenCode && v + u * kWarps < 256;
+            const int e = (int)(code >> 7);  // last pred of the run (if seen)
+            const int f = fcur[u][t];
+            const uint32_t m = __ballot_sync(0xffffffffu, seen);
+            const uint32_t lower = m & ((1u << lane) - 1u);
+            const int from = __shfl_sync(0xffffffffu, e, lower ? 31 - __clz(lower) : 0);
+            const int ffirst = __shfl_sync(0xffffffffu, f, m ? __ffs(m) - 1 : 0);
+            const int elast = __shfl_sync(0xffffffffu, e, m ? 31 - __clz(m) : 0);
+            const int before = lower ? from : carry[u];
+            seam[u][t] = (seen && before >= 0) ? (((uint32_t)before << 8) | (uint32_t)f) : ~0u;
+            if (m) {
+              first[u] = first[u] < 0 ? ffirst : first[u];
+              carry[u] = elast;
+            }
           }
         }
-        if (lane == (k & 31)) {
-          if (k < 32) { kf0 = first; kl0 = carry; }
-          else { kf1 = first; kl1 = carry; }
+        uint32_t flag = 0;
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int t = 0; t < kSteps; ++t) {
+            // predicated, not branched: the 12 atomics issue back to back
+            const uint32_t sm = seam[u][t];
+            const uint32_t inc = sm != ~0u ? pred_inc(sm & 0xFFu) : 0u;
+            uint32_t old = 0;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0xFFFFFFFF;\n\t"
+                "@p atom.shared.add.u32 %0, [%1], %2;\n\t}"
+                : "+r"(old)
+                : "r"(cs.hbase + 4u * word_of_bin(sm & 0xFFFFu)), "r"(inc), "r"(sm));
+            flag |= old ^ (old + inc);
+          }
+        if (flag & 0x80008000u) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int t = 0; t < kSteps; ++t) claim_spill(cs, seam[u][t]);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int ku = k + u;
+          if (lane == (ku & 31)) {
+            if (ku < 32) { kf0 = first[u]; kl0 = carry[u]; }
+            else { kf1 = first[u]; kl1 = carry[u]; }
+          }
         }
       }
       __syncthreads();  // the last-pred tables are dead from here on

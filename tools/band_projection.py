@@ -52,7 +52,12 @@ def main():
     raw = F * 2 * H * W
     print(json.dumps({"workload": name, "mode": "whole frames, one GPU", "ms": t_whole,
                       "GBps_raw": raw / (t_whole * 1e-3) / 1e9}), flush=True)
-    for n in (1, 2, 4, 8):
+    import os as _os
+    seg = int(_os.environ.get("PCBZ_BAND_SEGMENTS", "0"))
+    if seg:
+        from paper_2310_09467_b200 import _lib
+        _lib.load().pcbz_set_segment_override(seg)
+    for n in [int(x) for x in _os.environ.get("PCBZ_BAND_COUNTS", "1,2,4,8").split(",")]:
         judges = [BandJudge((F, H, W), pitch, wl.codes, wl.temporal, False, b, n) for b in range(n)]
         part = [timed(lambda j=j: j.partial(frames), steps) for j in judges]
         emulate_band_exchange(judges)          # collective stand-in: real inputs for the merge
