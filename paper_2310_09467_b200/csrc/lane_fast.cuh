@@ -26,12 +26,28 @@ struct ChunkRows {
   uint4 X, T1, TS, pX, pT1, pTS;
 };
 
+#ifndef PCBZ_PREFETCH
+#define PCBZ_PREFETCH 0   // L2 prefetch distance in chunks (0 = off)
+#endif
+__device__ __forceinline__ void prefetch_l2(const uint16_t *p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 template <bool TEMP, bool NT1, bool NTS>
 __device__ __forceinline__ ChunkRows ld_chunk_rows(const uint16_t *s, const uint16_t *p, int W,
                                                    int py, int y, int x0) {
   const uint16_t *z = reinterpret_cast<const uint16_t *>(&g_zero_chunk);
   const int64_t off = (int64_t)y * W + x0;
   const int64_t o1 = off - W, os = off - (int64_t)py * W;
+  if constexpr (PCBZ_PREFETCH > 0) {
+    // the rows PCBZ_PREFETCH chunks ahead (the next lines of this lane's run);
+    // DRAM misses then overlap the chunks in between
+    const int64_t d = 8 * PCBZ_PREFETCH;
+    prefetch_l2(s + off + d);
+    if constexpr (NT1) prefetch_l2(s + (y >= 1 ? o1 : off) + d);
+    if constexpr (NTS) prefetch_l2(s + (y >= py ? os : off) + d);
+    if constexpr (TEMP) prefetch_l2(p + off + d);
+  }
   ChunkRows c;
   c.X = ldg_v4_pinned(s + off);
   if constexpr (NT1) c.T1 = ldg_v4_pinned(y >= 1 ? s + o1 : z);

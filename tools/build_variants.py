@@ -15,6 +15,10 @@ VARIANTS = {
     "inline": ("PCBZ_LANE_INLINE=1",),
     "incptr_inline": ("PCBZ_INCPTR=1", "PCBZ_LANE_INLINE=1"),
     "half_lsb": ("PCBZ_HALF_MSB=0",),
+    "pf4": ("PCBZ_PREFETCH=4",),
+    "pf8": ("PCBZ_PREFETCH=8",),
+    "pf16": ("PCBZ_PREFETCH=16",),
+    "pf32": ("PCBZ_PREFETCH=32",),
 }
 
 def build_from_git(rev: str, name: str):
