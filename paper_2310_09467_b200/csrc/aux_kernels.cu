@@ -1,5 +1,7 @@
 // aux_kernels.cu -- emission, residual image, temporal delta, the composed
 // approximate-BWT route, the entropy2d API kernel and the decompression side.
+#include <algorithm>
+#include <utility>
 #include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
@@ -206,6 +208,171 @@ __global__ void __launch_bounds__(1024) reconstruct_kernel(const uint16_t *res, 
   }
 }
 
+// Inverse intra prediction as a pipelined wavefront over 32-row bands (one
+// warp per band, lane = row): lane r handles column s - r at step s, so the
+// neighbours up (row r - sy, same column) and left (own row, column - sx)
+// were computed at an earlier step of the same warp and sit in a per-warp
+// shared-memory ring of the band's rows; rows above the band come from the
+// band above, copied into the ring's halo rows once per 32 steps after its
+// published progress covers them.  Units (frame, band) are grabbed
+// band-major, so a band only ever waits on a band grabbed before it (no
+// deadlock); a band runs ~64 steps behind the band above, so a 2048^2 frame
+// is ~6,200 dependent steps deep instead of 4,095 CTA-wide barriers.
+// Pitches px <= 64, py <= 31 (the ring holds 128 columns, the halo 32 rows).
+constexpr int kRecWarps = 4;
+constexpr int kRecRing = 128;
+constexpr int kRecRows = 64;   // 32 halo rows + the band's 32 rows
+constexpr size_t kRecSmemBytes = (size_t)kRecWarps * kRecRows * kRecRing * sizeof(uint16_t);
+
+__device__ __forceinline__ int64_t mn64(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ int64_t mx64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+__device__ __forceinline__ int ld_acquire_i32(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_i32(int *p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// One band (32 rows from row 32 * b) of one frame; GRP / F compile-time
+// (make_cfg), columns in 32-bit.
+template <int GRP, int F>
+__device__ __forceinline__ void reconstruct_band(const uint16_t *__restrict__ R, uint16_t *O, int h, int w,
+                                                 int px, int py, int b, int *pg,
+                                                 uint16_t (*rg)[kRecRing], int lane) {
+  constexpr int kMask = kRecRing - 1;
+  const int sx = GRP == 0 ? 1 : px, sy = GRP == 0 ? 1 : py;
+  const int dy_max = GRP == 2 ? max(py, 1) : sy;
+  const int y = b * 32 + lane;
+  const bool row_ok = y < h;
+  const uint16_t *Rrow = R + (int64_t)(row_ok ? y : 0) * w;
+  const uint16_t *own = rg[32 + lane];
+  const uint16_t *up = rg[32 + lane - sy];
+  const uint16_t *up1 = rg[32 + lane - 1];
+  const bool top = y >= sy, top1 = y >= 1;
+  for (int s0 = 0; s0 < w + 31; s0 += 32) {
+    if (b > 0) {
+      // rows above: the band above must have finished columns < s0 + 33
+      const int need = min(w, s0 + 33);
+      if (lane == 0)
+        while (ld_acquire_i32(pg + b - 1) < need) __nanosleep(32);
+      __syncwarp();
+      // only this block's 32 new columns: earlier ones are in the ring
+      // already (final when copied), and the ring keeps 128 columns
+      const int x = s0 + lane;
+      if (x < w) {
+        uint16_t v[31];
+#pragma unroll
+        for (int i = 0; i < 31; ++i)
+          v[i] = i < dy_max ? __ldcg(O + (int64_t)(b * 32 - dy_max + i) * w + x) : 0;
+#pragma unroll
+        for (int i = 0; i < 31; ++i)
+          if (i < dy_max) rg[32 - dy_max + i][x & kMask] = v[i];
+      }
+      __syncwarp();
+    }
+    uint32_t rr[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int x = s0 + j - lane;
+      rr[j] = (row_ok && x >= 0 && x < w) ? __ldg(Rrow + x) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int x = s0 + j - lane;
+      if (row_ok && x >= 0 && x < w) {
+        const bool left = x >= sx;
+        const int A = left ? own[(x - sx) & kMask] : 0;
+        const int B = top ? up[x & kMask] : 0;
+        const int C = (left && top) ? up[(x - sx) & kMask] : 0;
+        int pr;
+        if constexpr (F == 1) pr = A + B - C;
+        else if constexpr (F == 2) pr = A + ((B - C) >> 1);
+        else if constexpr (F == 3) pr = B + ((A - C) >> 1);
+        else pr = (A + B) >> 1;
+        if constexpr (GRP == 2) {  // phase: average with the pixel-adjacent prediction
+          const bool l1 = x >= 1;
+          const int a1 = l1 ? own[(x - 1) & kMask] : 0;
+          const int b1 = top1 ? up1[x & kMask] : 0;
+          const int c1 = (l1 && top1) ? up1[(x - 1) & kMask] : 0;
+          int p1;
+          if constexpr (F == 1) p1 = a1 + b1 - c1;
+          else if constexpr (F == 2) p1 = a1 + ((b1 - c1) >> 1);
+          else if constexpr (F == 3) p1 = b1 + ((a1 - c1) >> 1);
+          else p1 = (a1 + b1) >> 1;
+          pr = (pr + p1) >> 1;
+        }
+        rg[32 + lane][x & kMask] = (uint16_t)(rr[j] + (uint32_t)pr);
+      }
+      __syncwarp();
+    }
+    // the block's 32 new columns of every row, stored row by row with the
+    // lanes along the columns (coalesced), then published
+    for (int i = 0; i < 32; ++i) {
+      const int x = s0 - i + lane;
+      if (b * 32 + i < h && x >= 0 && x < w) O[(int64_t)(b * 32 + i) * w + x] = rg[32 + i][x & kMask];
+    }
+    __syncwarp();
+    // row 31 has finished columns < s0 + 1; rows above it are further on
+    if (lane == 31) {
+      __threadfence();
+      st_release_i32(pg + b, min(w, max(0, s0 + 1)));
+    }
+  }
+}
+
+template <int... IDs>
+__device__ __forceinline__ void reconstruct_band_dispatch(int id, const uint16_t *R, uint16_t *O, int h, int w,
+                                                          int px, int py, int b, int *pg,
+                                                          uint16_t (*rg)[kRecRing], int lane,
+                                                          std::integer_sequence<int, IDs...>) {
+  ((id == IDs ? reconstruct_band<(IDs - 1) / 4, (IDs - 1) % 4 + 1>(R, O, h, w, px, py, b, pg, rg, lane)
+              : void()), ...);
+}
+
+__global__ void __launch_bounds__(32 * kRecWarps, 3) reconstruct_bands_kernel(
+    const uint16_t *res, int h, int w, int px, int py, const uint8_t *sel, uint16_t *out,
+    int64_t nframes, int nbands, int *prog, unsigned long long *counter) {
+  extern __shared__ uint16_t rec_smem[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint16_t(*rg)[kRecRing] = reinterpret_cast<uint16_t(*)[kRecRing]>(rec_smem + (size_t)wid * kRecRows * kRecRing);
+  const int64_t npix = (int64_t)h * w;
+  const int64_t units = nframes * nbands;
+  for (;;) {
+    unsigned long long u = 0;
+    if (lane == 0) u = atomicAdd(counter, 1ull);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= (unsigned long long)units) break;
+    const int b = (int)(u / nframes);
+    const int64_t f = (int64_t)(u % nframes);
+    const int id = sel[f] & 0x7F;
+    const uint16_t *R = res + f * npix;
+    uint16_t *O = out + f * npix;
+    int *pg = prog + f * nbands;
+    if (id == 0) {  // identity: no dependencies; the band's rows, 16 bytes per lane
+      const int64_t r0 = (int64_t)b * 32 * w, r1 = min((int64_t)(b + 1) * 32 * w, npix);
+      if ((((uintptr_t)R | (uintptr_t)O) & 15) == 0 && (r0 & 7) == 0) {
+        const int64_t v1 = r0 + ((r1 - r0) & ~(int64_t)7);
+        for (int64_t i = r0 + 8 * lane; i < v1; i += 256)
+          *reinterpret_cast<uint4 *>(O + i) = __ldg(reinterpret_cast<const uint4 *>(R + i));
+        for (int64_t i = v1 + lane; i < r1; i += 32) O[i] = R[i];
+      } else {
+        for (int64_t i = r0 + lane; i < r1; i += 32) O[i] = R[i];
+      }
+    } else {
+      reconstruct_band_dispatch(id, R, O, h, w, px, py, b, pg, rg, lane,
+                                std::integer_sequence<int, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12>{});
+    }
+    __syncwarp();
+    if (lane == 31) {
+      __threadfence();
+      st_release_i32(pg + b, w);
+    }
+  }
+}
+
 // Temporal undelta chain: frame f = inverse_f (+ frame f-1 if temporal).
 // Pixels are independent, frames are walked in order by every thread.
 __global__ void undelta_chain_kernel(uint16_t *frames, const uint16_t *halo, int64_t nframes,
@@ -225,9 +392,39 @@ __global__ void undelta_chain_kernel(uint16_t *frames, const uint16_t *halo, int
 cudaError_t launch_reconstruct(const uint16_t *res, const uint16_t *halo, int64_t nframes,
                                int64_t h, int64_t w, int px, int py, const uint8_t *sel,
                                uint16_t *out, cudaStream_t st) {
-  reconstruct_kernel<<<(unsigned)nframes, 1024, 0, st>>>(res, h, w, px, py, sel, out);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  cudaError_t e;
+  const int64_t nbands = (h + 31) / 32;
+  if (px <= 64 && py <= 31 && w < (1ll << 30) && h < (1ll << 30) && nframes * nbands < (1ll << 40)) {
+    static bool configured = false;
+    if (!configured) {
+      e = cudaFuncSetAttribute(reconstruct_bands_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kRecSmemBytes);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    // progress words (one per band) + the unit counter, stream-ordered scratch
+    const size_t words = (size_t)nframes * nbands;
+    char *scratch = nullptr;
+    if ((e = cudaMallocAsync(reinterpret_cast<void **>(&scratch), words * 4 + 16, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(scratch, 0, words * 4 + 16, st)) != cudaSuccess) return e;
+    int *prog = reinterpret_cast<int *>(scratch + 16);
+    auto *counter = reinterpret_cast<unsigned long long *>(scratch);
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    // persistent grid (3 CTAs of 64 KiB per SM); units are grabbed by running
+    // warps only, so a waiting band's predecessor is always being worked on
+    const int64_t want = (words + kRecWarps - 1) / kRecWarps;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * 3));
+    reconstruct_bands_kernel<<<grid, 32 * kRecWarps, kRecSmemBytes, st>>>(res, (int)h, (int)w, px, py, sel, out,
+                                                                         nframes, (int)nbands, prog, counter);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaFreeAsync(scratch, st)) != cudaSuccess) return e;
+  } else {
+    reconstruct_kernel<<<(unsigned)nframes, 1024, 0, st>>>(res, h, w, px, py, sel, out);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   undelta_chain_kernel<<<grid_for(h * w, 256), 256, 0, st>>>(out, halo, nframes, h * w, sel);
   return cudaGetLastError();
 }

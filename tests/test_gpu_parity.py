@@ -542,3 +542,25 @@ def test_band_sharded_c4_frames_26_candidates():
     assert np.array_equal(ent, e0, equal_nan=True)
     assert np.array_equal(sel, s0)
     assert np.array_equal(streams, st0)
+
+
+@pytest.mark.parametrize("h,w,px,py", [(96, 128, 15, 15), (70, 61, 6, 5), (33, 200, 64, 31),
+                                       (1, 50, 3, 2), (65, 9, 1, 1), (40, 48, 17, 40)])
+def test_reconstruct_inverts_every_predictor(h, w, px, py):
+    """Inverse prediction (_kernels.py:69-90; the band wavefront kernel, or the
+    one-CTA sweep for py > 31) restores every frame from its residuals, per
+    frame (_kernels.reconstruct_image) and batched with temporal modes
+    (pcbz_reconstruct_host, predictors.py:101-147)."""
+    rng = np.random.default_rng(h * 1000 + w)
+    vol = rng.integers(0, 65536, (13, h, w), dtype=np.uint16)
+    for cid in range(13):
+        res = oracle.residual_image(vol[cid], cid, px, py)
+        assert np.array_equal(_kernels.reconstruct_image(res, cid, px, py), vol[cid]), cid
+    sel = np.array([c | (0x80 if c % 3 == 1 else 0) for c in range(13)], np.uint8)
+    sel[0] &= 0x7F
+    res = np.stack([oracle.residual_image(oracle.temporal_delta(vol[f], vol[f - 1]) if sel[f] & 0x80
+                                          else vol[f], sel[f] & 0x7F, px, py) for f in range(13)])
+    out = np.empty_like(vol)
+    _lib.check(_lib.load().pcbz_reconstruct_host(_lib.ptr(res), None, 13, h, w, px, py, _lib.ptr(sel),
+                                                 _lib.ptr(out)))
+    assert np.array_equal(out, vol)
