@@ -83,3 +83,13 @@ def test_rank_frames_shards_cover_series(world):
             assert np.array_equal(halo, whole[first - 1])
         seen.extend(range(first, first + fr.shape[0]))
     assert seen == list(range(SMALL.frames))
+
+
+def test_reference_arm_other_ranks_exit_without_work(monkeypatch, capsys):
+    """Under torchrun the reference arm runs on rank 0 only; other ranks
+    print nothing and exit 0."""
+    monkeypatch.setenv("RANK", "1")
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    monkeypatch.setattr(bench, "make_frames", lambda *a, **k: (_ for _ in ()).throw(AssertionError("worked")))
+    assert bench.main(["--impl", "reference", "--gpus", "2"]) == 0
+    assert capsys.readouterr().out == ""
