@@ -155,32 +155,29 @@ int validate_specs(const uint8_t *specs, int k) {
 // Work decomposition: segments per (frame, candidate) stream.  Items are
 // pulled dynamically by one CTA per SM; item costs differ by candidate (up to
 // ~1.8x, temporal phase predictors dearest; dispatched dearest first), and
-// every extra segment adds a histogram flush, a stitch and the finalize
-// pass.  Measured (profiles/r01_notes.md, tools/sweep_segments.py,
-// tools/trace_items.py):
+// every extra segment adds a partial flush, a stitch and the merge.
+// Measured (profiles/r01_notes.md, profiles/r02_band_sweep.jsonl,
+// profiles/r02_sweep_c5.jsonl):
 //  * small jobs (even the finest split is under two waves): fill one wave as
 //    exactly as possible (C1, 13 pairs of 2048^2: S = 11, 143 items);
-//  * otherwise the fewest power-of-two segments giving >= 8 waves (C2 1300
-//    pairs and C3: S = 1, no flush / finalize; C4 4096^2 x 195 pairs: S = 8).
+//  * whole frames with >= 8 waves unsplit: S = 1, direct mode (no flush or
+//    merge; C2 1300 pairs, C3 2600);
+//  * otherwise the fewest power-of-two segments giving items of <= ~2.2 M
+//    pixels and >= 4 waves: every measured optimum -- 26 C2 frames S = 2
+//    (42.3 vs 37.9 / 40.9 GB/s at S = 1 / 4), C4 S = 8 (13.0 vs 13.9 ms at 4),
+//    C4 bands: 2 -> S = 4 (6.19 vs 6.55 / 7.21 ms), 4 -> S = 4 (3.24 vs
+//    3.64 / 3.97), 8 -> S = 4 (1.90 vs 1.84 at S = 2, 2.26 at 8).
 // Items stay >= kMinItemPixels, below which per-item overhead dominates.
 int choose_segments(int64_t npairs, int64_t npix, bool want_hist, bool band = false) {
   (void)want_hist;
-  static const int64_t whole_waves = [] {
-    const char *e = getenv("PCBZ_TARGET_WAVES");
-    const int64_t v = e ? atoll(e) : 8;
+  auto env = [](const char *name, int64_t dflt) {
+    const char *e = getenv(name);
+    const int64_t v = e ? atoll(e) : dflt;
     return v < 1 ? 1 : v;
-  }();
-  // a band's items are nbands times smaller, so the per-item overhead (run
-  // starts, in-CTA stitch, partial flush) weighs more against the tail: C4
-  // partial per rank (ms) for S = 2 / 4 / 8 at 2 bands 7.21 / 6.19 / 6.55,
-  // 4 bands 3.64 / 3.24 / 3.97, 8 bands 1.84 / 1.90 / 2.26
-  // (profiles/r02_band_sweep.jsonl): >= 5 waves
-  static const int64_t band_waves = [] {
-    const char *e = getenv("PCBZ_BAND_TARGET_WAVES");
-    const int64_t v = e ? atoll(e) : 5;
-    return v < 1 ? 1 : v;
-  }();
-  const int64_t target_waves = band ? band_waves : whole_waves;
+  };
+  static const int64_t direct_waves = env("PCBZ_TARGET_WAVES", 8);
+  static const int64_t min_waves = env("PCBZ_MIN_WAVES", 4);
+  static const int64_t item_pixels = env("PCBZ_ITEM_PIXELS", 2200000);
   const int64_t nsm = num_sms_cached();
   const int64_t s_min = std::max<int64_t>(1, (npix + kMaxSegPixels - 1) / kMaxSegPixels);
   const int64_t s_cap = std::max<int64_t>(s_min, std::min<int64_t>(4096, npix / kMinItemPixels));
@@ -196,7 +193,8 @@ int choose_segments(int64_t npairs, int64_t npix, bool want_hist, bool band = fa
   }
   int64_t s = 1;
   while (s < s_min) s <<= 1;
-  while (npairs * s < target_waves * nsm && 2 * s <= s_cap) s <<= 1;
+  if (!band && s == 1 && npairs >= direct_waves * nsm) return 1;
+  while ((npix / s > item_pixels || npairs * s < min_waves * nsm) && 2 * s <= s_cap) s <<= 1;
   return (int)std::max<int64_t>(s_min, std::min<int64_t>(s, s_cap));
 }
 
