@@ -11,11 +11,21 @@ static __device__ const uint4 g_zero_chunk = {0u, 0u, 0u, 0u};
 // 128-bit read-only load whose position in the instruction stream is pinned
 // (volatile asm is not sunk toward its use, so the next chunk's rows really
 // are in flight while the current chunk is processed).
+#ifndef PCBZ_LDG_HINT
+#define PCBZ_LDG_HINT 0   // 1: L2::evict_last on the row loads (A/B of the DRAM re-reads)
+#endif
 __device__ __forceinline__ uint4 ldg_v4_pinned(const uint16_t *p) {
   uint4 r;
+#if PCBZ_LDG_HINT == 1
+  asm volatile("{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+               "ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], pol;\n\t}"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+#else
   asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
+#endif
   return r;
 }
 

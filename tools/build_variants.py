@@ -19,6 +19,7 @@ VARIANTS = {
     "pf8": ("PCBZ_PREFETCH=8",),
     "pf16": ("PCBZ_PREFETCH=16",),
     "pf32": ("PCBZ_PREFETCH=32",),
+    "evict_last": ("PCBZ_LDG_HINT=1",),
 }
 
 def build_from_git(rev: str, name: str):
