@@ -32,7 +32,13 @@ void PCBZ_CAT(judge_launch_px, PCBZ_PX)(const JudgeParams &p, int grid, cudaStre
 }
 
 void PCBZ_CAT(emit_launch_px, PCBZ_PX)(const EmitParams &p, int grid, cudaStream_t st) {
-  if constexpr (PCBZ_PX > 0) emit_chunks_kernel<PCBZ_PX><<<grid, 256, 0, st>>>(p);
+#ifndef PCBZ_EMIT_RUNS
+#define PCBZ_EMIT_RUNS 1
+#endif
+  if constexpr (PCBZ_PX > 0) {
+    if (PCBZ_EMIT_RUNS) emit_runs_kernel<PCBZ_PX><<<grid, 256, 0, st>>>(p);
+    else emit_chunks_kernel<PCBZ_PX><<<grid, 256, 0, st>>>(p);
+  }
 }
 #endif
 

@@ -20,6 +20,7 @@ VARIANTS = {
     "pf16": ("PCBZ_PREFETCH=16",),
     "pf32": ("PCBZ_PREFETCH=32",),
     "evict_last": ("PCBZ_LDG_HINT=1",),
+    "emit_chunks": ("PCBZ_EMIT_RUNS=0",),
 }
 
 def build_from_git(rev: str, name: str):
