@@ -564,3 +564,26 @@ def test_reconstruct_inverts_every_predictor(h, w, px, py):
     _lib.check(_lib.load().pcbz_reconstruct_host(_lib.ptr(res), None, 13, h, w, px, py, _lib.ptr(sel),
                                                  _lib.ptr(out)))
     assert np.array_equal(out, vol)
+
+
+def test_candidate_entropy():
+    """criterion.candidate_entropy (criterion.py:99-106): the identity
+    candidate's entropy of a symbol image, bit-identical to numpy entropy2d
+    of the oracle's fused histogram (and of the composed bwt -> pairs route,
+    test_criterion.py:170-177), incl. the reference's KAT: a constant-7 2x2
+    image packs to 00 07 x 4 (test_criterion.py:152-161)."""
+    rng = np.random.default_rng(7)
+    for h, w in [(1, 1), (2, 2), (3, 2), (16, 16), (40, 30), (61, 75), (256, 200)]:
+        img = rng.integers(0, 65536, (h, w), dtype=np.uint16)
+        got = criterion.candidate_entropy(img)
+        want = oracle.entropy2d(oracle.residual_bwt_pair_hist(img, 0, 1, 1), 2 * h * w - 1)
+        assert got == want, (h, w, got.hex(), want.hex())
+        s = oracle.pack_symbols(img)
+        assert got == oracle.entropy2d(oracle.bwt_pair_hist(np.frombuffer(s, np.uint8)), 2 * h * w - 1)
+        assert got == criterion.candidate_entropy(Frame(img, LensletGeometry(1, 1)))
+    const = np.full((2, 2), 7, np.uint16)
+    assert oracle.pack_symbols(const) == bytes([0, 7] * 4)
+    assert criterion.candidate_entropy(const) == oracle.entropy2d(
+        oracle.bwt_pair_hist(np.frombuffer(oracle.pack_symbols(const), np.uint8)), 7)
+    with pytest.raises(TypeError):
+        criterion.candidate_entropy(np.zeros((2, 2), np.int32))
