@@ -8,6 +8,10 @@ level="kernels": replace the compiled kernels the reference looks up at call
     decompress_stack inverse prediction (predictors.py:101-106) to the GPU.
     Entropies are then still reduced by the reference's numpy entropy2d, so
     its exact-float tests hold unchanged.
+level="pipeline": additionally code every bzip2 block of the reference's
+    compress_blocks (blocks.py:73-81, bound by name in pcbz.pipeline) with
+    the GPU coder (csrc/bzip2.cu, byte-exact with libbzip2 1.0.8), so the
+    reference's own compress_stack runs judge, emission and bzip2 on the B200.
 level="api" (default): additionally replace select_predictor in every module
     that bound it by name -- pcbz.criterion, pcbz.pipeline (pipeline.py:22),
     pcbz.cli (cli.py:22) and the package namespace -- with one batched device
@@ -66,21 +70,54 @@ def _device_select(pcbz):
     return select_predictor
 
 
+#: streams shorter than this are bzip2-coded by the host libbzip2 under
+#: level="pipeline" (the device coder's fixed cost exceeds a small block's)
+DEVICE_BZ2_MIN_BYTES = 1 << 20
+
+
+def _device_compress_blocks(pcbz):
+    """blocks.compress_blocks (blocks.py:73-81) with every block coded by the
+    GPU bzip2 coder (codec.bz2_blocks_device: byte-exact with bz2.compress at
+    level 9); returns the reference's own CompressedBlocks."""
+    blocks = pcbz.blocks
+    reference = blocks.compress_blocks
+
+    def compress_blocks(stream, block_size=blocks.DEFAULT_BLOCK_SIZE, workers=1):
+        if len(stream) < DEVICE_BZ2_MIN_BYTES:
+            return reference(stream, block_size, workers)
+        from .codec import bz2_blocks_device
+        plan = blocks.BlockPlan.for_length(len(stream), block_size)
+        view = memoryview(stream)
+        chunks = [view[i * block_size:(i + 1) * block_size] for i in range(plan.block_count)]
+        return blocks.CompressedBlocks(plan, tuple(bz2_blocks_device(chunks)))
+
+    compress_blocks.__doc__ = reference.__doc__
+    compress_blocks.__wrapped_reference__ = reference
+    return compress_blocks
+
+
 def install(pcbz=None, level: str = "api"):
-    """Patch `pcbz` (imported if not given) in place and return it."""
+    """Patch `pcbz` (imported if not given) in place and return it.
+    level "kernels" < "api" < "pipeline" (each includes the previous)."""
     if pcbz is None:
         import pcbz  # noqa: F811  (the reference package must be importable)
-    if level not in ("api", "kernels"):
-        raise ValueError("level must be 'api' or 'kernels'")
+    if level not in ("api", "kernels", "pipeline"):
+        raise ValueError("level must be 'api', 'kernels' or 'pipeline'")
     _lib.load()
     k = pcbz._kernels
     for name in ("residual_bwt_pair_hist", "residual_image", "reconstruct_image", "counting_bwt",
                  "pair_hist", "bwt_pair_hist"):
         setattr(k, name, getattr(_kernels, name))
-    if level == "api":
+    if level in ("api", "pipeline"):
         fn = _device_select(pcbz)
         for modname in ("pcbz.criterion", "pcbz.pipeline", "pcbz.cli", "pcbz"):
             mod = sys.modules.get(modname)
             if mod is not None and hasattr(mod, "select_predictor"):
                 mod.select_predictor = fn
+    if level == "pipeline":
+        cb = _device_compress_blocks(pcbz)
+        for modname in ("pcbz.blocks", "pcbz.pipeline", "pcbz"):   # pipeline.py:19 binds it by name
+            mod = sys.modules.get(modname)
+            if mod is not None and hasattr(mod, "compress_blocks"):
+                mod.compress_blocks = cb
     return pcbz

@@ -65,3 +65,21 @@ def test_patched_select_validates_like_reference(pcbz_ref):
         pcbz_ref.select_predictor(f, candidates=[pcbz_ref.PredictorSpec(True, 1)])
     with pytest.raises(ValueError):
         pcbz_ref.select_predictor(f, candidates=[pcbz_ref.PredictorSpec(False, 2)] * 2)
+
+
+def test_install_pipeline_level_rebinds_compress_blocks(pcbz_ref):
+    """level="pipeline" also routes blocks.compress_blocks (bound by name in
+    pcbz.pipeline, pipeline.py:19) to the GPU coder; streams under 1 MiB stay
+    on the reference's libbzip2 path (so this runs without a GPU)."""
+    import bz2
+    import paper_2310_09467_b200 as b200
+    orig = pcbz_ref.blocks.compress_blocks
+    b200.install(pcbz_ref, level="pipeline")
+    cb = pcbz_ref.blocks.compress_blocks
+    assert cb is not orig and cb.__wrapped_reference__ is orig
+    assert pcbz_ref.pipeline.compress_blocks is cb and pcbz_ref.compress_blocks is cb
+    assert pcbz_ref.pipeline.select_predictor.__wrapped_reference__ is not None
+    data = bytes(range(256)) * 100
+    out = cb(data, 10000, 2)
+    assert isinstance(out, pcbz_ref.blocks.CompressedBlocks)
+    assert out.payloads == tuple(bz2.compress(data[i:i + 10000], 9) for i in range(0, len(data), 10000))
