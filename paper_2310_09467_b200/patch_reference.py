@@ -8,10 +8,6 @@ level="kernels": replace the compiled kernels the reference looks up at call
     decompress_stack inverse prediction (predictors.py:101-106) to the GPU.
     Entropies are then still reduced by the reference's numpy entropy2d, so
     its exact-float tests hold unchanged.
-level="pipeline": additionally code every bzip2 block of the reference's
-    compress_blocks (blocks.py:73-81, bound by name in pcbz.pipeline) with
-    the GPU coder (csrc/bzip2.cu, byte-exact with libbzip2 1.0.8), so the
-    reference's own compress_stack runs judge, emission and bzip2 on the B200.
 level="api" (default): additionally replace select_predictor in every module
     that bound it by name -- pcbz.criterion, pcbz.pipeline (pipeline.py:22),
     pcbz.cli (cli.py:22) and the package namespace -- with one batched device
@@ -22,6 +18,10 @@ level="api" (default): additionally replace select_predictor in every module
     own log2 is used and near ties are re-scored on the host
     (criterion.NEAR_TIE_REL).  tests/test_reference_suite.py runs the
     reference's own test suite under both levels.
+level="pipeline": additionally code every bzip2 block of the reference's
+    compress_blocks (blocks.py:73-81, bound by name in pcbz.pipeline) with
+    the GPU coder (csrc/bzip2.cu, byte-exact with libbzip2 1.0.8), so the
+    reference's own compress_stack runs judge, emission and bzip2 on the B200.
 """
 from __future__ import annotations
 
