@@ -631,7 +631,8 @@ def run_gpu_bands(args, wl: Workload):
                 "d2h_bytes_per_step": band_h.numel() + F,
                 "api": "paper_2310_09467_b200.device.BandJudge (pcbz_judge_band_device, reduce-scatter + all-to-all, pcbz_judge_merge_slots_device, all-gather, pcbz_judge_select_device, pcbz_emit_band_device)",
                 "clocks": clk.summary(t_e0, t_e1), "steps": e2e_steps},
-        "gpu_launches": (5 if judge.stream is not None else 4) * args.steps,  # band hist + reduce, owned merge, select, emit
+        # band: (delta frames if temporal) + hist + reduce, owned merge, select, emit
+        "gpu_launches": ((5 if judge.stream is not None else 4) + (1 if wl.temporal else 0)) * args.steps,
         "clocks": clk.summary(t_dev0, t_dev1),
     }
     print(json.dumps(res), flush=True)

@@ -46,6 +46,22 @@ __global__ void temporal_delta_kernel(const uint16_t *cur, const uint16_t *prev,
     out[t] = (uint16_t)(cur[t] - prev[t]);
 }
 
+// (F - P) mod 2^16 of pixels [pix0, pix1) of frames f0.. (8-aligned), 8 pixels
+// per thread (predictors.py:116-120)
+__global__ void delta_frames_kernel(const uint16_t *frames, const uint16_t *halo, int64_t nframes,
+                                    int64_t npix, int64_t f0, int64_t pix0, int64_t pix1, uint16_t *delta) {
+  const int64_t per = (pix1 - pix0) / 8;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (nframes - f0) * per;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = f0 + t / per, i = pix0 + (t % per) * 8;
+    const uint16_t *cur = frames + f * npix, *prv = f > 0 ? frames + (f - 1) * npix : halo;
+    const uint4 a = __ldg(reinterpret_cast<const uint4 *>(cur + i));
+    const uint4 b = __ldg(reinterpret_cast<const uint4 *>(prv + i));
+    *reinterpret_cast<uint4 *>(delta + f * npix + i) =
+        make_uint4(sub16x2(a.x, b.x), sub16x2(a.y, b.y), sub16x2(a.z, b.z), sub16x2(a.w, b.w));
+  }
+}
+
 // overlapping byte pairs, first byte high (_kernels.py:116-122)
 __global__ void pair_hist_kernel(const uint8_t *s, int64_t n, uint32_t *hist) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t + 1 < n;
@@ -128,6 +144,15 @@ cudaError_t launch_residual_image(const uint16_t *img, const uint16_t *prev, int
 cudaError_t launch_temporal_delta(const uint16_t *cur, const uint16_t *prev, int64_t n,
                                   uint16_t *out, cudaStream_t st) {
   temporal_delta_kernel<<<grid_for(n, 256), 256, 0, st>>>(cur, prev, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_delta_frames(const uint16_t *frames, const uint16_t *halo, int64_t nframes,
+                                int64_t npix, int64_t f0, int64_t pix0, int64_t pix1, uint16_t *delta,
+                                cudaStream_t st) {
+  if (nframes <= f0 || pix1 <= pix0) return cudaSuccess;
+  delta_frames_kernel<<<grid_for((nframes - f0) * ((pix1 - pix0) / 8), 256), 256, 0, st>>>(
+      frames, halo, nframes, npix, f0, pix0, pix1, delta);
   return cudaGetLastError();
 }
 

@@ -342,6 +342,38 @@ size_t workspace_upper_bound(int64_t nframes, int64_t h, int64_t w, int k, bool 
   return best;
 }
 
+// PCBZ_DELTA=0 keeps the in-register (F - P) of both frames' rows
+bool use_delta(const JudgeParams &jp, const uint16_t *d_frames, const uint16_t *d_halo, bool band = false) {
+  static const bool on = [] {
+    const char *e = getenv("PCBZ_DELTA");
+    return !(e && atoi(e) == 0);
+  }();
+  if (!on || (jp.nbands != 1 && !band) || jp.npix % 8 != 0) return false;
+  if ((reinterpret_cast<uintptr_t>(d_frames) | reinterpret_cast<uintptr_t>(d_halo)) & 15) return false;
+  for (int i = 0; i < jp.cl.kB; ++i)
+    if (jp.cl.byteB[i] & 0x80) return true;
+  for (int i = 0; i < jp.cl.kA; ++i)
+    if (jp.cl.byteA[i] & 0x80) return true;
+  return false;
+}
+
+// Stream-ordered scratch from the device's default pool, kept cached
+// between calls (release threshold raised once per device).
+cudaError_t pooled_alloc(void **p, size_t bytes, cudaStream_t st) {
+  static bool configured[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 64 && !configured[dev]) {
+    cudaMemPool_t pool;
+    if ((e = cudaDeviceGetDefaultMemPool(&pool, dev)) != cudaSuccess) return e;
+    uint64_t keep = UINT64_MAX;
+    if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess) return e;
+    configured[dev] = true;
+  }
+  return cudaMallocAsync(p, bytes, st);
+}
+
 // Enqueue the whole judge (+ optional emission) on `st`.
 int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double *d_ent,
              uint8_t *d_sel, uint8_t *d_stream, uint32_t *d_hist, void *d_ws, cudaStream_t st,
@@ -390,8 +422,20 @@ int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double 
     ++launches;
   }
   CUDA_TRY(cudaMemsetAsync(d_ent, 0xFF, (size_t)jp.nframes * jp.cl.k * sizeof(double), st));  // NaN
+  // temporal candidates read a materialised delta frame (one pass per frame)
+  // instead of both frames' rows per (frame, candidate) item
+  uint16_t *d_delta = nullptr;
+  jp.delta = nullptr;
+  const int64_t delta_f0 = d_halo ? 0 : 1;
+  if (use_delta(jp, d_frames, d_halo) && jp.nframes > delta_f0) {
+    CUDA_TRY(pooled_alloc(reinterpret_cast<void **>(&d_delta), (size_t)jp.nframes * jp.npix * 2, st));
+    CUDA_TRY(launch_delta_frames(d_frames, d_halo, jp.nframes, jp.npix, delta_f0, 0, jp.npix, d_delta, st));
+    jp.delta = d_delta;
+    ++launches;
+  }
   CUDA_TRY(launch_judge(jp, pl.grid, st));
   ++launches;
+  if (d_delta) CUDA_TRY(cudaFreeAsync(d_delta, st));
   if (!jp.direct) { CUDA_TRY(launch_reduce_parts(jp, st)); ++launches; }
   if (g_profile) cudaEventRecord(tc.e1, st);
   if (!jp.direct) { CUDA_TRY(launch_finalize(jp, st)); ++launches; }
@@ -1044,9 +1088,34 @@ int pcbz_judge_band_device(const uint16_t *d_frames, const uint16_t *d_halo_prev
     cudaEventRecord(tc.e0, st);
   }
   CUDA_TRY(cudaMemsetAsync(ws, 0, pl.off_fscratch, st));
+  // temporal candidates on materialised delta frames (whole frames: rows
+  // outside this band's neighbourhood may hold anything and are never read)
+  uint16_t *d_delta = nullptr;
+  jp.delta = nullptr;
+  const int64_t delta_f0 = d_halo_prev ? 0 : 1;
+  int launches = 2;
+  if (use_delta(jp, d_frames, d_halo_prev, true) && jp.nframes > delta_f0) {
+    CUDA_TRY(pooled_alloc(reinterpret_cast<void **>(&d_delta), (size_t)jp.nframes * jp.npix * 2, st));
+    // only the rows this band reads: its own, py + 1 above, and for band 0
+    // the last py + 1 rows (the wrapped predecessor of stream byte 0)
+    int64_t b0 = 0, b1 = 0;
+    if ((rc = pcbz_band_range(h, w, nbands, band, &b0, &b1))) return rc;
+    const int64_t above = (py + 1) * w;
+    const int64_t r0 = std::max<int64_t>(0, (b0 / w) * w - above) & ~7ll;
+    const int64_t r1 = std::min<int64_t>(jp.npix, ((b1 + w - 1) / w * w + 7) & ~7ll);
+    CUDA_TRY(launch_delta_frames(d_frames, d_halo_prev, jp.nframes, jp.npix, delta_f0, r0, r1, d_delta, st));
+    if (band == 0) {
+      const int64_t t0 = std::max<int64_t>(r1, jp.npix - above);
+      CUDA_TRY(launch_delta_frames(d_frames, d_halo_prev, jp.nframes, jp.npix, delta_f0, t0 & ~7ll, jp.npix,
+                                   d_delta, st));
+    }
+    jp.delta = d_delta;
+    ++launches;
+  }
   CUDA_TRY(launch_judge(jp, pl.grid, st));
+  if (d_delta) CUDA_TRY(cudaFreeAsync(d_delta, st));
   CUDA_TRY(launch_reduce_parts(jp, st));   // writes every row of d_hist_out
-  g_launches = 2;
+  g_launches = launches;
   if (g_profile) {
     cudaEventRecord(tc.e1, st);
     cudaEventRecord(tc.e2, st);

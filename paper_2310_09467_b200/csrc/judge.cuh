@@ -62,6 +62,8 @@ struct CandLists {
 struct JudgeParams {
   const uint16_t *frames;   // [nframes][npix]
   const uint16_t *halo;     // previous original frame of frames[0] or nullptr
+  const uint16_t *delta;    // [nframes][npix] (F - P) mod 2^16 for temporal pairs, or nullptr
+                            // (then formed in registers from both frames' rows)
   int64_t nframes, npix;
   int H, W, px, py;
   CandLists cl;
@@ -111,6 +113,11 @@ cudaError_t launch_residual_image(const uint16_t *img, const uint16_t *prev, int
                                   cudaStream_t st);
 cudaError_t launch_temporal_delta(const uint16_t *cur, const uint16_t *prev, int64_t n,
                                   uint16_t *out, cudaStream_t st);
+// delta[f][p] = frames[f][p] - prev(f)[p] mod 2^16 for f in [f0, nframes),
+// p in [pix0, pix1) (8-aligned; prev(0) = halo)
+cudaError_t launch_delta_frames(const uint16_t *frames, const uint16_t *halo, int64_t nframes,
+                                int64_t npix, int64_t f0, int64_t pix0, int64_t pix1, uint16_t *delta,
+                                cudaStream_t st);
 cudaError_t launch_pair_hist(const uint8_t *s, int64_t n, uint32_t *hist, cudaStream_t st);
 cudaError_t launch_counting_bwt(const uint8_t *s, int64_t n, uint8_t *out, uint32_t *scratch,
                                 size_t scratch_words, cudaStream_t st);

@@ -555,6 +555,10 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
     const PairRef pr = pair_ref(P, pair);
     const uint16_t *src = P.frames + pr.frame * P.npix;
     const uint16_t *prv = (pr.spec & 0x80) ? prev_of(P.frames, P.halo, P.npix, pr.frame) : nullptr;
+    if (prv && P.delta) {  // temporal candidate on the materialised delta frame
+      src = P.delta + pr.frame * P.npix;
+      prv = nullptr;
+    }
     const PredCfg cfg = make_cfg(pr.spec & 0x7F, P.px, P.py);
 
     if constexpr (PX > 0) {
@@ -563,7 +567,7 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
       const int64_t cb = nchunk * gseg / gtot, ce = nchunk * (gseg + 1) / gtot;
       const int64_t ca = cb + (ce - cb) * w_lo / w_total;
       const int64_t cz = cb + (ce - cb) * w_hi / w_total;
-      if (pr.spec & 0x80)
+      if (prv)
         lane_fast_dispatch<PX, true>(pr.spec & 0x7F, src, prv, P.W, P.py, P.npix, ca * 8, cz - ca,
                                      cfg, cs, std::make_integer_sequence<int, 13>{});
       else
