@@ -357,8 +357,9 @@ bool use_delta(const JudgeParams &jp, const uint16_t *d_frames, const uint16_t *
   return false;
 }
 
-// Stream-ordered scratch from the device's default pool, kept cached
-// between calls (release threshold raised once per device).
+// Stream-ordered scratch from the device's default pool; up to 2 GiB of it
+// stays cached between calls (release threshold raised once per device),
+// larger reservations go back to the driver at the next synchronisation.
 cudaError_t pooled_alloc(void **p, size_t bytes, cudaStream_t st) {
   static bool configured[64] = {};
   int dev = 0;
@@ -367,7 +368,7 @@ cudaError_t pooled_alloc(void **p, size_t bytes, cudaStream_t st) {
   if (dev < 64 && !configured[dev]) {
     cudaMemPool_t pool;
     if ((e = cudaDeviceGetDefaultMemPool(&pool, dev)) != cudaSuccess) return e;
-    uint64_t keep = UINT64_MAX;
+    uint64_t keep = 2ull << 30;
     if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess) return e;
     configured[dev] = true;
   }
