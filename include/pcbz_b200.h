@@ -291,10 +291,10 @@ PCBZ_API int pcbz_set_segment_override(int segments);
  * profiling was off). */
 PCBZ_API int pcbz_set_profiling(int on);
 /* Tuning hook: while on, judge calls on this thread record per work item
- * (item = pair * S + segment) the pair (smid << 48 | start ns) and end ns of
- * the CTA that ran it; pcbz_item_trace synchronises the device, copies up to
- * max_items records of the last call into out[2 * max_items], stores S and
- * returns the number of records. */
+ * (item = pair * S + segment) (smid << 48 | start ns), the ns at which every
+ * lane run was done and the end ns, of the CTA that ran it; pcbz_item_trace
+ * synchronises the device, copies up to max_items records of the last call
+ * into out[3 * max_items], stores S and returns the number of records. */
 PCBZ_API int pcbz_set_item_trace(int on);
 PCBZ_API int64_t pcbz_item_trace(uint64_t *out, int64_t max_items, int *segments);
 PCBZ_API int pcbz_last_timing(float *hist_ms, float *total_ms, int *launches);

@@ -84,7 +84,7 @@ struct JudgeParams {
   int16_t *segsum;          // [nbands][nframes*k][S][2][256] when !direct
   uint8_t *fscratch;        // [gridDim.x][kJudgeThreads][256]
   int *counter;             // dynamic item counter (zeroed before launch)
-  uint64_t *trace;          // optional [items][2]: (smid << 48 | start ns, end ns)
+  uint64_t *trace;          // optional [items][3]: (smid << 48 | start ns, runs-done ns, end ns)
   int *err;                 // sticky error flag
 };
 

@@ -580,6 +580,7 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
                    sb + len * (tid + 1) / kJudgeThreads, cs);
     }
     __syncthreads();
+    if (P.trace && tid == 0) P.trace[3 * item + 1] = globaltimer_ns();  // every run done
     for (int w4 = tid; w4 < kHistWords / 4; w4 += kJudgeThreads) {
       const uint4 q = reinterpret_cast<const uint4 *>(hist_w)[w4];
       if ((q.x | q.y | q.z | q.w) & 0x80008000u) {
@@ -735,8 +736,8 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
     }
     __syncthreads();
     if (P.trace && tid == 0) {
-      P.trace[2 * item] = ((uint64_t)smid() << 48) | (t_start & 0xFFFFFFFFFFFFull);
-      P.trace[2 * item + 1] = globaltimer_ns();
+      P.trace[3 * item] = ((uint64_t)smid() << 48) | (t_start & 0xFFFFFFFFFFFFull);
+      P.trace[3 * item + 2] = globaltimer_ns();
     }
   }
 }

@@ -38,15 +38,16 @@ def main():
     lib.pcbz_set_item_trace(1)
     judge(frames)
     torch.cuda.synchronize()
-    buf = np.zeros(2 * 1 << 20, np.uint64)
+    buf = np.zeros(3 * (1 << 20), np.uint64)
     seg = ctypes.c_int()
     n = lib.pcbz_item_trace(buf.ctypes.data, 1 << 20, ctypes.byref(seg))
     lib.pcbz_set_item_trace(0)
     lib.pcbz_set_segment_override(0)
-    rec = buf[:2 * n].reshape(n, 2)
+    rec = buf[:3 * n].reshape(n, 3)
     sm = (rec[:, 0] >> 48).astype(int)
     t0 = (rec[:, 0] & ((1 << 48) - 1)).astype(np.int64)
-    t1 = rec[:, 1].astype(np.int64)
+    t_runs = rec[:, 1].astype(np.int64)
+    t1 = rec[:, 2].astype(np.int64)
     base = (int(t1[0]) >> 48) << 48   # start stamps were truncated to 48 bits
     t0 = t0 + base
     t0 = np.where(t0 > t1, t0 - (1 << 48), t0)
@@ -77,6 +78,8 @@ def main():
         "makespan_us": float((t1.max() - start) / 1e3),
         "first_sm_idle_us": float(ends[0] / 1e3), "median_sm_end_us": float(np.median(ends) / 1e3),
         "item_us_mean": float(dur.mean()), "item_us_p10": float(np.percentile(dur, 10)),
+        "runs_us_mean": float(((t_runs - t0) / 1e3).mean()),
+        "after_runs_us_mean": float(((t1 - t_runs) / 1e3).mean()),
         "item_us_p90": float(np.percentile(dur, 90)),
         "by_candidate_us": {f"0x{c:02X}": round(float(np.mean(v)), 1) for c, v in sorted(by_cand.items())},
     }))
