@@ -407,11 +407,11 @@ int run_plan(Plan &pl, const uint16_t *d_frames, const uint16_t *d_halo, double 
   jp.trace = nullptr;
   if (g_trace_on) {
     const int64_t items = jp.npairs * jp.S;
-    if ((size_t)items * 3 > g_trace_cap) {
+    if ((size_t)items * kTraceWords > g_trace_cap) {
       if (g_trace_dev) cudaFree(g_trace_dev);
       g_trace_cap = 0;
-      CUDA_TRY(cudaMalloc(&g_trace_dev, (size_t)items * 24));
-      g_trace_cap = (size_t)items * 3;
+      CUDA_TRY(cudaMalloc(&g_trace_dev, (size_t)items * 8 * kTraceWords));
+      g_trace_cap = (size_t)items * kTraceWords;
     }
     jp.trace = g_trace_dev;
     g_trace_items = items;
@@ -1240,7 +1240,7 @@ int64_t pcbz_item_trace(uint64_t *out, int64_t max_items, int *segments) {
   if (!g_trace_dev || g_trace_items == 0) return 0;
   const int64_t n = std::min(max_items, g_trace_items);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(PCBZ_E_CUDA, "trace sync failed");
-  if (cudaMemcpy(out, g_trace_dev, (size_t)n * 24, cudaMemcpyDeviceToHost) != cudaSuccess)
+  if (cudaMemcpy(out, g_trace_dev, (size_t)n * 8 * kTraceWords, cudaMemcpyDeviceToHost) != cudaSuccess)
     return fail(PCBZ_E_CUDA, "trace copy failed");
   if (segments) *segments = g_trace_segments;
   return n;

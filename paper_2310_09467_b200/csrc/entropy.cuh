@@ -117,19 +117,39 @@ __device__ __forceinline__ double np_term(double c, double total) {
 // 32w + j occupied) and synchronised.
 template <typename Get>
 __device__ double block_entropy(Get get, double total, NpScratch &S, const double *terms,
-                                bool occ_ready = false, int64_t nterms = kTermTable) {
+                                bool occ_ready = false, int64_t nterms = kTermTable,
+                                uint64_t *stamps = nullptr) {
   const int t = threadIdx.x;
+  auto stamp = [&](int i) {  // phase timestamps for profiling (PCBZ_TRACE_WORDS = 9)
+    if (stamps && t == 0) {
+      uint64_t v;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+      stamps[i] = v;
+    }
+  };
   // occupancy bitmap: one warp per 32-bin word (lane j reads bin 32w + j,
   // so the reads are bank-conflict free), a ballot makes the word
   if (!occ_ready) {
+    // four words per warp step: their count reads are independent
     const int lane = t & 31;
-    for (int w = t >> 5; w < kOccWords; w += kEntropyThreads / 32) {
-      const bool occ = total > 0.0 && get(32 * w + lane) != 0;
-      const uint32_t bits = __ballot_sync(0xffffffffu, occ);
-      if (lane == 0) S.occ[w] = bits;
+    constexpr int kStep = kEntropyThreads / 32;
+    for (int w0 = t >> 5; w0 < kOccWords; w0 += 4 * kStep) {
+      bool occ[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int w = w0 + u * kStep;
+        occ[u] = w < kOccWords && total > 0.0 && get(32 * w + lane) != 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int w = w0 + u * kStep;
+        const uint32_t bits = __ballot_sync(0xffffffffu, occ[u]);
+        if (lane == 0 && w < kOccWords) S.occ[w] = bits;
+      }
     }
   }
   __syncthreads();
+  stamp(0);
   const int w_lo = occ_word_lo(t), w_hi = occ_word_lo(t + 1);
   uint32_t cnt = 0;
   for (int w = w_lo; w < w_hi; ++w) cnt += __popc(S.occ[w]);
@@ -155,9 +175,20 @@ __device__ double block_entropy(Get get, double total, NpScratch &S, const doubl
     __syncthreads();
     return 0.0;
   }
+  stamp(1);
   if (t < 32) np_build_tree(n_all, S);
   __syncthreads();
+  stamp(2);
   const int nodes = (int)S.level_start[S.nlevels];
+  // a host-registered table covers every count (nterms = total + 1)
+  const bool full_table = terms && (double)nterms > total;
+  auto term_of = [&](uint64_t c) -> double {
+    if (full_table) return __ldg(terms + c);
+    if (!terms) return np_term((double)c, total);
+    const bool in = c < (uint64_t)nterms;
+    const double v = __ldg(terms + (in ? c : 0));
+    return in ? v : np_term((double)c, total);
+  };
   // ---- leaves ---------------------------------------------------------------
   for (int j = t; j < nodes; j += kEntropyThreads) {
     if (S.node_child[j] != kNpLeaf) continue;
@@ -180,12 +211,6 @@ __device__ double block_entropy(Get get, double total, NpScratch &S, const doubl
       const int bin = 32 * w + __ffs(bits) - 1;
       bits &= bits - 1;
       return bin;
-    };
-    auto term_of = [&](uint64_t c) -> double {
-      if (!terms) return np_term((double)c, total);
-      const bool in = c < (uint64_t)nterms;
-      const double v = __ldg(terms + (in ? c : 0));
-      return in ? v : np_term((double)c, total);
     };
     auto next_term = [&]() -> double { return term_of(get(next_bin())); };
     // eight terms at a time: bin indices first (bitmap walk), then all eight
@@ -221,6 +246,7 @@ __device__ double block_entropy(Get get, double total, NpScratch &S, const doubl
     S.node_sum[j] = res;
   }
   __syncthreads();
+  stamp(3);
   // ---- internal nodes, deepest level first ----------------------------------
   for (int L = S.nlevels - 2; L >= 0; --L) {
     for (int j = (int)S.level_start[L] + t; j < (int)S.level_start[L + 1]; j += kEntropyThreads) {

@@ -20,6 +20,10 @@ constexpr int64_t kMinItemPixels = 1 << 18;    // smaller work items lose to per
 constexpr int kEntropyThreads = 192;           // all entropy reductions use this shape
 constexpr int kMaxFastPitch = 16;              // fast path: pitch_x <= 16 (template parameter)
 constexpr int kTermTable = 65536;              // precomputed entropy terms per call (entropy.cuh)
+#ifndef PCBZ_TRACE_WORDS
+#define PCBZ_TRACE_WORDS 3   // per-item trace stamps (5: + claim-sweep and stitch ends, for profiling)
+#endif
+constexpr int kTraceWords = PCBZ_TRACE_WORDS;
 // per-item partial histogram of a multi-segment / band judge: the item's
 // packed u16 words as they sit in shared memory, its spill count and its
 // spilled bins (each + kSpill), written with plain stores (judge_kernel.cuh)

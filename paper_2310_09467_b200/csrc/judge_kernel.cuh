@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
                    sb + len * (tid + 1) / kJudgeThreads, cs);
     }
     __syncthreads();
-    if (P.trace && tid == 0) P.trace[3 * item + 1] = globaltimer_ns();  // every run done
+    if (P.trace && tid == 0) P.trace[kTraceWords * item + 1] = globaltimer_ns();  // every run done
     for (int w4 = tid; w4 < kHistWords / 4; w4 += kJudgeThreads) {
       const uint4 q = reinterpret_cast<const uint4 *>(hist_w)[w4];
       if ((q.x | q.y | q.z | q.w) & 0x80008000u) {
@@ -591,6 +591,7 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
       }
     }
     __syncthreads();
+    if (kTraceWords > 3 && P.trace && tid == 0) P.trace[kTraceWords * item + 3] = globaltimer_ns();
 
     // ---- stitch the 192 runs in stream order (segment-summary combine) -----
     // One warp per key, 32 runs per step: the runs holding key v are found
@@ -686,6 +687,7 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
     }
     __syncthreads();
 
+    if (kTraceWords > 4 && P.trace && tid == 0) P.trace[kTraceWords * item + 4] = globaltimer_ns();
     if (P.direct) {
       // whole stream in this CTA: bucket seams (_kernels.py:125-133) ...
       if (tid < 32) {  // one warp: each non-empty bucket pairs with the previous one
@@ -712,11 +714,12 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
       __syncthreads();
       auto get = [&](int bin) -> uint64_t {
         uint32_t c = bin_count16(hist_w, (uint32_t)bin);
-        if (spilled[bin >> 5] & (1u << (bin & 31)))
+        if (ns && (spilled[bin >> 5] & (1u << (bin & 31))))
           for (int i = 0; i < ns; ++i) c += spill_w[i] == (uint32_t)bin ? kSpill : 0u;
         return c;
       };
-      const double e = block_entropy(get, (double)(2 * P.npix - 1), scr, P.terms, false, P.nterms);
+      const double e = block_entropy(get, (double)(2 * P.npix - 1), scr, P.terms, false, P.nterms,
+                                     (kTraceWords > 5 && P.trace) ? P.trace + kTraceWords * item + 5 : nullptr);
       if (tid == 0) P.ent[pr.slot] = e;
     } else {
       // publish the item's partial histogram (coalesced plain stores of the
@@ -736,8 +739,8 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
     }
     __syncthreads();
     if (P.trace && tid == 0) {
-      P.trace[3 * item] = ((uint64_t)smid() << 48) | (t_start & 0xFFFFFFFFFFFFull);
-      P.trace[3 * item + 2] = globaltimer_ns();
+      P.trace[kTraceWords * item] = ((uint64_t)smid() << 48) | (t_start & 0xFFFFFFFFFFFFull);
+      P.trace[kTraceWords * item + 2] = globaltimer_ns();
     }
   }
 }

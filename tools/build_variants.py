@@ -21,6 +21,8 @@ VARIANTS = {
     "pf32": ("PCBZ_PREFETCH=32",),
     "evict_last": ("PCBZ_LDG_HINT=1",),
     "emit_chunks": ("PCBZ_EMIT_RUNS=0",),
+    "trace5": ("PCBZ_TRACE_WORDS=5",),
+    "trace9": ("PCBZ_TRACE_WORDS=9",),
 }
 
 def build_from_git(rev: str, name: str):
