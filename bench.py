@@ -447,6 +447,7 @@ def run_gpu(args, wl: Workload):
     sel_h = torch.empty(nloc, dtype=torch.uint8).pin_memory().numpy()
     stream_h = torch.empty((nloc, 2 * H * W), dtype=torch.uint8).pin_memory().numpy()
     out = (ent_h, sel_h, stream_h)
+    pipeline.judge_volume(vol_np, geo, codes, wl.temporal, halo=halo_np, out=out)   # sizes the buffers
     t0 = time.perf_counter()
     pipeline.judge_volume(vol_np, geo, codes, wl.temporal, halo=halo_np, out=out)
     one = time.perf_counter() - t0
@@ -598,6 +599,7 @@ def run_gpu_bands(args, wl: Workload):
         sel_h.copy_(judge.sel, non_blocking=True)
         torch.cuda.synchronize(dev)
 
+    e2e_step()   # sizes the buffers
     t0 = time.perf_counter()
     e2e_step()
     one = time.perf_counter() - t0
