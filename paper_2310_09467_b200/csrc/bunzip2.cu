@@ -956,7 +956,9 @@ int decode_batch(const uint8_t *const *payloads, const int64_t *plen, const std:
               if (v & (1u << q)) r ^= zs[(k - 1) * 32 + q];
             zs[k * 32 + bit] = r;
           }
-        BZD_TRY(cudaMemcpy(g.zs.p, zs.data(), zs.size() * 4, cudaMemcpyHostToDevice));
+        // on the decode stream (a pageable cudaMemcpy is not ordered with it)
+        BZD_TRY(cudaMemcpyAsync(g.zs.p, zs.data(), zs.size() * 4, cudaMemcpyHostToDevice, st));
+        BZD_TRY(cudaStreamSynchronize(st));
         g.zs_ready = true;
       }
       BZD_TRY(g.crcacc.ensure((size_t)nvb * 4));

@@ -946,7 +946,10 @@ int pcbz_register_entropy_terms(int64_t total, const double *terms, int64_t n) {
                 g_terms_bytes, bytes);
   double *d = nullptr;
   CUDA_TRY(cudaMalloc(&d, bytes));
-  if (cudaMemcpy(d, terms, bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+  // a pageable cudaMemcpy may return before its DMA lands, and the kernels
+  // that read the table run on non-blocking streams: wait for the device
+  if (cudaMemcpy(d, terms, bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {
     cudaFree(d);
     return fail(PCBZ_E_CUDA, "copy of the entropy term table failed");
   }

@@ -574,7 +574,10 @@ __global__ void __launch_bounds__(kJudgeThreads, 1) judge_hist_kernel(const Judg
         lane_fast_dispatch<PX, false>(pr.spec & 0x7F, src, prv, P.W, P.py, P.npix, ca * 8,
                                       cz - ca, cfg, cs, std::make_integer_sequence<int, 13>{});
     } else {
-      const int64_t sb = P.npix * gseg / gtot, se = P.npix * (gseg + 1) / gtot;
+      // 8-pixel granules whenever npix % 8 == 0, as pcbz_band_range splits
+      // bands: a band then reads exactly the rows shard.band_rows gives it
+      const int64_t g = P.npix % 8 == 0 ? 8 : 1, n = P.npix / g;
+      const int64_t sb = g * (n * gseg / gtot), se = g * (n * (gseg + 1) / gtot);
       const int64_t len = se - sb;
       lane_generic(src, prv, cfg, P.W, P.npix, sb + len * tid / kJudgeThreads,
                    sb + len * (tid + 1) / kJudgeThreads, cs);

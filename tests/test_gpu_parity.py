@@ -392,7 +392,11 @@ def _run_bands(vol_t, halo_t, shape, pitch, codes, temporal, nbands, rows_only=F
 @pytest.mark.parametrize("shape,pitch,halo,nbands", [
     ((3, 96, 128), (15, 15), True, 2), ((3, 96, 128), (15, 15), True, 3),
     ((3, 96, 128), (15, 15), True, 8), ((2, 61, 75), (6, 5), False, 3),
-    ((2, 40, 48), (17, 9), False, 5), ((1, 64, 64), (13, 13), False, 1)])
+    ((2, 40, 48), (17, 9), False, 5), ((1, 64, 64), (13, 13), False, 1),
+    # generic path (W % 8 != 0 or pitch > 16) with npix % 8 == 0 and band edges
+    # off the 8-pixel granule of a pixel-granular split (tools/stress_bands.py)
+    ((3, 187, 8), (17, 22), False, 2), ((1, 18, 20), (14, 13), True, 7),
+    ((2, 108, 34), (9, 13), True, 7), ((3, 248, 9), (12, 4), True, 6)])
 @pytest.mark.parametrize("rows_only,replicated", [(False, False), (True, False), (False, True)])
 def test_band_sharded_judge_equals_whole_frames(shape, pitch, halo, nbands, rows_only, replicated):
     """pcbz_judge_band_device x nbands + the owner-computes merge (or the
