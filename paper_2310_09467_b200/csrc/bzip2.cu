@@ -347,21 +347,10 @@ __global__ void pair_keys_kernel(const uint32_t *U, uint32_t m, const uint32_t *
 // C: BWT column, MTF and zero-run coding (compress.c generateMTFValues)
 // ---------------------------------------------------------------------------
 //
-// One warp per block.  The 256-entry MTF list lives in registers: lane l
-// holds positions 8l..8l+7 as the bytes of a 64-bit word.  A symbol is found
-// with two SIMD byte compares and a ballot; moving it to the front shifts
-// every lane below it by one byte (the carry byte comes from the lane below
-// through a shuffle).  BWT characters are gathered 32 at a time.
+// One warp per segment of a block's BWT column (C3 below); BWT characters
+// are gathered 32 at a time.
 
 constexpr int kMtfWarps = 4;
-
-__device__ __forceinline__ uint32_t byte_match(uint64_t w, uint32_t s) {
-  // mask of bytes of w equal to s (bit k set for byte k)
-  const uint32_t lo = __vcmpeq4((uint32_t)w, s * 0x01010101u);
-  const uint32_t hi = __vcmpeq4((uint32_t)(w >> 32), s * 0x01010101u);
-  const uint64_t m = ((uint64_t)hi << 32) | lo;        // 0xFF per matching byte
-  return (uint32_t)(__popcll(m & 0x0101010101010101ull) ? (__ffsll(m) - 1) / 8 + 1 : 0);
-}
 
 // Segment-parallel form: the MTF list at any position is "symbols by most
 // recent occurrence, then the never-seen ones in symbol order", so each
@@ -441,7 +430,15 @@ __global__ void mtf_prefix_kernel(const uint32_t *seg0, int32_t *lastpos) {
   }
 }
 
-// C3: MTF ranks of one segment (warp), list in registers
+// C3: MTF ranks of one segment (warp).  The warp holds the inverse of the
+// MTF list -- the current position of every symbol -- as 16-bit fields, lane
+// l owning symbols 8l..8l+7 in four registers.  Coding symbol s: its owner's
+// field is the rank r (one byte permute + one shuffle); every symbol at a
+// position below r moves down one (SWAR: the borrow of (b | 0x8000) - r in
+// each field's guard bit), and s itself goes to position 0.  About 35
+// instructions per symbol with no data-dependent branch, against ~75 for a
+// list kept in list order (find by byte compare + ballot, shift by a
+// shuffled carry byte), measured 77 ms on C2 (profiles/r01_compress_launches_c2_100.txt).
 __global__ void __launch_bounds__(32 * kMtfWarps) mtf_rank_kernel(const Block *blocks, const int *ids, int nb,
                                                                    const uint32_t *seg0, const uint8_t *symseq,
                                                                    const int32_t *before, uint8_t *ranks) {
@@ -454,7 +451,7 @@ __global__ void __launch_bounds__(32 * kMtfWarps) mtf_rank_kernel(const Block *b
   const Block &B = blocks[ids[t]];
   const uint32_t k = sg - seg0[t];
   int32_t *bef = s_bef[warp];
-  uint8_t *at = s_at[warp];
+  uint8_t *at = s_at[warp];   // at[symbol] = its position in the segment's initial list
   int seen_mine = 0;
   for (int x = lane; x < 256; x += 32) {
     bef[x] = before[(size_t)sg * 256 + x];
@@ -472,11 +469,14 @@ __global__ void __launch_bounds__(32 * kMtfWarps) mtf_rank_kernel(const Block *b
       pos = nseen;
       for (int y = 0; y < x; ++y) pos += bef[y] < 0;
     }
-    at[pos] = (uint8_t)x;
+    at[x] = (uint8_t)pos;
   }
   __syncwarp();
-  uint64_t lst = 0;
-  for (int q = 0; q < 8; ++q) lst |= (uint64_t)at[8 * lane + q] << (8 * q);
+  uint32_t w0, w1, w2, w3;   // positions of symbols 8l + {0,1}, {2,3}, {4,5}, {6,7}
+  w0 = at[8 * lane + 0] | ((uint32_t)at[8 * lane + 1] << 16);
+  w1 = at[8 * lane + 2] | ((uint32_t)at[8 * lane + 3] << 16);
+  w2 = at[8 * lane + 4] | ((uint32_t)at[8 * lane + 5] << 16);
+  w3 = at[8 * lane + 6] | ((uint32_t)at[8 * lane + 7] << 16);
   const uint32_t n = (uint32_t)B.n;
   const uint32_t j0 = k * kMtfSeg, j1 = min(n, j0 + kMtfSeg);
   for (uint32_t jb = j0; jb < j1; jb += 32) {
@@ -486,19 +486,25 @@ __global__ void __launch_bounds__(32 * kMtfWarps) mtf_rank_kernel(const Block *b
     uint32_t myrank = 0;
     for (int q = 0; q < cnt; ++q) {
       const uint32_t s = __shfl_sync(0xffffffffu, sym, q);
-      const uint32_t k1 = byte_match(lst, s);
-      const uint32_t ball = __ballot_sync(0xffffffffu, k1 != 0);
-      const int pl = __ffs(ball) - 1;
-      const int pk = (int)__shfl_sync(0xffffffffu, k1, pl) - 1;
-      const uint32_t top = (uint32_t)(lst >> 56);
-      uint32_t carry = __shfl_up_sync(0xffffffffu, top, 1);
-      if (lane == 0) carry = s;
-      // branch-free: lanes below pl shift all entries, lane pl those up to pk
-      const uint64_t shifted = (lst << 8) | carry;
-      const uint64_t keep = pk == 7 ? 0ull : (~0ull << (8 * (pk + 1)));
-      const uint64_t partial = (shifted & ~keep) | (lst & keep);
-      lst = lane < pl ? shifted : (lane == pl ? partial : lst);
-      myrank = lane == q ? (uint32_t)(8 * pl + pk) : myrank;
+      const uint32_t f = s & 7u;                      // field of s in its owner lane
+      const uint32_t lo = f & 4u ? w2 : w0, hi = f & 4u ? w3 : w1;
+      const uint32_t b0 = (f & 3u) * 2u;              // its two bytes within (hi:lo)
+      const uint32_t mine = __byte_perm(lo, hi, b0 | ((b0 + 1u) << 4)) & 0xFFFFu;
+      const uint32_t r = __shfl_sync(0xffffffffu, mine, (int)(s >> 3));
+      const uint32_t R2 = r * 0x00010001u;
+      // fields b < r gain one: no borrow into the guard bit of (b | 0x8000) - r
+      w0 += (~(w0 + 0x80008000u - R2) & 0x80008000u) >> 15;
+      w1 += (~(w1 + 0x80008000u - R2) & 0x80008000u) >> 15;
+      w2 += (~(w2 + 0x80008000u - R2) & 0x80008000u) >> 15;
+      w3 += (~(w3 + 0x80008000u - R2) & 0x80008000u) >> 15;
+      // s (field value r, unchanged above) moves to the front
+      const uint32_t clr = lane == (int)(s >> 3) ? r << ((f & 1u) << 4) : 0u;
+      const uint32_t wi = f >> 1;
+      w0 -= wi == 0u ? clr : 0u;
+      w1 -= wi == 1u ? clr : 0u;
+      w2 -= wi == 2u ? clr : 0u;
+      w3 -= wi == 3u ? clr : 0u;
+      myrank = lane == q ? r : myrank;
     }
     if (j < j1) ranks[B.base + j] = (uint8_t)myrank;
   }
