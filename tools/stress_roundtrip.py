@@ -8,16 +8,14 @@ default bzip2 block sizes, device or host bzip2 coder.  Every case must give
   * decompress_stack(container) == the input (device bzip2 decoder where it
     takes the container, GPU inverse prediction incl. the band wavefront
     kernel for pitch_x <= 64, pitch_y <= 31),
-  * the pipelined host judge (pcbz_judge_host in chunks of 3 frames, a halo
-    across chunks) == the oracle's selections and streams.
+  * the pipelined host judge (pcbz_judge_host; run as a script, in chunks of
+    3 frames with a halo across chunks) == the oracle's selections and streams.
 
     python tools/stress_roundtrip.py [cases] [seed] [--only=i,j]
 """
 import os
 import sys
 from pathlib import Path
-
-os.environ.setdefault("PCBZ_HOST_CHUNK", "3")   # read once by the library: pipeline every call
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path[:0] = [str(ROOT), str(ROOT / "oracle"), str(ROOT / "tools")]
@@ -98,4 +96,7 @@ def main():
 
 
 if __name__ == "__main__":
+    # read once per process by the library (first pcbz_judge_host call):
+    # pipeline every call, a halo across every chunk boundary
+    os.environ.setdefault("PCBZ_HOST_CHUNK", "3")
     sys.exit(main())
