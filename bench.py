@@ -45,14 +45,18 @@ from workloads.configs import (ALL26, INTRA, SNR_LEVELS, WORKLOADS, Workload, c2
 frame_params = c2_params  # used by tools/
 
 
-def config(wl: Workload, world: int = 1, shard: str = "frames"):
+def config(wl: Workload, world: int = 1, shard: str = "frames", exchange: str = "nccl"):
     """The workload description -- identical on both arms (ours / reference)."""
     nbytes = wl.frames * 2 * wl.height * wl.width
     c = {"workload": wl.description, "frames": wl.frames, "height": wl.height, "width": wl.width,
          "pitch": [wl.pitch, wl.pitch], "candidates": len(wl.codes), "temporal": wl.temporal,
          "l2_policy": (f"inputs ({nbytes / 1e6:.0f} MB/GPU) larger than L2 (126 MB), no flush"
                        if nbytes > 126e6 else "input smaller than L2: L2 flushed (256 MB write) before every step")}
-    if shard == "bands":
+    if shard == "bands" and exchange == "peer":
+        c["parallelism"] = (f"within-frame bands x{world} (owner-computes merge pulling the partial pair "
+                            "histograms and segment summaries of its slots from every rank over symmetric "
+                            "memory and pushing the entropies to every rank, flag barriers; no NCCL)")
+    elif shard == "bands":
         c["parallelism"] = (f"within-frame bands x{world} (NCCL reduce-scatter of partial pair histograms, "
                             "all-to-all of segment summaries, owner-computes merge, all-gather of entropies)")
     elif world > 1:
@@ -237,7 +241,7 @@ def run_reference(args, wl: Workload):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong" if wl.series else "weak", "vs_baseline": None, "dtype": "u16",
-        "data": "synthetic (reference synth.generate, bit-identical)", "config": config(wl, world, args.shard),
+        "data": "synthetic (reference synth.generate, bit-identical)", "config": config(wl, world, args.shard, args.exchange),
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample,
                          "cpu": _cpu_model()},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -555,8 +559,12 @@ def run_gpu_bands(args, wl: Workload):
     pinned = torch.empty((F, H, W), dtype=torch.uint16).pin_memory()
     pinned.numpy()[...] = host
     frames = pinned.to(dev)
+    peer = args.exchange == "peer"
     judge = BandJudge((F, H, W), (wl.pitch, wl.pitch), wl.codes, wl.temporal, False, rank, world,
-                      device=dev)
+                      device=dev, exchange=args.exchange,
+                      group=dist.group.WORLD if peer and world > 1 else None)
+    if peer and world == 1:
+        judge.attach_peers([judge])
     stream = torch.cuda.current_stream(dev)
     ranks = Ranks(world, dev)
     barrier, max_over_ranks = ranks.barrier, ranks.max
@@ -625,16 +633,23 @@ def run_gpu_bands(args, wl: Workload):
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u16", "data": "synthetic (reference synth.generate, bit-identical)",
-        "config": config(wl, world, "bands"),
+        "config": config(wl, world, "bands", args.exchange),
         "roofline": {"bound": "hbm", "kernel": "judge_hist_kernel (band partial)", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                      "peak_kind": peak_kind, "hist_kernel_ms": hist_ms, "algorithmic_bytes_per_launch": alg},
         "e2e": {"value": raw_bytes / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": band_h.numel() + F,
-                "api": "paper_2310_09467_b200.device.BandJudge (pcbz_judge_band_device, reduce-scatter + all-to-all, pcbz_judge_merge_slots_device, all-gather, pcbz_judge_select_device, pcbz_emit_band_device)",
+                "api": ("paper_2310_09467_b200.device.BandJudge (pcbz_judge_band_device, pcbz_peer_signal, "
+                        "pcbz_judge_merge_peers_device: pull-reduce + push of the entropies over symmetric "
+                        "memory, pcbz_peer_signal, pcbz_judge_select_device, pcbz_emit_band_device)" if peer else
+                        "paper_2310_09467_b200.device.BandJudge (pcbz_judge_band_device, reduce-scatter + "
+                        "all-to-all, pcbz_judge_merge_slots_device, all-gather, pcbz_judge_select_device, "
+                        "pcbz_emit_band_device)"),
                 "clocks": clk.summary(t_e0, t_e1), "steps": e2e_steps},
         # band: (delta frames if temporal) + hist + reduce, owned merge, select, emit
-        "gpu_launches": ((5 if judge.stream is not None else 4) + (1 if wl.temporal else 0)) * args.steps,
+        # (+ two barrier kernels with the peer exchange)
+        "gpu_launches": ((5 if judge.stream is not None else 4) + (1 if wl.temporal else 0)
+                         + (2 if peer else 0)) * args.steps,
         "clocks": clk.summary(t_dev0, t_dev1),
     }
     print(json.dumps(res), flush=True)
@@ -672,6 +687,9 @@ def parse_args(argv=None):
     ap.add_argument("--numba-baseline", action="store_true",
                     help="also time the reference's own numba path (baseline/_ref) on a sample")
     ap.add_argument("--no-pipeline", action="store_true", help="skip the informational pipeline_e2e")
+    ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
+                    help="--shard bands: merge exchange through NCCL collectives, or inside the merge "
+                         "kernel over symmetric (NVLink peer) memory")
     ap.add_argument("--shard", choices=["frames", "bands"], default="frames",
                     help="N>1: frame shards / replicas (default) or within-frame bands (c1, c4)")
     return ap.parse_args(argv)

@@ -202,6 +202,33 @@ PCBZ_API int pcbz_judge_merge_slots_device(int64_t nframes, int64_t h, int64_t w
                                   const uint8_t *specs, int k, int temporal, int has_halo, int nbands,
                                   int64_t slot_begin, int64_t slot_count, uint32_t *d_hist_owned,
                                   const int16_t *d_summaries_owned, double *d_ent_owned, void *stream);
+/* The same merge with the exchange in the kernel, over peer memory (NVLink
+ * P2P / symmetric memory mapped into this process; replaces the
+ * reduce-scatter + all-to-all + all-gather of the owner-computes merge):
+ * d_peer_hist / d_peer_summaries / d_peer_ent are DEVICE arrays of nbands
+ * pointers to every band's partial histograms ([nbands*q][65536] u32, as
+ * pcbz_judge_band_device writes them), segment summaries ([nbands*q][S][2][256]
+ * i16) and gathered-entropy table ([nbands*q] f64), q = ceil(nframes*k /
+ * nbands).  This rank (band) pulls and sums the rows of its slots
+ * [band*q, band*q + q) from every band, stitches them with every band's
+ * summaries, scores them, and stores each entropy into every rank's table
+ * (NaN for unscored slots); d_hist_scratch [q][65536] u32 and d_ent_owned [q]
+ * are its own.  The caller orders it between the partials and the argmin
+ * of every rank with pcbz_peer_signal.  Identical, bit for bit, to the
+ * owner-computes merge. */
+PCBZ_API int pcbz_judge_merge_peers_device(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py,
+                                  const uint8_t *specs, int k, int temporal, int has_halo, int nbands,
+                                  int band, const uint64_t *d_peer_hist, const uint64_t *d_peer_summaries,
+                                  const uint64_t *d_peer_ent, uint32_t *d_hist_scratch, double *d_ent_owned,
+                                  void *stream);
+/* Cross-rank barrier over peer memory, enqueued on `stream` (one thread):
+ * mode 1 arrives (release-stores `epoch` at index `rank` of every rank's flag
+ * array; d_peer_flags = device array of nranks pointers to them), mode 2
+ * waits until every entry of this rank's array d_my_flags[nranks] reached
+ * `epoch` (acquire; wrap-safe), 3 does both.  A rank that never arrives
+ * traps the kernel after ~30 s. */
+PCBZ_API int pcbz_peer_signal(const uint64_t *d_peer_flags, uint32_t *d_my_flags, int nranks, int rank,
+                     uint32_t epoch, int mode, void *stream);
 PCBZ_API int pcbz_judge_select_device(int64_t nframes, const uint8_t *specs, int k, int temporal, int has_halo,
                              const double *d_ent, uint8_t *d_sel_out, void *stream);
 PCBZ_API int pcbz_emit_band_device(const uint16_t *d_frames, const uint16_t *d_halo_prev, int64_t nframes,

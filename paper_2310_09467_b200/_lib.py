@@ -64,6 +64,10 @@ SIGNATURES = {
     "pcbz_judge_merge_slots_device": (_c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _c_int,
                                                _c_int, _c_int, _c_int, _c_i64, _c_i64, _vp, _vp, _vp,
                                                _vp]),
+    "pcbz_judge_merge_peers_device": (_c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _c_int,
+                                               _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp,
+                                               _vp, _vp]),
+    "pcbz_peer_signal": (_c_int, [_vp, _vp, _c_int, _c_int, ctypes.c_uint32, _c_int, _vp]),
     "pcbz_judge_select_device": (_c_int, [_c_i64, _vp, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
     "pcbz_emit_band_device": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp,
                                        _c_int, _c_int, _vp, _vp]),

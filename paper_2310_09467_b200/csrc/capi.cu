@@ -1194,6 +1194,61 @@ int pcbz_judge_merge_slots_device(int64_t nframes, int64_t h, int64_t w, int64_t
   return PCBZ_OK;
 }
 
+int pcbz_judge_merge_peers_device(int64_t nframes, int64_t h, int64_t w, int64_t px, int64_t py,
+                                  const uint8_t *specs, int k, int temporal, int has_halo, int nbands,
+                                  int band, const uint64_t *d_peer_hist, const uint64_t *d_peer_summaries,
+                                  const uint64_t *d_peer_ent, uint32_t *d_hist_scratch, double *d_ent_owned,
+                                  void *stream) {
+  int rc = check_device();
+  if (rc) return rc;
+  if (!d_peer_hist || !d_peer_summaries || !d_peer_ent || !d_hist_scratch || !d_ent_owned)
+    return fail(PCBZ_E_INVALID, "peer merge needs the peer pointer arrays and the owned buffers");
+  if (band < 0 || band >= nbands)
+    return fail(PCBZ_E_INVALID, "band %d of %d invalid", band, nbands);
+  Plan pl;
+  rc = make_plan(nframes, h, w, px, py, specs, k, has_halo != 0, temporal, true, pl, nbands, 0);
+  if (rc) return rc;
+  JudgeParams &jp = pl.jp;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  g_launches = 0;
+  const int64_t q = (nframes * k + nbands - 1) / nbands;   // owned slots per rank (shard.BandBuffers)
+  jp.slot0 = (int64_t)band * q;
+  jp.slot_count = q;
+  jp.nslots = q;
+  jp.ghist = d_hist_scratch;
+  jp.segsum = nullptr;
+  jp.ent = d_ent_owned;
+  jp.peer_hist = d_peer_hist;
+  jp.peer_summ = d_peer_summaries;
+  jp.peer_ent = d_peer_ent;
+  double *terms = nullptr;
+  const bool host_terms = use_registered_terms(jp);
+  if (!host_terms) {
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&terms), kTermTable * sizeof(double), st));
+    CUDA_TRY(launch_term_table((double)(2 * jp.npix - 1), terms, st));
+    jp.terms = terms;
+    jp.nterms = kTermTable;
+  }
+  CUDA_TRY(cudaMemsetAsync(d_ent_owned, 0xFF, (size_t)q * sizeof(double), st));  // NaN
+  CUDA_TRY(launch_finalize_slots(jp, st));
+  if (terms) CUDA_TRY(cudaFreeAsync(terms, st));
+  g_launches = host_terms ? 1 : 2;
+  return PCBZ_OK;
+}
+
+int pcbz_peer_signal(const uint64_t *d_peer_flags, uint32_t *d_my_flags, int nranks, int rank, uint32_t epoch,
+                     int mode, void *stream) {
+  int rc = check_device();
+  if (rc) return rc;
+  if (nranks < 1 || rank < 0 || rank >= nranks || mode < 1 || mode > 3)
+    return fail(PCBZ_E_INVALID, "peer signal: rank %d of %d, mode %d invalid", rank, nranks, mode);
+  if (((mode & 1) && !d_peer_flags) || ((mode & 2) && !d_my_flags))
+    return fail(PCBZ_E_INVALID, "peer signal needs the flag arrays");
+  CUDA_TRY(launch_peer_signal(d_peer_flags, d_my_flags, nranks, rank, epoch, mode, static_cast<cudaStream_t>(stream)));
+  g_launches = 1;
+  return PCBZ_OK;
+}
+
 int pcbz_judge_select_device(int64_t nframes, const uint8_t *specs, int k, int temporal, int has_halo,
                              const double *d_ent, uint8_t *d_sel_out, void *stream) {
   int rc = check_device();

@@ -20,11 +20,15 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
   // block = slot - slot0 of this rank's slots, whose histograms, summaries
   // and entropies are stored at that local index
   PairRef pr;
-  int64_t lslot;
+  int64_t lslot, slot = 0;
   if (P.slot_count > 0) {
-    const int64_t slot = P.slot0 + blockIdx.x;
+    slot = P.slot0 + blockIdx.x;
     const int64_t pair = slot_pair(P, slot);
-    if (pair < 0) return;  // unscored (entropy stays NaN) or padding
+    if (pair < 0) {  // unscored (entropy stays NaN) or padding
+      if (P.peer_ent && threadIdx.x < P.nbands)
+        reinterpret_cast<double *>(P.peer_ent[threadIdx.x])[slot] = __longlong_as_double(-1ll);
+      return;
+    }
     pr = pair_ref(P, pair);
     lslot = blockIdx.x;
   } else {
@@ -32,6 +36,20 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
     lslot = pr.slot;
   }
   uint32_t *G = P.ghist + (size_t)lslot * 65536;
+  if (P.peer_hist) {
+    // the reduce-scatter, fused: this owner pulls its slot's row from every
+    // band's partial histograms over peer memory and sums it in place
+    uint4 *G4w = reinterpret_cast<uint4 *>(G);
+    for (int i = threadIdx.x; i < 16384; i += kEntropyThreads) {
+      uint4 acc = make_uint4(0, 0, 0, 0);
+      for (int b = 0; b < P.nbands; ++b) {
+        const uint4 v = __ldcv(reinterpret_cast<const uint4 *>(P.peer_hist[b]) + (size_t)slot * 16384 + i);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+      G4w[i] = acc;
+    }
+    __syncthreads();
+  }
   // the pair's segment summaries in stream order, staged in the (not yet
   // used) count buffer when they fit: 16-byte loads instead of a dependent
   // chain of 2-byte loads per key
@@ -40,15 +58,21 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
   if (staged) {
     uint4 *dst = reinterpret_cast<uint4 *>(c16);
     for (int b = 0; b < P.nbands; ++b) {
-      const uint4 *src = reinterpret_cast<const uint4 *>(
-          P.segsum + ((size_t)b * P.nslots + lslot) * P.S * 512);
-      for (int i = threadIdx.x; i < P.S * 64; i += kEntropyThreads) dst[b * P.S * 64 + i] = __ldcg(src + i);
+      if (P.peer_summ) {   // every band's summaries of this slot, over peer memory
+        const uint4 *src = reinterpret_cast<const uint4 *>(P.peer_summ[b]) + (size_t)slot * P.S * 64;
+        for (int i = threadIdx.x; i < P.S * 64; i += kEntropyThreads) dst[b * P.S * 64 + i] = __ldcv(src + i);
+      } else {
+        const uint4 *src = reinterpret_cast<const uint4 *>(
+            P.segsum + ((size_t)b * P.nslots + lslot) * P.S * 512);
+        for (int i = threadIdx.x; i < P.S * 64; i += kEntropyThreads) dst[b * P.S * 64 + i] = __ldcg(src + i);
+      }
     }
     __syncthreads();
   }
   auto seg_sum = [&](int g) -> const int16_t * {
     if (staged) return reinterpret_cast<const int16_t *>(c16) + (size_t)g * 512;
     const int b = g / P.S, s = g - b * P.S;
+    if (P.peer_summ) return reinterpret_cast<const int16_t *>(P.peer_summ[b]) + ((size_t)slot * P.S + s) * 512;
     return P.segsum + (((size_t)b * P.nslots + lslot) * P.S + s) * 512;
   };
   for (int v = threadIdx.x; v < 256; v += kEntropyThreads) {
@@ -114,6 +138,38 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
   };
   const double e = block_entropy(get, (double)(2 * P.npix - 1), scr, P.terms, true, P.nterms);
   if (threadIdx.x == 0) P.ent[lslot] = e;
+  // the all-gather, fused: the entropy goes straight into every rank's table
+  if (P.peer_ent && threadIdx.x < P.nbands) reinterpret_cast<double *>(P.peer_ent[threadIdx.x])[slot] = e;
+}
+
+// Flag barrier over peer memory (one thread): release-store this rank's
+// epoch into every peer's flag array, then acquire-spin on its own array.
+// A peer that never arrives traps the kernel after ~30 s instead of hanging.
+__global__ void peer_signal_kernel(const uint64_t *peer_flags, uint32_t *my_flags, int nranks, int rank,
+                                   uint32_t epoch, int mode) {
+  if (mode & 1) {
+    __threadfence_system();
+    for (int p = 0; p < nranks; ++p) {
+      uint32_t *f = reinterpret_cast<uint32_t *>(peer_flags[p]) + rank;
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+    }
+  }
+  if (mode & 2) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int p = 0; p < nranks; ++p) {
+      for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(my_flags + p) : "memory");
+        if ((int32_t)(v - epoch) >= 0) break;
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 30000000000ull) __trap();
+        __nanosleep(200);
+      }
+    }
+    __threadfence_system();
+  }
 }
 
 // Sum of a slot's S per-item partial histograms (packed u16 words in the
@@ -243,6 +299,12 @@ cudaError_t launch_reduce_parts(const JudgeParams &p, cudaStream_t st) {
 cudaError_t launch_finalize_slots(const JudgeParams &p, cudaStream_t st) {
   if (p.slot_count <= 0) return cudaSuccess;
   judge_finalize_kernel<<<(unsigned)p.slot_count, kEntropyThreads, kFinalizeSmemBytes, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_signal(const uint64_t *peer_flags, uint32_t *my_flags, int nranks, int rank,
+                               uint32_t epoch, int mode, cudaStream_t st) {
+  peer_signal_kernel<<<1, 1, 0, st>>>(peer_flags, my_flags, nranks, rank, epoch, mode);
   return cudaGetLastError();
 }
 

@@ -86,6 +86,12 @@ struct JudgeParams {
   int64_t slot0, slot_count;  // slot-range finalize (owner-computes band merge): slots
                               // [slot0, slot0 + slot_count); slot_count 0 = per-pair mode
   int16_t *segsum;          // [nbands][nframes*k][S][2][256] when !direct
+  // peer exchange of the band merge (pcbz_judge_merge_peers_device; nullptr
+  // otherwise): device arrays of nbands pointers into every band's buffers,
+  // mapped into this process (NVLink peer memory / symmetric memory)
+  const uint64_t *peer_hist;  // [nbands] -> partial histograms [nbands*q][65536] u32
+  const uint64_t *peer_summ;  // [nbands] -> segment summaries [nbands*q][S][2][256] i16
+  const uint64_t *peer_ent;   // [nbands] -> gathered entropies [nbands*q] f64
   uint8_t *fscratch;        // [gridDim.x][kJudgeThreads][256]
   int *counter;             // dynamic item counter (zeroed before launch)
   uint64_t *trace;          // optional [items][3]: (smid << 48 | start ns, runs-done ns, end ns)
@@ -110,6 +116,11 @@ cudaError_t launch_reduce_parts(const JudgeParams &p, cudaStream_t st);
 // finalize of slots [p.slot0, p.slot0 + p.slot_count) (one block per slot)
 cudaError_t launch_finalize_slots(const JudgeParams &p, cudaStream_t st);
 cudaError_t launch_select(const JudgeParams &p, uint8_t *sel, cudaStream_t st);
+// cross-rank flag barrier over peer memory: mode 1 arrive (store `epoch` at
+// index `rank` of every peer's flag array), 2 wait (until every entry of
+// this rank's array reached `epoch`), 3 both
+cudaError_t launch_peer_signal(const uint64_t *peer_flags, uint32_t *my_flags, int nranks, int rank,
+                               uint32_t epoch, int mode, cudaStream_t st);
 cudaError_t launch_emit(const EmitParams &p, cudaStream_t st);       // per pixel, any shape
 cudaError_t launch_emit_any(const EmitParams &p, cudaStream_t st);   // chunked when possible
 cudaError_t launch_residual_image(const uint16_t *img, const uint16_t *prev, int64_t h, int64_t w,

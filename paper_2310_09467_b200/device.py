@@ -77,10 +77,23 @@ class BandJudge:
     """
 
     def __init__(self, frames_shape, pitch, codes, temporal: bool, has_halo: bool, band: int,
-                 nbands: int, want_stream: bool = True, device=None):
+                 nbands: int, want_stream: bool = True, device=None, exchange: str = "nccl",
+                 group=None):
+        """exchange "nccl": reduce-scatter / all-to-all / all-gather through
+        torch.distributed (shard.band_collective); "peer": the exchange
+        inside the merge kernel over peer memory (shard.band_peer_exchange)
+        -- with a process group the exchanged buffers are allocated in
+        symmetric memory and mapped from every rank (NVLink), without one
+        the caller wires the peers (attach_peers; one-GPU emulation)."""
         import torch
 
         from .shard import BandBuffers
+
+        if exchange not in ("nccl", "peer"):
+            raise ValueError(f"exchange must be 'nccl' or 'peer', got {exchange!r}")
+        self.exchange = exchange
+        self._epoch = 0
+        self._peer_arrays = None
 
         self.torch = torch
         F, H, W = frames_shape
@@ -106,7 +119,20 @@ class BandJudge:
         dev = self.device
         self.nslots = F * self.k
         self.workspace = torch.empty(max(ws.value, 1), dtype=torch.uint8, device=dev)
-        self.buf = BandBuffers.allocate(self.nslots, self.nbands, self.segments * 512, dev)
+        shared, symm = None, None
+        if exchange == "peer" and group is not None:
+            import torch.distributed._symmetric_memory as symm
+            shared = lambda shape, dtype: symm.empty(*shape, dtype=dtype, device=dev)  # noqa: E731
+        self.buf = BandBuffers.allocate(self.nslots, self.nbands, self.segments * 512, dev, shared)
+        # barrier flags of the peer exchange: entry r = last epoch rank r arrived at
+        self.flags = (shared((self.nbands,), torch.int32) if shared else
+                      torch.empty(self.nbands, dtype=torch.int32, device=dev))
+        self.flags.zero_()
+        if symm is not None:
+            torch.cuda.synchronize(dev)
+            handles = [symm.rendezvous(t, group) for t in
+                       (self.buf.hist, self.buf.summary, self.buf.ent_all, self.flags)]
+            self._set_peer_arrays(*[list(h.buffer_ptrs) for h in handles])
         self.q = self.buf.owned
         self.slot_begin = self.band * self.q
         self.ent = self.buf.ent_all[:self.nslots].view(F, self.k)
@@ -153,6 +179,53 @@ class BandJudge:
         _lib.check(rc)
         return self.buf.ent_owned
 
+    # ---- peer exchange (shard.band_peer_exchange) ------------------------------
+    def _set_peer_arrays(self, hist, summ, ent, flags):
+        t = self.torch
+        for name, ptrs in (("hist", hist), ("summaries", summ), ("entropies", ent), ("flags", flags)):
+            if len(ptrs) != self.nbands:
+                raise ValueError(f"{len(ptrs)} peer {name} pointers for {self.nbands} bands")
+        self._peer_arrays = tuple(t.tensor([int(p) for p in ptrs], dtype=t.int64, device=self.device)
+                                  for ptrs in (hist, summ, ent, flags))
+
+    def attach_peers(self, judges) -> None:
+        """Wire this band to the buffers of `judges` (every band, in band
+        order) living in this process -- the one-GPU stand-in for the
+        symmetric-memory mapping."""
+        js = sorted(judges, key=lambda j: j.band)
+        if [j.band for j in js] != list(range(self.nbands)):
+            raise ValueError("attach_peers needs one judge per band")
+        self._set_peer_arrays([j.buf.hist.data_ptr() for j in js], [j.buf.summary.data_ptr() for j in js],
+                              [j.buf.ent_all.data_ptr() for j in js], [j.flags.data_ptr() for j in js])
+
+    def next_epoch(self) -> int:
+        self._epoch += 1
+        return self._epoch
+
+    def _peers(self):
+        if self._peer_arrays is None:
+            raise RuntimeError("peer exchange without peers: build with exchange='peer' and a group, "
+                               "or call attach_peers")
+        return self._peer_arrays
+
+    def signal(self, epoch: int, mode: int, stream=None) -> None:
+        """pcbz_peer_signal: 1 arrive, 2 wait, 3 both (enqueued)."""
+        flags = self._peers()[3]
+        _lib.check(_lib.load().pcbz_peer_signal(flags.data_ptr(), self.flags.data_ptr(), self.nbands,
+                                                 self.band, ctypes.c_uint32(epoch & 0xFFFFFFFF), mode,
+                                                 self._st(stream)))
+
+    def merge_peers(self, stream=None):
+        """This rank's slots, pulled from every band over peer memory, scored,
+        and their entropies stored into every rank's table."""
+        h, sm, en, _ = self._peers()
+        rc = _lib.load().pcbz_judge_merge_peers_device(
+            self.F, self.H, self.W, self.px, self.py, self.codes.ctypes.data, self.k, self.temporal,
+            self.has_halo, self.nbands, self.band, h.data_ptr(), sm.data_ptr(), en.data_ptr(),
+            self.buf.hist_owned.data_ptr(), self.buf.ent_owned.data_ptr(), self._st(stream))
+        _lib.check(rc)
+        return self.buf.ent_owned
+
     def select(self, stream=None):
         """Every frame's argmin from the gathered entropies."""
         rc = _lib.load().pcbz_judge_select_device(
@@ -175,11 +248,15 @@ class BandJudge:
 
     def __call__(self, frames, halo=None, group=None, stream=None):
         """partial -> reduce-scatter / all-to-all -> owned merge -> all-gather
-        -> argmin -> emit (shard.band_collective)."""
+        -> argmin -> emit (shard.band_collective), or with exchange="peer"
+        partial -> barrier -> pull-merge-push over peer memory -> barrier ->
+        argmin -> emit (shard.band_peer_exchange)."""
         import contextlib
 
-        from .shard import band_collective
+        from .shard import band_collective, band_peer_exchange
 
+        if self.exchange == "peer":
+            return band_peer_exchange(self, frames, halo, stream)
         # the collectives order against torch's current stream: run the whole
         # sequence on `stream` as current
         ctx = self.torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()

@@ -110,18 +110,24 @@ class BandBuffers:
     ent_all: object
 
     @staticmethod
-    def allocate(nslots: int, nbands: int, summary_len: int, device=None):
+    def allocate(nslots: int, nbands: int, summary_len: int, device=None, shared=None):
+        """`shared(shape, dtype)` allocates the buffers other ranks read or
+        write in a peer exchange (hist, summary, ent_all: e.g. symmetric
+        memory); default torch.empty."""
         import torch
         q = -(-nslots // nbands)
-        hist = torch.zeros((nbands * q, 65536), dtype=torch.int32, device=device)
-        summary = torch.full((nbands * q, summary_len), -1, dtype=torch.int16, device=device)
+        shared = shared or (lambda shape, dtype: torch.empty(shape, dtype=dtype, device=device))
+        hist = shared((nbands * q, 65536), torch.int32)
+        hist.zero_()
+        summary = shared((nbands * q, summary_len), torch.int16)
+        summary.fill_(-1)
         if nbands == 1:   # no exchange: the owned views are the partial buffers themselves
-            ent = torch.empty(q, dtype=torch.float64, device=device)
+            ent = shared((q,), torch.float64)
             return BandBuffers(hist, summary, hist, summary.view(1, q, summary_len), ent, ent)
         return BandBuffers(hist, summary, torch.empty((q, 65536), dtype=torch.int32, device=device),
                            torch.empty((nbands, q, summary_len), dtype=torch.int16, device=device),
                            torch.empty(q, dtype=torch.float64, device=device),
-                           torch.empty(nbands * q, dtype=torch.float64, device=device))
+                           shared((nbands * q,), torch.float64))
 
     @property
     def owned(self) -> int:
@@ -155,6 +161,44 @@ def band_collective(partial_fn, merge_owned_fn, select_fn, emit_fn, buf: BandBuf
         dist.all_gather_into_tensor(buf.ent_all, buf.ent_owned, group=group)
     sel = select_fn()
     return buf.ent_all, sel, emit_fn()
+
+
+def band_peer_exchange(judge, frames, halo=None, stream=None):
+    """The band merge with the exchange inside the kernels, over peer memory
+    (DESIGN.md §7): partial -> barrier -> owner pulls and sums its slots'
+    rows from every band, stitches, scores and stores each entropy into every
+    rank's table -> barrier -> argmin -> emit.  No NCCL call: the barriers
+    are flag kernels over peer memory (pcbz_peer_signal), so the whole
+    sequence stays enqueued on `stream`.  `judge` is a BandJudge whose peers
+    are attached (BandJudge(exchange="peer", group=...) or attach_peers)."""
+    e = judge.next_epoch()
+    judge.partial(frames, halo, stream)
+    judge.signal(2 * e - 1, 3, stream)
+    judge.merge_peers(stream)
+    judge.signal(2 * e, 3, stream)
+    sel = judge.select(stream)
+    return judge.ent, sel, judge.emit(frames, halo, stream)
+
+
+def emulate_band_peer_exchange(judges, views) -> None:
+    """band_peer_exchange for ALL bands held by one process (one GPU), their
+    peer pointers wired to each other: every step of every band runs before
+    the next step of any (arrivals before waits), so no band waits on one
+    that has not been enqueued.  views[b] = (frames, halo) of band b."""
+    for j in judges:
+        j.attach_peers(judges)
+    e = judges[0].next_epoch()
+    for j in judges[1:]:
+        j.next_epoch()
+    for j in judges:
+        j.partial(*views[j.band])
+    for epoch, step in ((2 * e - 1, "merge_peers"), (2 * e, "select")):
+        for j in judges:
+            j.signal(epoch, 1)
+        for j in judges:
+            j.signal(epoch, 2)
+        for j in judges:
+            getattr(j, step)()
 
 
 def emulate_band_exchange(judges) -> None:

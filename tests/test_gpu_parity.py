@@ -351,7 +351,8 @@ def _band_view(vol_t, halo_t, shape, pitch, nbands, band, seed):
     return v, h
 
 
-def _run_bands(vol_t, halo_t, shape, pitch, codes, temporal, nbands, rows_only=False, replicated=False):
+def _run_bands(vol_t, halo_t, shape, pitch, codes, temporal, nbands, rows_only=False, replicated=False,
+               peer=False):
     """All bands of a band-sharded judge on one GPU, one after another; the
     rank exchange (reduce-scatter, all-to-all, all-gather) is emulated with
     torch ops (shard.emulate_band_exchange) -- no rank waits on another.
@@ -360,14 +361,23 @@ def _run_bands(vol_t, halo_t, shape, pitch, codes, temporal, nbands, rows_only=F
     import torch
     from paper_2310_09467_b200 import _lib
     from paper_2310_09467_b200.device import BandJudge
-    from paper_2310_09467_b200.shard import emulate_band_exchange
-    judges = [BandJudge(shape, pitch, codes, temporal, halo_t is not None, b, nbands)
-              for b in range(nbands)]
+    from paper_2310_09467_b200.shard import emulate_band_exchange, emulate_band_peer_exchange
+    judges = [BandJudge(shape, pitch, codes, temporal, halo_t is not None, b, nbands,
+                        exchange="peer" if peer else "nccl") for b in range(nbands)]
     views = [(_band_view(vol_t, halo_t, shape, pitch, nbands, b, 100 + b) if rows_only
               else (vol_t, halo_t)) for b in range(nbands)]
+    j0 = judges[0]
+    if peer:   # partials, pull-merge-push over (same-device) peer pointers, flag barriers
+        emulate_band_peer_exchange(judges, views)
+        ent, sel = j0.ent, j0.sel
+        for j in judges[1:]:
+            assert torch.equal(j.sel, sel)
+            assert torch.equal(j.ent.nan_to_num(-1.0), ent.nan_to_num(-1.0))
+        streams = [j.emit(*views[j.band]).clone() for j in judges]
+        torch.cuda.synchronize()
+        return ent.cpu().numpy(), sel.cpu().numpy(), torch.cat(streams, dim=1).cpu().numpy()
     for j in judges:
         j.partial(*views[j.band])
-    j0 = judges[0]
     if replicated:
         n = j0.nslots
         total = sum(j.hist[:n] for j in judges[1:]) + j0.hist[:n]
@@ -397,8 +407,9 @@ def _run_bands(vol_t, halo_t, shape, pitch, codes, temporal, nbands, rows_only=F
     # off the 8-pixel granule of a pixel-granular split (tools/stress_bands.py)
     ((3, 187, 8), (17, 22), False, 2), ((1, 18, 20), (14, 13), True, 7),
     ((2, 108, 34), (9, 13), True, 7), ((3, 248, 9), (12, 4), True, 6)])
-@pytest.mark.parametrize("rows_only,replicated", [(False, False), (True, False), (False, True)])
-def test_band_sharded_judge_equals_whole_frames(shape, pitch, halo, nbands, rows_only, replicated):
+@pytest.mark.parametrize("rows_only,replicated,peer", [(False, False, False), (True, False, False),
+                                                     (False, True, False), (True, False, True)])
+def test_band_sharded_judge_equals_whole_frames(shape, pitch, halo, nbands, rows_only, replicated, peer):
     """pcbz_judge_band_device x nbands + the owner-computes merge (or the
     replicated merge) == pcbz_judge_device, bit for bit (entropies, modes),
     and the concatenated band streams == whole streams."""
@@ -413,7 +424,8 @@ def test_band_sharded_judge_equals_whole_frames(shape, pitch, halo, nbands, rows
     codes = list(range(13)) + [0x80 | i for i in range(13)]
     whole = DeviceJudge(shape, pitch, codes, temporal=True)
     e0, s0, st0 = (x.cpu().numpy() for x in whole(frames, halo_t))
-    ent, sel, streams = _run_bands(frames, halo_t, shape, pitch, codes, True, nbands, rows_only, replicated)
+    ent, sel, streams = _run_bands(frames, halo_t, shape, pitch, codes, True, nbands, rows_only, replicated,
+                                   peer)
     assert np.array_equal(ent, e0, equal_nan=True)
     assert np.array_equal(sel, s0)
     assert np.array_equal(streams, st0)

@@ -22,7 +22,7 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 from paper_2310_09467_b200.device import BandJudge, DeviceJudge  # noqa: E402
-from paper_2310_09467_b200.shard import emulate_band_exchange  # noqa: E402
+from paper_2310_09467_b200.shard import emulate_band_exchange, emulate_band_peer_exchange  # noqa: E402
 
 
 def timed(fn, steps):
@@ -68,6 +68,17 @@ def main():
         t_emit = max(timed(lambda j=j: j.emit(frames), steps) for j in judges)
         per_rank = max(part) + t_merge + t_select + t_emit
         q = judges[0].q
+        # the peer exchange: each owner pulls its slots' rows from every band
+        # and pushes the entropies (pcbz_judge_merge_peers_device); here the
+        # "peers" are buffers on this GPU, so the pull reads local HBM where
+        # a real rank reads (n-1)/n of it over NVLink (reported in bytes)
+        peers = [BandJudge((F, H, W), pitch, wl.codes, wl.temporal, False, b, n, exchange="peer")
+                 for b in range(n)]
+        emulate_band_peer_exchange(peers, [(frames, None)] * n)
+        if not all(torch.equal(j.sel, sel_ref) for j in peers):
+            raise RuntimeError(f"peer-exchange modes differ from the whole-frame judge (N={n})")
+        t_merge_peers = max(timed(lambda j=j: j.merge_peers(), steps) for j in peers)
+        t_signal = timed(lambda: (peers[0].signal(2, 1), peers[0].signal(2, 2)), steps)   # already met: launch cost
         print(json.dumps({
             "workload": name, "bands": n, "segments_per_band": judges[0].segments,
             "partial_ms_per_band": part, "merge_owned_ms_max_rank": t_merge, "select_ms": t_select,
@@ -76,6 +87,10 @@ def main():
             "reduce_scatter_bytes_sent_per_rank": (n - 1) * q * 65536 * 4,
             "all_to_all_bytes_sent_per_rank": (n - 1) * q * judges[0].segments * 512 * 2,
             "all_gather_bytes_per_rank": q * 8,
+            "merge_peers_ms_max_rank": t_merge_peers,
+            "peer_signal_pair_ms": t_signal,
+            "peer_pull_bytes_remote_per_rank": (n - 1) * q * (65536 * 4 + judges[0].segments * 512 * 2),
+            "per_rank_compute_ms_peer_exchange": max(part) + t_merge_peers + 2 * t_signal + t_select + t_emit,
             "GBps_raw_excluding_collective": raw / (per_rank * 1e-3) / 1e9}), flush=True)
 
 

@@ -1,6 +1,7 @@
 """Randomised parity stress of the band-sharded judge: random
 frame shapes, pitches, value kinds, band counts, halo / no halo, band views
-whose rows outside the band are garbage, owner-computes or replicated merge.
+whose rows outside the band are garbage, owner-computes (collective or
+peer-memory exchange) or replicated merge.
 Every case must equal the whole-frame device judge bit for bit (entropies,
 selections, concatenated band streams) and, for the selections and streams,
 the oracle.  Runs on one GPU with the rank exchange emulated
@@ -38,7 +39,8 @@ def main():
         nb = int(rng.integers(1, 9))
         halo = bool(rng.integers(0, 2))
         rows_only = bool(rng.integers(0, 2))
-        replicated = bool(rng.integers(0, 4) == 0)
+        merge = int(rng.integers(0, 4))          # 0 replicated, 1 owner-computes (NCCL form), 2-3 peer
+        replicated, peer = merge == 0, merge >= 2
         kind = str(rng.choice(["smooth", "full", "narrow", "const"]))
         vol = np.stack([frame(rng, H, W, kind) for _ in range(F + 1)])
         if only and t not in only:
@@ -48,7 +50,7 @@ def main():
         whole = DeviceJudge((F, H, W), (px, py), codes, temporal=True)
         e0, s0, st0 = (x.cpu().numpy() for x in whole(frames, halo_t))
         ent, sel, streams = _run_bands(frames, halo_t, (F, H, W), (px, py), codes, True, nb,
-                                       rows_only, replicated)
+                                       rows_only, replicated, peer)
         why = []
         if not np.array_equal(ent, e0, equal_nan=True):
             d = np.argwhere(~((ent == e0) | (np.isnan(ent) & np.isnan(e0))))
@@ -74,7 +76,7 @@ def main():
         if why:
             bad += 1
             print(f"MISMATCH case {t}: F={F} {H}x{W} pitch {px}x{py} {kind} bands {nb} halo {halo} "
-                  f"rows_only {rows_only} replicated {replicated}: " + "; ".join(why), flush=True)
+                  f"rows_only {rows_only} merge {('replicated', 'owner', 'peer', 'peer')[merge]}: " + "; ".join(why), flush=True)
     print(f"{cases} band cases, {bad} mismatches", flush=True)
     return 1 if bad else 0
 
