@@ -603,3 +603,34 @@ def test_candidate_entropy():
         oracle.bwt_pair_hist(np.frombuffer(oracle.pack_symbols(const), np.uint8)), 7)
     with pytest.raises(TypeError):
         criterion.candidate_entropy(np.zeros((2, 2), np.int32))
+
+
+def test_band_peer_exchange_symmetric_memory_one_rank():
+    """The multi-process form of the peer exchange (buffers in
+    torch.distributed._symmetric_memory, peer pointers from the rendezvous)
+    on a one-rank NCCL group: equals the whole-frame judge bit for bit."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    from paper_2310_09467_b200.device import BandJudge, DeviceJudge
+    F, H, W, pitch = 2, 96, 128, (15, 15)
+    vol = generate_array(SynthParams(W, H, 15, 15, mode="smooth_lenslet", noise_sigma=20.0,
+                                     photon_scale=0.05, frames=F, drift=1.0, seed=8))
+    frames = torch.from_numpy(vol).cuda()
+    codes = list(range(13)) + [0x80 | i for i in range(13)]
+    e0, s0, st0 = (x.cpu().numpy() for x in DeviceJudge((F, H, W), pitch, codes, temporal=True)(frames))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        bj = BandJudge((F, H, W), pitch, codes, True, False, 0, 1, exchange="peer", group=dist.group.WORLD)
+        for _ in range(2):   # two epochs through the barriers
+            ent, sel, stream = (x.cpu().numpy() for x in bj(frames))
+            assert np.array_equal(ent, e0, equal_nan=True)
+            assert np.array_equal(sel, s0)
+            assert np.array_equal(stream, st0)
+    finally:
+        dist.destroy_process_group()
