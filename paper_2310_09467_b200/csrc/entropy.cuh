@@ -39,8 +39,10 @@ constexpr int kNpNodeMax = 2048;   // <= 1024 leaves (>= 64 terms each once n > 
 constexpr int kNpLevelMax = 16;
 constexpr uint32_t kNpLeaf = 0xFFFFFFFFu;
 
-struct NpScratch {
-  uint32_t off[kEntropyThreads + 1];  // compacted index of each thread's first term
+// scratch of a block of NT threads
+template <int NT>
+struct NpScratchT {
+  uint32_t off[NT + 1];               // compacted index of each thread's first term
   uint32_t occ[kOccWords];            // occupancy bitmap
   uint32_t node_beg[kNpNodeMax];
   uint32_t node_len[kNpNodeMax];
@@ -49,11 +51,15 @@ struct NpScratch {
   uint32_t level_start[kNpLevelMax + 1];
   int nlevels;
 };
+using NpScratch = NpScratchT<kEntropyThreads>;
 
-__device__ __forceinline__ int occ_word_lo(int t) { return (kOccWords * t) / kEntropyThreads; }
+// first occupancy word of thread t's run (a block of NT threads)
+template <int NT>
+__device__ __forceinline__ int occ_word_lo(int t) { return (kOccWords * t) / NT; }
 
 // Breadth-first recursion tree of numpy's pairwise sum over n terms; one warp.
-__device__ inline void np_build_tree(uint32_t n, NpScratch &S) {
+template <typename Scratch>
+__device__ inline void np_build_tree(uint32_t n, Scratch &S) {
   const int lane = threadIdx.x & 31;
   if (lane == 0) {
     S.node_beg[0] = 0;
@@ -111,14 +117,15 @@ __device__ __forceinline__ double np_term(double c, double total) {
 // log2 is not correctly rounded; the device's log2 differs from it in the
 // last ulp for ~0.02 % of arguments).
 
-// `get(bin)` returns the bin count (integer; 0 = empty); all threads of the
-// block (kEntropyThreads) must call this.  `terms` may be null.
+// `get(bin)` returns the bin count (integer; 0 = empty); all NT threads of
+// the block must call this.  `terms` may be null.
 // If occ_ready, the caller has already filled S.occ (bit j of word w = bin
 // 32w + j occupied) and synchronised.
-template <typename Get>
-__device__ double block_entropy(Get get, double total, NpScratch &S, const double *terms,
-                                bool occ_ready = false, int64_t nterms = kTermTable,
-                                uint64_t *stamps = nullptr) {
+template <int NT, typename Get>
+__device__ double block_entropy_n(Get get, double total, NpScratchT<NT> &S, const double *terms,
+                                  bool occ_ready = false, int64_t nterms = kTermTable,
+                                  uint64_t *stamps = nullptr) {
+  static_assert(NT % 32 == 0 && NT >= 64, "whole warps");
   const int t = threadIdx.x;
   auto stamp = [&](int i) {  // phase timestamps for profiling (PCBZ_TRACE_WORDS = 9)
     if (stamps && t == 0) {
@@ -132,7 +139,7 @@ __device__ double block_entropy(Get get, double total, NpScratch &S, const doubl
   if (!occ_ready) {
     // four words per warp step: their count reads are independent
     const int lane = t & 31;
-    constexpr int kStep = kEntropyThreads / 32;
+    constexpr int kStep = NT / 32;
     for (int w0 = t >> 5; w0 < kOccWords; w0 += 4 * kStep) {
       bool occ[4];
 #pragma unroll
@@ -150,7 +157,7 @@ __device__ double block_entropy(Get get, double total, NpScratch &S, const doubl
   }
   __syncthreads();
   stamp(0);
-  const int w_lo = occ_word_lo(t), w_hi = occ_word_lo(t + 1);
+  const int w_lo = occ_word_lo<NT>(t), w_hi = occ_word_lo<NT>(t + 1);
   uint32_t cnt = 0;
   for (int w = w_lo; w < w_hi; ++w) cnt += __popc(S.occ[w]);
   uint32_t incl = cnt;
@@ -163,14 +170,14 @@ __device__ double block_entropy(Get get, double total, NpScratch &S, const doubl
   if ((t & 31) == 31) S.off[t >> 5] = incl;  // warp totals, temporarily
   __syncthreads();
   uint32_t base = 0, n_all = 0;
-  for (int w = 0; w < kEntropyThreads / 32; ++w) {
+  for (int w = 0; w < NT / 32; ++w) {
     const uint32_t v = S.off[w];
     if (w < (t >> 5)) base += v;
     n_all += v;
   }
   __syncthreads();
   S.off[t] = base + incl - cnt;
-  if (t == 0) S.off[kEntropyThreads] = n_all;
+  if (t == 0) S.off[NT] = n_all;
   if (n_all == 0 || !(total > 0.0)) {
     __syncthreads();
     return 0.0;
@@ -190,15 +197,15 @@ __device__ double block_entropy(Get get, double total, NpScratch &S, const doubl
     return in ? v : np_term((double)c, total);
   };
   // ---- leaves ---------------------------------------------------------------
-  for (int j = t; j < nodes; j += kEntropyThreads) {
+  for (int j = t; j < nodes; j += NT) {
     if (S.node_child[j] != kNpLeaf) continue;
     const uint32_t beg = S.node_beg[j], len = S.node_len[j];
-    int r0 = 0, r1 = kEntropyThreads - 1;  // last thread range with off <= beg
+    int r0 = 0, r1 = NT - 1;  // last thread range with off <= beg
     while (r0 < r1) {
       const int mid = (r0 + r1 + 1) >> 1;
       if (S.off[mid] <= beg) r0 = mid; else r1 = mid - 1;
     }
-    int w = occ_word_lo(r0);
+    int w = occ_word_lo<NT>(r0);
     uint32_t idx = S.off[r0];
     uint32_t bits = S.occ[w];
     while (idx + __popc(bits) <= beg) {
@@ -249,7 +256,7 @@ __device__ double block_entropy(Get get, double total, NpScratch &S, const doubl
   stamp(3);
   // ---- internal nodes, deepest level first ----------------------------------
   for (int L = S.nlevels - 2; L >= 0; --L) {
-    for (int j = (int)S.level_start[L] + t; j < (int)S.level_start[L + 1]; j += kEntropyThreads) {
+    for (int j = (int)S.level_start[L] + t; j < (int)S.level_start[L + 1]; j += NT) {
       const uint32_t c = S.node_child[j];
       if (c != kNpLeaf) S.node_sum[j] = __dadd_rn(S.node_sum[c], S.node_sum[c + 1]);
     }
@@ -258,6 +265,14 @@ __device__ double block_entropy(Get get, double total, NpScratch &S, const doubl
   const double e = -S.node_sum[0];
   __syncthreads();
   return e;
+}
+
+// the judge kernel's shape (kEntropyThreads)
+template <typename Get>
+__device__ __forceinline__ double block_entropy(Get get, double total, NpScratch &S, const double *terms,
+                                                bool occ_ready = false, int64_t nterms = kTermTable,
+                                                uint64_t *stamps = nullptr) {
+  return block_entropy_n<kEntropyThreads>(get, total, S, terms, occ_ready, nterms, stamps);
 }
 
 }  // namespace pcbz

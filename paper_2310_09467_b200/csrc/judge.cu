@@ -8,13 +8,21 @@ namespace pcbz {
 // cross-segment stitch + bucket seams + entropy (one CTA per pair)
 // ---------------------------------------------------------------------------
 
-constexpr size_t kFinalizeSmemBytes = 65536 * sizeof(uint16_t) + sizeof(NpScratch) + 2048;
+// one CTA of kFinalizeThreads per stream: only one finalize CTA fits an SM
+// (128 KiB of staged counts), so it takes 4x the judge's 192 threads -- the
+// numpy-order leaves and the staging pass run wider (profiles/r02_notes.md)
+#ifndef PCBZ_FINALIZE_THREADS
+#define PCBZ_FINALIZE_THREADS 768
+#endif
+constexpr int kFinalizeThreads = PCBZ_FINALIZE_THREADS;
+using FinScratch = NpScratchT<kFinalizeThreads>;
+constexpr size_t kFinalizeSmemBytes = 65536 * sizeof(uint16_t) + sizeof(FinScratch) + 2048;
 
-__global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(const JudgeParams P) {
+__global__ void __launch_bounds__(kFinalizeThreads, 1) judge_finalize_kernel(const JudgeParams P) {
   extern __shared__ uint4 smem_raw[];
   uint16_t *c16 = reinterpret_cast<uint16_t *>(smem_raw);
-  NpScratch &scr = *reinterpret_cast<NpScratch *>(c16 + 65536);
-  int *s_first = reinterpret_cast<int *>(reinterpret_cast<char *>(&scr) + sizeof(NpScratch));
+  FinScratch &scr = *reinterpret_cast<FinScratch *>(c16 + 65536);
+  int *s_first = reinterpret_cast<int *>(reinterpret_cast<char *>(&scr) + sizeof(FinScratch));
   int *s_last = s_first + 256;
   // per-pair mode: block = pair; slot mode (owner-computes band merge):
   // block = slot - slot0 of this rank's slots, whose histograms, summaries
@@ -40,7 +48,7 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
     // the reduce-scatter, fused: this owner pulls its slot's row from every
     // band's partial histograms over peer memory and sums it in place
     uint4 *G4w = reinterpret_cast<uint4 *>(G);
-    for (int i = threadIdx.x; i < 16384; i += kEntropyThreads) {
+    for (int i = threadIdx.x; i < 16384; i += kFinalizeThreads) {
       uint4 acc = make_uint4(0, 0, 0, 0);
       for (int b = 0; b < P.nbands; ++b) {
         const uint4 v = __ldcv(reinterpret_cast<const uint4 *>(P.peer_hist[b]) + (size_t)slot * 16384 + i);
@@ -60,11 +68,11 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
     for (int b = 0; b < P.nbands; ++b) {
       if (P.peer_summ) {   // every band's summaries of this slot, over peer memory
         const uint4 *src = reinterpret_cast<const uint4 *>(P.peer_summ[b]) + (size_t)slot * P.S * 64;
-        for (int i = threadIdx.x; i < P.S * 64; i += kEntropyThreads) dst[b * P.S * 64 + i] = __ldcv(src + i);
+        for (int i = threadIdx.x; i < P.S * 64; i += kFinalizeThreads) dst[b * P.S * 64 + i] = __ldcv(src + i);
       } else {
         const uint4 *src = reinterpret_cast<const uint4 *>(
             P.segsum + ((size_t)b * P.nslots + lslot) * P.S * 512);
-        for (int i = threadIdx.x; i < P.S * 64; i += kEntropyThreads) dst[b * P.S * 64 + i] = __ldcg(src + i);
+        for (int i = threadIdx.x; i < P.S * 64; i += kFinalizeThreads) dst[b * P.S * 64 + i] = __ldcg(src + i);
       }
     }
     __syncthreads();
@@ -75,7 +83,7 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
     if (P.peer_summ) return reinterpret_cast<const int16_t *>(P.peer_summ[b]) + ((size_t)slot * P.S + s) * 512;
     return P.segsum + (((size_t)b * P.nslots + lslot) * P.S + s) * 512;
   };
-  for (int v = threadIdx.x; v < 256; v += kEntropyThreads) {
+  for (int v = threadIdx.x; v < 256; v += kFinalizeThreads) {
     int carried = -1, first = -1;
     for (int g = 0; g < nseg; ++g) {
       const int16_t *sum = seg_sum(g);
@@ -102,7 +110,7 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
   // stage saturated u16 copies of the counts in shared memory (16-byte loads,
   // eight in flight per thread before any store: the loop is latency bound)
   // and build the occupancy bitmap on the way: 4 bins per thread, 8 lanes
-  // per 32-bin word OR their nibbles together.  192 threads = 24 words per
+  // per 32-bin word OR their nibbles together.  kFinalizeThreads / 8 words per
   // pass, so each word's eight lanes are in one warp.
   {
     const uint4 *G4 = reinterpret_cast<const uint4 *>(G);
@@ -110,16 +118,16 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
     auto sat = [](uint32_t c) -> uint32_t { return c < 0xFFFFu ? c : 0xFFFFu; };
     constexpr int kUnroll = 8;
     const int lane = threadIdx.x & 31;
-    for (int b0 = threadIdx.x; b0 < 16384; b0 += kEntropyThreads * kUnroll) {
+    for (int b0 = threadIdx.x; b0 < 16384; b0 += kFinalizeThreads * kUnroll) {
       uint4 v[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
-        const int b = b0 + u * kEntropyThreads;
+        const int b = b0 + u * kFinalizeThreads;
         v[u] = b < 16384 ? __ldcg(G4 + b) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
-        const int b = b0 + u * kEntropyThreads;
+        const int b = b0 + u * kFinalizeThreads;
         if (b < 16384)
           c4[b] = make_uint2(sat(v[u].x) | (sat(v[u].y) << 16), sat(v[u].z) | (sat(v[u].w) << 16));
         uint32_t nib = (v[u].x != 0) | (v[u].y != 0) << 1 | (v[u].z != 0) << 2 | (v[u].w != 0) << 3;
@@ -136,7 +144,8 @@ __global__ void __launch_bounds__(kEntropyThreads, 1) judge_finalize_kernel(cons
     const uint32_t c = c16[bin];
     return c < 0xFFFFu ? c : __ldcg(G + bin);
   };
-  const double e = block_entropy(get, (double)(2 * P.npix - 1), scr, P.terms, true, P.nterms);
+  const double e = block_entropy_n<kFinalizeThreads>(get, (double)(2 * P.npix - 1), scr, P.terms, true,
+                                                      P.nterms);
   if (threadIdx.x == 0) P.ent[lslot] = e;
   // the all-gather, fused: the entropy goes straight into every rank's table
   if (P.peer_ent && threadIdx.x < P.nbands) reinterpret_cast<double *>(P.peer_ent[threadIdx.x])[slot] = e;
@@ -287,7 +296,7 @@ cudaError_t launch_emit_any(const EmitParams &p, cudaStream_t st) {
 }
 
 cudaError_t launch_finalize(const JudgeParams &p, cudaStream_t st) {
-  judge_finalize_kernel<<<(unsigned)p.npairs, kEntropyThreads, kFinalizeSmemBytes, st>>>(p);
+  judge_finalize_kernel<<<(unsigned)p.npairs, kFinalizeThreads, kFinalizeSmemBytes, st>>>(p);
   return cudaGetLastError();
 }
 
@@ -298,7 +307,7 @@ cudaError_t launch_reduce_parts(const JudgeParams &p, cudaStream_t st) {
 
 cudaError_t launch_finalize_slots(const JudgeParams &p, cudaStream_t st) {
   if (p.slot_count <= 0) return cudaSuccess;
-  judge_finalize_kernel<<<(unsigned)p.slot_count, kEntropyThreads, kFinalizeSmemBytes, st>>>(p);
+  judge_finalize_kernel<<<(unsigned)p.slot_count, kFinalizeThreads, kFinalizeSmemBytes, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -1,8 +1,11 @@
 // judge_px.cu -- one instantiation of the histogram kernel (and the chunked
 // emission kernel) per fast-path pitch.  build_native.py compiles this file
 // once per PCBZ_PX in [0, kMaxFastPitch] (0 = generic path), in parallel.
-// PCBZ_STUB=1 builds an empty placeholder (experimental variant builds that
-// only need some pitches); the host never selects a stubbed pitch there.
+// PCBZ_STUB=1 builds a placeholder (experimental variant builds that only
+// need some pitches) that aborts if a call selects its pitch.
+#include <cstdio>
+#include <cstdlib>
+
 #include "judge_kernel.cuh"
 
 #ifndef PCBZ_PX
@@ -19,8 +22,14 @@ namespace pcbz {
 
 #if PCBZ_STUB
 cudaError_t PCBZ_CAT(judge_configure_px, PCBZ_PX)() { return cudaSuccess; }
-void PCBZ_CAT(judge_launch_px, PCBZ_PX)(const JudgeParams &, int, cudaStream_t) {}
-void PCBZ_CAT(emit_launch_px, PCBZ_PX)(const EmitParams &, int, cudaStream_t) {}
+void PCBZ_CAT(judge_launch_px, PCBZ_PX)(const JudgeParams &, int, cudaStream_t) {
+  fprintf(stderr, "pcbz: pitch %d is a stub in this experimental build\n", PCBZ_PX);
+  abort();
+}
+void PCBZ_CAT(emit_launch_px, PCBZ_PX)(const EmitParams &, int, cudaStream_t) {
+  fprintf(stderr, "pcbz: pitch %d is a stub in this experimental build\n", PCBZ_PX);
+  abort();
+}
 #else
 cudaError_t PCBZ_CAT(judge_configure_px, PCBZ_PX)() {
   return cudaFuncSetAttribute(judge_hist_kernel<PCBZ_PX>,

@@ -23,6 +23,10 @@ VARIANTS = {
     "emit_chunks": ("PCBZ_EMIT_RUNS=0",),
     "trace5": ("PCBZ_TRACE_WORDS=5",),
     "trace9": ("PCBZ_TRACE_WORDS=9",),
+    "fin192": ("PCBZ_FINALIZE_THREADS=192",),
+    "fin384": ("PCBZ_FINALIZE_THREADS=384",),
+    "fin512": ("PCBZ_FINALIZE_THREADS=512",),
+    "fin768": ("PCBZ_FINALIZE_THREADS=768",),
 }
 
 def build_from_git(rev: str, name: str):
@@ -47,4 +51,8 @@ if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
     for n in names:
         out = ROOT / "paper_2310_09467_b200" / "_native" / "variants" / n
-        print(n, build_native.build_library(force=True, defines=VARIANTS[n], out_dir=out, pitches={15}), flush=True)
+        # VARIANT_PITCHES=13,15: fast-path pitches to instantiate (others abort if selected)
+        import os
+        pitches = {int(x) for x in os.environ.get("VARIANT_PITCHES", "15").split(",")}
+        print(n, build_native.build_library(force=True, defines=VARIANTS[n], out_dir=out, pitches=pitches),
+              flush=True)
