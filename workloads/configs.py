@@ -7,8 +7,8 @@ shared by bench.py and the full-size parity tests.
       photon 0.05; 33 low: amp 3000 sigma 500 photon 0.01), seeds 0..99,
       13 intra candidates
   c3  2048x2048 smooth_lenslet series (amp 20000, sigma 20, photon 0.05,
-      drift 1), pitch 15, temporal on (26 candidates from frame 1); the
-      bench uses a 100-frame prefix of the 1000-frame series
+      drift 1), pitch 15, temporal on (26 candidates from frame 1); "c3" is
+      a 100-frame prefix of the 1000-frame series, "c3full" all of it
   c4  4096x4096 pitch-13 smooth_lenslet series, 26 candidates
 
 Frames are bit-identical to the reference's synth.generate
@@ -53,6 +53,9 @@ WORKLOADS = {
     "c3": Workload("c3", "C3 prefix: 100-frame 2048x2048 smooth_lenslet series, pitch 15x15, drift 1, "
                    "temporal on (26 candidates from frame 1), frames sharded over ranks with a 1-frame halo",
                    100, 2048, 2048, 15, ALL26, True, True),
+    "c3full": Workload("c3full", "C3: the full 1000-frame 2048x2048 smooth_lenslet series (8.4 GB), pitch "
+                       "15x15, drift 1, temporal on (26 candidates from frame 1), frames sharded over ranks "
+                       "with a 1-frame halo", 1000, 2048, 2048, 15, ALL26, True, True),
     "c4": Workload("c4", "C4: 8-frame 4096x4096 smooth_lenslet series, pitch 13x13, drift 1, temporal on "
                    "(26 candidates), frames sharded over ranks with a 1-frame halo",
                    8, 4096, 4096, 13, ALL26, True, True),
