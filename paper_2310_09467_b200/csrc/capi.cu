@@ -577,17 +577,18 @@ int pcbz_judge_device(const uint16_t *d_frames, const uint16_t *d_halo_prev, int
 }
 
 // Frame counts of the pipeline chunks of pcbz_judge_host: uploads of chunk
-// i+1, the judge of chunk i and downloads of chunk i-1 overlap on three
-// streams, so the first upload and the last download are exposed.  Base
-// chunks of ~n/10 frames (>= 8) measured best on C2 (4/6/8/10/13 frames:
-// 25.4/32.6/35.8/36.6/35.2 GB/s e2e, profiles/r01_notes.md).  Optional
-// ramps (PCBZ_HOST_RAMP / PCBZ_HOST_RAMP_DOWN: doubling from that many frames
-// at the start / halving to it at the end) shorten the exposed ends;
-// PCBZ_HOST_CHUNK forces the base size.
-// Fewer than 16 frames: one chunk, unless the volume is large (>= 128 MB)
-// -- then chunks of ~32 MB of frames, i.e. one 4096^2 frame (C4, 8 frames:
-// e2e 13.3 -> 22.0 GB/s; 2 / 3 / 4-frame chunks 19.5 / 17.9 / 15.6).
-std::vector<int64_t> host_chunks(int64_t nframes, int64_t frame_bytes) {
+// i+1, the judge of chunk i and downloads of chunk i-1 overlap, so the first
+// upload and the last download are exposed.  A chunk holds ~135 items
+// (frames x candidates x segments of the call's plan, about one wave of the
+// persistent grid): C2 (13 items / frame) 10 frames, C3 (26) 5, C4 (26 x 8
+// segments) 1 -- measured e2e, frames per chunk: C2 9 / 10 / 11 / 12 ->
+// 39.0 / 39.1 / 38.0 / 37.7 GB/s; C3 4 / 5 / 6 / 7 / 10 -> 22.0 / 23.1 /
+// 23.4 / 23.1 / 22.5; C4 1 / 2 / 3 / 4 / 8 -> 22.0 / 19.5 / 17.9 / 15.6 /
+// 13.3 (profiles/r02_notes.md).  Volumes under 128 MB (PCBZ_HOST_BIG_MB)
+// stay one chunk.  Optional ramps (PCBZ_HOST_RAMP / PCBZ_HOST_RAMP_DOWN: doubling
+// from that many frames at the start / halving to it at the end) shorten the
+// exposed ends; PCBZ_HOST_CHUNK forces the base size.
+std::vector<int64_t> host_chunks(int64_t nframes, int64_t frame_bytes, int64_t items_per_frame) {
   auto env = [](const char *name) -> int64_t {
     const char *e = getenv(name);
     return e ? atoll(e) : 0;
@@ -599,14 +600,10 @@ std::vector<int64_t> host_chunks(int64_t nframes, int64_t frame_bytes) {
     const char *e = getenv("PCBZ_HOST_BIG_MB");
     return (int64_t)(e ? atoll(e) : 128) << 20;
   }();
-  if (nframes < 16 && forced <= 0) {
-    if (nframes < 2 || nframes * frame_bytes < big) return {nframes};  // too little to pay for a pipeline
-    std::vector<int64_t> out;
-    const int64_t c = std::max<int64_t>(1, ((int64_t)32 << 20) / std::max<int64_t>(frame_bytes, 1));
-    for (int64_t left = nframes; left > 0; left -= c) out.push_back(std::min(c, left));
-    return out;
-  }
-  const int64_t base = forced > 0 ? std::min(forced, nframes) : std::max<int64_t>(8, (nframes + 9) / 10);
+  if (forced <= 0 && (nframes < 2 || nframes * frame_bytes < big))
+    return {nframes};  // too little to pay for a pipeline
+  const int64_t per_chunk = (135 + std::max<int64_t>(items_per_frame, 1) / 2) / std::max<int64_t>(items_per_frame, 1);
+  const int64_t base = std::min(nframes, forced > 0 ? forced : std::max<int64_t>(1, per_chunk));
   std::vector<int64_t> head, tail, out;
   int64_t left = nframes;
   for (int64_t c = ramp; c > 0 && c < base && left >= 4 * c; c *= 2) {
@@ -638,7 +635,7 @@ int pcbz_judge_host(const uint16_t *frames, const uint16_t *halo_prev, int64_t n
   if (rc) return rc;
   const int64_t npix = h * w;
   const size_t fbytes = (size_t)nframes * npix * 2;
-  const std::vector<int64_t> sizes = host_chunks(nframes, npix * 2);
+  const std::vector<int64_t> sizes = host_chunks(nframes, npix * 2, (int64_t)k * full.jp.S);
   const int64_t nchunks = (int64_t)sizes.size();
   std::vector<int64_t> starts(nchunks + 1, 0);
   for (int64_t i = 0; i < nchunks; ++i) starts[i + 1] = starts[i] + sizes[i];
