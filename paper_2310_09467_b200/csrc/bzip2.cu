@@ -9,9 +9,9 @@
 //                        (scan), libbz2's greedy block split (binary search
 //                        per job), bytes, block CRCs (GF(2)-linear, chunked),
 //                        used-symbol maps
-//   B  prefix doubling   cyclic-rotation sort of every block at once: CUB
-//                        radix sorts of (group, partner rank) keys over the
-//                        shrinking set of unresolved groups
+//   B  prefix doubling   cyclic-rotation sort of every block at once: radix
+//                        sorts (radix_sort.cuh) of (group, partner rank) keys
+//                        over the shrinking set of unresolved groups
 //   C  mtf_kernel        one thread per block: BWT column, MTF, RUNA/RUNB
 //   D  tables_kernel     one CTA per block: initial tables, four refinement
 //                        passes (parallel over 50-symbol groups), huffman.c
@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "../../include/pcbz_b200.h"
+#include "radix_sort.cuh"
 
 namespace pcbz {
 namespace bz {
@@ -977,7 +978,7 @@ struct Scratch {  // grow-only device buffers, one set per host thread
     void *p = nullptr;
     size_t cap = 0;
   };
-  Buf b[40];
+  Buf b[44];
   template <typename T>
   int get(int slot, size_t count, T **out) {
     Buf &x = b[slot];
@@ -1018,11 +1019,18 @@ int sort_rotations(Block *d_blocks, const int *d_ids, int nb, int nslots, const 
       (rc = g_scr.get(11, N, &gs)) || (rc = g_scr.get(12, N, &keys_a)) || (rc = g_scr.get(13, N, &keys_b)) ||
       (rc = g_scr.get(14, N, &hd)) || (rc = g_scr.get(15, N, &unres)) || (rc = g_scr.get(16, 1, &d_nsel)))
     return rc;
-  size_t t_sort = 0, t_scan = 0, t_sel = 0;
-  BZ_TRY(cub::DeviceRadixSort::SortPairs(nullptr, t_sort, keys_a, keys_b, vals_a, vals_b, N, 0, 64, st));
+  uint32_t *rs_totals, *rs_ctr;
+  unsigned long long *rs_status, *rs_mask;
+  if ((rc = g_scr.get(39, (size_t)256 * rsort::tiles_of(N), &rs_status)) ||
+      (rc = g_scr.get(40, 8 * 256, &rs_totals)) || (rc = g_scr.get(41, 1, &rs_mask)) ||
+      (rc = g_scr.get(42, 8, &rs_ctr)))
+    return rc;
+  uint64_t *ks;   // the sorted pairs: keys_b / vals_b or keys_a / vals_a
+  uint32_t *vs;
+  size_t t_scan = 0, t_sel = 0;
   BZ_TRY(cub::DeviceScan::InclusiveScan(nullptr, t_scan, gs, gs, MaxOp(), N, st));
   BZ_TRY(cub::DeviceSelect::Flagged(nullptr, t_sel, U, unres, U2, d_nsel, N, st));
-  const size_t t_all = std::max({t_sort, t_scan, t_sel});
+  const size_t t_all = std::max(t_scan, t_sel);
   uint8_t *d_tmp;
   if ((rc = g_scr.get(17, t_all, &d_tmp))) return rc;
   int bits_b = 1;
@@ -1033,15 +1041,16 @@ int sort_rotations(Block *d_blocks, const int *d_ids, int nb, int nslots, const 
   init_keys_kernel<<<grid_of(N), 256, 0, st>>>(d_blocks, block_of, d_rle, N, keys_a, vals_a);
   BZ_TRY(cudaGetLastError());
   size_t tb = t_all;
-  BZ_TRY(cub::DeviceRadixSort::SortPairs(d_tmp, tb, keys_a, keys_b, vals_a, vals_b, N, 0, 32 + bits_b, st));
-  heads_kernel<<<grid_of(N), 256, 0, st>>>(keys_b, N, hd);
+  BZ_TRY(rsort::sort_pairs(keys_a, vals_a, keys_b, vals_b, N, 32 + bits_b, rs_status, rs_totals, rs_ctr, rs_mask, &ks, &vs, st));
+  heads_kernel<<<grid_of(N), 256, 0, st>>>(ks, N, hd);
   head_pos_kernel<<<grid_of(N), 256, 0, st>>>(hd, nullptr, N, gs);
   tb = t_all;
   BZ_TRY(cub::DeviceScan::InclusiveScan(d_tmp, tb, gs, gs, MaxOp(), N, st));
-  settle_kernel<<<grid_of(N), 256, 0, st>>>(vals_b, nullptr, N, hd, gs, sa, rank, block_of, d_blocks, 4, unres);
-  iota_kernel<<<grid_of(N), 256, 0, st>>>(vals_a, N);
+  settle_kernel<<<grid_of(N), 256, 0, st>>>(vs, nullptr, N, hd, gs, sa, rank, block_of, d_blocks, 4, unres);
+  uint32_t *idx = vs == vals_a ? vals_b : vals_a;   // the value buffer settle_kernel does not read
+  iota_kernel<<<grid_of(N), 256, 0, st>>>(idx, N);
   tb = t_all;
-  BZ_TRY(cub::DeviceSelect::Flagged(d_tmp, tb, vals_a, unres, U, d_nsel, N, st));
+  BZ_TRY(cub::DeviceSelect::Flagged(d_tmp, tb, idx, unres, U, d_nsel, N, st));
   int h_nsel = 0;
   BZ_TRY(cudaMemcpyAsync(&h_nsel, d_nsel, sizeof(int), cudaMemcpyDeviceToHost, st));
   BZ_TRY(cudaStreamSynchronize(st));
@@ -1051,12 +1060,12 @@ int sort_rotations(Block *d_blocks, const int *d_ids, int nb, int nslots, const 
   for (uint64_t h = 4; m > 0; h *= 2) {
     pair_keys_kernel<<<grid_of(m), 256, 0, st>>>(U, m, sa, rank, block_of, d_blocks, h, keys_a, vals_a);
     tb = t_all;
-    BZ_TRY(cub::DeviceRadixSort::SortPairs(d_tmp, tb, keys_a, keys_b, vals_a, vals_b, m, 0, 32 + bits_r, st));
-    heads_kernel<<<grid_of(m), 256, 0, st>>>(keys_b, m, hd);
+    BZ_TRY(rsort::sort_pairs(keys_a, vals_a, keys_b, vals_b, m, 32 + bits_r, rs_status, rs_totals, rs_ctr, rs_mask, &ks, &vs, st));
+    heads_kernel<<<grid_of(m), 256, 0, st>>>(ks, m, hd);
     head_pos_kernel<<<grid_of(m), 256, 0, st>>>(hd, U, m, gs);
     tb = t_all;
     BZ_TRY(cub::DeviceScan::InclusiveScan(d_tmp, tb, gs, gs, MaxOp(), m, st));
-    settle_kernel<<<grid_of(m), 256, 0, st>>>(vals_b, U, m, hd, gs, sa, rank, block_of, d_blocks, 2 * h, unres);
+    settle_kernel<<<grid_of(m), 256, 0, st>>>(vs, U, m, hd, gs, sa, rank, block_of, d_blocks, 2 * h, unres);
     tb = t_all;
     BZ_TRY(cub::DeviceSelect::Flagged(d_tmp, tb, U, unres, U2, d_nsel, m, st));
     BZ_TRY(cudaMemcpyAsync(&h_nsel, d_nsel, sizeof(int), cudaMemcpyDeviceToHost, st));
