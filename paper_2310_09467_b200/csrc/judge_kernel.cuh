@@ -381,7 +381,10 @@ __global__ void __launch_bounds__(256) emit_chunks_kernel(const EmitParams P) {
 // frame, carrying the left neighbours in registers like the judge's lanes
 // (lane_fast.cuh): three row loads per chunk plus one history fill per run
 // instead of up to eight overlapping chunk loads per chunk.
-constexpr int kEmitRun = 4;
+#ifndef PCBZ_EMIT_RUN
+#define PCBZ_EMIT_RUN 2  // A/B on 100 C2 frames: 1 / 2 / 4 / 8 / 16 -> 517 / 361 / 427 / 797 / 759 us (profiles/r02_notes.md)
+#endif
+constexpr int kEmitRun = PCBZ_EMIT_RUN;
 
 template <int PX, int ID, bool TEMP>
 __device__ __forceinline__ void emit_run(const uint16_t *__restrict__ src, const uint16_t *__restrict__ prv,
@@ -441,8 +444,11 @@ __device__ __forceinline__ void emit_run_dispatch(int id, const uint16_t *src, c
 }
 
 // one thread per run of kEmitRun chunks of a frame's emitted range
+#ifndef PCBZ_EMIT_MINB
+#define PCBZ_EMIT_MINB 1
+#endif
 template <int PX>
-__global__ void __launch_bounds__(256) emit_runs_kernel(const EmitParams P) {
+__global__ void __launch_bounds__(256, PCBZ_EMIT_MINB) emit_runs_kernel(const EmitParams P) {
   const int64_t cpf = (P.pix1 - P.pix0) / 8;   // emitted chunks per frame
   const int64_t rpf = (cpf + kEmitRun - 1) / kEmitRun;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < P.nframes * rpf;

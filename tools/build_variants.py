@@ -21,6 +21,14 @@ VARIANTS = {
     "pf32": ("PCBZ_PREFETCH=32",),
     "evict_last": ("PCBZ_LDG_HINT=1",),
     "emit_chunks": ("PCBZ_EMIT_RUNS=0",),
+    "emit_run2": ("PCBZ_EMIT_RUN=2",),
+    "emit_run8": ("PCBZ_EMIT_RUN=8",),
+    "emit_run16": ("PCBZ_EMIT_RUN=16",),
+    "emit_run1": ("PCBZ_EMIT_RUN=1",),
+    "emit_run1_m8": ("PCBZ_EMIT_RUN=1", "PCBZ_EMIT_MINB=8"),
+    "emit_run2_m6": ("PCBZ_EMIT_RUN=2", "PCBZ_EMIT_MINB=6"),
+    "emit_run2_m8": ("PCBZ_EMIT_RUN=2", "PCBZ_EMIT_MINB=8"),
+    "emit_run4_m6": ("PCBZ_EMIT_RUN=4", "PCBZ_EMIT_MINB=6"),
     "trace5": ("PCBZ_TRACE_WORDS=5",),
     "trace9": ("PCBZ_TRACE_WORDS=9",),
     "fin192": ("PCBZ_FINALIZE_THREADS=192",),
