@@ -323,7 +323,10 @@ __global__ void settle_kernel(const uint32_t *vals, const uint32_t *U, uint32_t 
     const bool open = !hd[k] || (k + 1 < m && !hd[k + 1]);
     uint8_t u = 0;
     if (open) {
-      const uint32_t b = block_of[g];
+      // a block's suffix-array slots are its own position range [base, base
+      // + n) (the first sort orders by block id, ids ascend with base), so
+      // the slot's block is g's block: a sequential read, not a random one
+      const uint32_t b = block_of[slot];
       if (plen >= (uint64_t)blocks[b].n) blocks[b].tie = 1;  // equal full rotations
       else u = 1;
     }
