@@ -217,15 +217,9 @@ inline cudaError_t sort_pairs(uint64_t *ka, uint32_t *va, uint64_t *kb, uint32_t
   *kres = ka;
   *vres = va;
   if (n < 2) return cudaSuccess;
-  static bool attr = false;
-  cudaError_t e;
-  if (!attr) {
-    e = cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kScatterSmem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(hist_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 256 * kHistCopies * 4);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  // set on every call: cheap, and correct for whichever device is current
+  cudaError_t e = cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kScatterSmem);
+  if (e != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(d_mask, 0, sizeof(unsigned long long), st)) != cudaSuccess) return e;
   const int g = (int)std::min<uint32_t>((n + 255) / 256, 148u * 8u);
   vary_kernel<<<g, 256, 0, st>>>(ka, n, d_mask);
