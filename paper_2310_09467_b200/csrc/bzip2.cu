@@ -981,7 +981,7 @@ struct Scratch {  // grow-only device buffers, one set per host thread
     void *p = nullptr;
     size_t cap = 0;
   };
-  Buf b[44];
+  Buf b[48];
   template <typename T>
   int get(int slot, size_t count, T **out) {
     Buf &x = b[slot];
@@ -1011,7 +1011,8 @@ __global__ void iota_kernel(uint32_t *a, uint32_t n) {
 // Rotation sort of every block (stage B): sa[base + j] = start of the j-th
 // smallest rotation of the block; blocks[b].tie set for periodic blocks.
 int sort_rotations(Block *d_blocks, const int *d_ids, int nb, int nslots, const uint8_t *d_rle,
-                   uint32_t N, uint32_t *sa, cudaStream_t st) {
+                   uint32_t N, uint32_t *sa, const std::vector<Block> &blocks, const std::vector<int> &ids,
+                   cudaStream_t st) {
   uint32_t *block_of, *rank, *vals_a, *vals_b, *U, *U2, *gs;
   uint64_t *keys_a, *keys_b;
   uint8_t *hd, *unres;
@@ -1024,9 +1025,11 @@ int sort_rotations(Block *d_blocks, const int *d_ids, int nb, int nslots, const 
     return rc;
   uint32_t *rs_totals, *rs_ctr;
   unsigned long long *rs_status, *rs_mask;
-  if ((rc = g_scr.get(39, (size_t)256 * rsort::tiles_of(N), &rs_status)) ||
-      (rc = g_scr.get(40, 8 * 256, &rs_totals)) || (rc = g_scr.get(41, 1, &rs_mask)) ||
-      (rc = g_scr.get(42, 8, &rs_ctr)))
+  uint32_t *rs_tables;
+  if ((rc = g_scr.get(39, (size_t)256 * (rsort::tiles_of(N) + nb + 1), &rs_status)) ||
+      (rc = g_scr.get(40, (size_t)8 * 256 * std::max(nb, 1), &rs_totals)) || (rc = g_scr.get(41, 1, &rs_mask)) ||
+      (rc = g_scr.get(42, 8, &rs_ctr)) ||
+      (rc = g_scr.get(43, (size_t)4 * nb + rsort::tiles_of(N) + nb + 2, &rs_tables)))
     return rc;
   uint64_t *ks;   // the sorted pairs: keys_b / vals_b or keys_a / vals_a
   uint32_t *vs;
@@ -1044,7 +1047,22 @@ int sort_rotations(Block *d_blocks, const int *d_ids, int nb, int nslots, const 
   init_keys_kernel<<<grid_of(N), 256, 0, st>>>(d_blocks, block_of, d_rle, N, keys_a, vals_a);
   BZ_TRY(cudaGetLastError());
   size_t tb = t_all;
-  BZ_TRY(rsort::sort_pairs(keys_a, vals_a, keys_b, vals_b, N, 32 + bits_b, rs_status, rs_totals, rs_ctr, rs_mask, &ks, &vs, st));
+  // first sort: the pairs already lie in their blocks' ranges in block order,
+  // so each block's range is sorted by its 4-byte prefixes alone (segmented;
+  // the block-id passes of a global sort by (block, prefix) are not needed)
+  static const bool seg_first = getenv("PCBZ_RSORT_SEG") ? atoi(getenv("PCBZ_RSORT_SEG")) != 0 : true;
+  if (seg_first) {
+    std::vector<uint32_t> seg_base(nb), seg_n(nb);
+    for (int t = 0; t < nb; ++t) {
+      seg_base[t] = (uint32_t)blocks[ids[t]].base;
+      seg_n[t] = (uint32_t)blocks[ids[t]].n;
+    }
+    BZ_TRY(rsort::sort_pairs_segmented(keys_a, vals_a, keys_b, vals_b, N, 32, seg_base, seg_n, rs_tables, rs_status,
+                                       rs_totals, rs_ctr, rs_mask, &ks, &vs, st));
+  } else {
+    BZ_TRY(rsort::sort_pairs(keys_a, vals_a, keys_b, vals_b, N, 32 + bits_b, rs_status, rs_totals, rs_ctr, rs_mask,
+                             &ks, &vs, st));
+  }
   heads_kernel<<<grid_of(N), 256, 0, st>>>(ks, N, hd);
   head_pos_kernel<<<grid_of(N), 256, 0, st>>>(hd, nullptr, N, gs);
   tb = t_all;
@@ -1233,7 +1251,7 @@ int compress_jobs(const uint8_t *d_in, const int64_t *in_off, int njobs, uint8_t
     block_meta_kernel<<<nb, 256, 0, st>>>(d_rle, d_blocks, d_ids, d_acc);
     BZ_TRY(cudaGetLastError());
     // ---- B, C, D ---------------------------------------------------------------
-    if ((rc = sort_rotations(d_blocks, d_ids, nb, nslots, d_rle, (uint32_t)N, sa, st))) return rc;
+    if ((rc = sort_rotations(d_blocks, d_ids, nb, nslots, d_rle, (uint32_t)N, sa, blocks, ids, st))) return rc;
     // ---- C: MTF + zero-run coding --------------------------------------------
     {
       std::vector<uint32_t> seg0(nb + 1, 0);

@@ -19,6 +19,7 @@
 // (VERDICT r1 weak 7).
 #pragma once
 #include <cstdint>
+#include <vector>
 
 namespace pcbz {
 namespace rsort {
@@ -102,6 +103,46 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *wsum) 
   return pre + x - v;
 }
 
+// Optional segments (sort_pairs_segmented): tile -> segment, each segment's
+// first tile, element base and length.  A segment's pairs stay inside its
+// range [base, base + n) and are sorted there; digit totals are per segment.
+struct Segs {
+  const uint32_t *tile_seg = nullptr, *tile0 = nullptr, *base = nullptr, *n = nullptr;
+};
+
+struct TileRange {
+  uint32_t seg, q, begin, end;  // segment, tile index within it, element range of the segment
+};
+
+__device__ __forceinline__ TileRange tile_range(const Segs &sg, uint32_t tile, uint32_t n) {
+  TileRange r{0u, tile, 0u, n};
+  if (sg.tile_seg) {
+    r.seg = sg.tile_seg[tile];
+    r.q = tile - sg.tile0[r.seg];
+    r.begin = sg.base[r.seg];
+    r.end = r.begin + sg.n[r.seg];
+  }
+  return r;
+}
+
+// digit totals of the first window per segment: one CTA per tile
+__global__ void __launch_bounds__(kThreads) hist_seg_kernel(const uint64_t *__restrict__ keys, const Segs sg,
+                                                            int shift, uint32_t *__restrict__ totals) {
+  __shared__ uint32_t hc[256 * kHistCopies];
+  for (int i = threadIdx.x; i < 256 * kHistCopies; i += kThreads) hc[i] = 0;
+  __syncthreads();
+  const TileRange tr = tile_range(sg, blockIdx.x, 0u);
+  const uint32_t t0 = tr.begin + tr.q * kTile, t1 = min(t0 + (uint32_t)kTile, tr.end);
+  const uint32_t c = threadIdx.x & (kHistCopies - 1);
+  for (uint32_t i = t0 + threadIdx.x; i < t1; i += kThreads)
+    atomicAdd(&hc[((uint32_t)(keys[i] >> shift) & 255u) * kHistCopies + c], 1u);
+  __syncthreads();
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kHistCopies; ++j) s += hc[threadIdx.x * kHistCopies + j];
+  if (s) atomicAdd(&totals[tr.seg * 256 + threadIdx.x], s);
+}
+
 // One pass: tiles take ids in launch order (atomic counter), rank their
 // pairs, publish per-digit tile counts (AGGREGATE), look back over earlier
 // tiles' published words until an INCLUSIVE prefix, publish their own
@@ -117,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(const uint64_t *_
                                                             int shift, const uint32_t *__restrict__ totals,
                                                             unsigned long long *status, uint32_t *tile_ctr,
                                                             uint32_t epoch, int next_shift,
-                                                            uint32_t *__restrict__ next_totals) {
+                                                            uint32_t *__restrict__ next_totals, const Segs sg) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t *sk = reinterpret_cast<uint64_t *>(smem);
   uint32_t *sv = reinterpret_cast<uint32_t *>(sk + kTile);
@@ -133,7 +174,11 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(const uint64_t *_
   nh[threadIdx.x] = 0;
   __syncthreads();
   const uint32_t tile = s_tile;
-  const uint32_t tile0 = tile * kTile;
+  const TileRange tr = tile_range(sg, tile, n);
+  n = tr.end;  // elements at or past the segment's end are not this tile's
+  totals += tr.seg * 256;
+  if (next_totals) next_totals += tr.seg * 256;
+  const uint32_t tile0 = tr.begin + tr.q * kTile;
   const uint32_t base = tile0 + w * kWarpSpan;
   const uint32_t lt = (1u << lane) - 1u;
   uint64_t k[kItems];
@@ -167,12 +212,12 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(const uint64_t *_
   }
   volatile unsigned long long *st = status;
   const unsigned long long tag = (unsigned long long)epoch << 34;
-  st[(size_t)tile * 256 + dd] = tag | (tile ? 1ull << 32 : 2ull << 32) | cnt;
-  const uint32_t dstart = block_excl_scan(totals[dd], wsum);
+  st[(size_t)tile * 256 + dd] = tag | (tr.q ? 1ull << 32 : 2ull << 32) | cnt;
+  const uint32_t dstart = tr.begin + block_excl_scan(totals[dd], wsum);
   tile_start[dd] = block_excl_scan(cnt, wsum);
   uint32_t excl = 0;
-  if (tile) {
-    for (int64_t t = (int64_t)tile - 1; t >= 0;) {
+  if (tr.q) {  // the segment's first tile publishes its inclusive prefix at once
+    for (int64_t t = (int64_t)tile - 1; t >= (int64_t)(tile - tr.q);) {
       const unsigned long long x = st[(size_t)t * 256 + dd];
       if ((x >> 34) != epoch) continue;  // not published yet in this pass
       excl += (uint32_t)x;
@@ -250,7 +295,84 @@ inline cudaError_t sort_pairs(uint64_t *ka, uint32_t *va, uint64_t *kb, uint32_t
     const bool last = p + 1 == win.n;
     onesweep_kernel<<<nt, kThreads, kScatterSmem, st>>>(ks, vs, kd, vd, n, win.shift[p], totals + 256 * p, status,
                                                         ctr + p, (uint32_t)p + 1, last ? 0 : win.shift[p + 1],
-                                                        last ? nullptr : totals + 256 * (p + 1));
+                                                        last ? nullptr : totals + 256 * (p + 1), Segs{});
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    std::swap(ks, kd);
+    std::swap(vs, vd);
+  }
+  *kres = ks;
+  *vres = vs;
+  return cudaSuccess;
+}
+
+// Segmented variant: sort each segment's pairs by key bits [0, end_bit) inside
+// its own range.  Segments are contiguous, in order, and cover [0, n); the
+// host tables (seg_base / seg_n per segment) are uploaded into `tables`
+// (4 * nseg + 2 * ntiles u32 of device scratch, ntiles = sum of tiles_of(seg_n)).
+// totals: 8 * nseg * 256 u32; status: 256 * ntiles u64.
+inline cudaError_t sort_pairs_segmented(uint64_t *ka, uint32_t *va, uint64_t *kb, uint32_t *vb, uint32_t n,
+                                        int end_bit, const std::vector<uint32_t> &seg_base,
+                                        const std::vector<uint32_t> &seg_n, uint32_t *tables,
+                                        unsigned long long *status, uint32_t *totals, uint32_t *ctr,
+                                        unsigned long long *d_mask, uint64_t **kres, uint32_t **vres,
+                                        cudaStream_t st) {
+  *kres = ka;
+  *vres = va;
+  const uint32_t nseg = (uint32_t)seg_base.size();
+  if (n < 2 || nseg == 0) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kScatterSmem);
+  if (e != cudaSuccess) return e;
+  std::vector<uint32_t> host(2 * nseg);  // tile0, then per-tile segment
+  uint32_t nt = 0;
+  for (uint32_t j = 0; j < nseg; ++j) {
+    host[j] = nt;
+    nt += tiles_of(seg_n[j]);
+  }
+  host.resize(2 * nseg + nt);
+  for (uint32_t j = 0; j < nseg; ++j)
+    for (uint32_t t = host[j]; t < host[j] + tiles_of(seg_n[j]); ++t) host[2 * nseg + t] = j;
+  std::copy(seg_base.begin(), seg_base.end(), host.begin() + nseg);
+  Segs sg;
+  sg.tile0 = tables;
+  sg.base = tables + nseg;
+  sg.tile_seg = tables + 2 * nseg;
+  sg.n = tables + 2 * nseg + nt;
+  if ((e = cudaMemcpyAsync(tables, host.data(), host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st)) !=
+      cudaSuccess)
+    return e;
+  if ((e = cudaMemcpyAsync(tables + 2 * nseg + nt, seg_n.data(), nseg * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                           st)) != cudaSuccess)
+    return e;
+  if ((e = cudaMemsetAsync(d_mask, 0, sizeof(unsigned long long), st)) != cudaSuccess) return e;
+  const int g = (int)std::min<uint32_t>((n + 255) / 256, 148u * 8u);
+  vary_kernel<<<g, 256, 0, st>>>(ka, n, d_mask);
+  unsigned long long mask = 0;
+  if ((e = cudaMemcpyAsync(&mask, d_mask, sizeof mask, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;  // also keeps `host` alive for the upload
+  if (end_bit < 64) mask &= (1ull << end_bit) - 1ull;
+  Windows win{};
+  for (int shift = 0; shift < 64 && (mask >> shift);) {
+    if (((mask >> shift) & 255u) == 0) {
+      shift += __builtin_ctzll(mask >> shift);
+      continue;
+    }
+    win.shift[win.n++] = shift;
+    shift += 8;
+  }
+  if (win.n == 0) return cudaSuccess;
+  const size_t per_window = (size_t)nseg * 256;
+  if ((e = cudaMemsetAsync(totals, 0, 8 * per_window * sizeof(uint32_t), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(ctr, 0, 8 * sizeof(uint32_t), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(status, 0, (size_t)nt * 256 * sizeof(unsigned long long), st)) != cudaSuccess) return e;
+  hist_seg_kernel<<<nt, kThreads, 0, st>>>(ka, sg, win.shift[0], totals);
+  uint64_t *ks = ka, *kd = kb;
+  uint32_t *vs = va, *vd = vb;
+  for (int p = 0; p < win.n; ++p) {
+    const bool last = p + 1 == win.n;
+    onesweep_kernel<<<nt, kThreads, kScatterSmem, st>>>(ks, vs, kd, vd, n, win.shift[p], totals + per_window * p,
+                                                        status, ctr + p, (uint32_t)p + 1,
+                                                        last ? 0 : win.shift[p + 1],
+                                                        last ? nullptr : totals + per_window * (p + 1), sg);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     std::swap(ks, kd);
     std::swap(vs, vd);
